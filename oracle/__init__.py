@@ -1,0 +1,6 @@
+"""CPU fp64 oracle — TEST INFRASTRUCTURE ONLY.
+
+May be imported only by tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs.  Shares no code with the CUDA path.
+"""
+from . import ref_attention, flops  # noqa: F401

@@ -1,0 +1,267 @@
+"""CPU fp64 oracle for the FlashAttention-2 hot path.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this
+module.  The product path (``paper_2307_08691_b200``) never imports it, and it
+imports nothing from the product path: the two share no code.
+
+What it computes is the *plain definition* of exact softmax attention, not the
+tiled algorithm: FlashAttention-2 is exact ("with no approximation", PAPER.md
+P:16), so the oracle materialises S and P in full.
+
+Citations are PAPER.md line numbers (P:n) and SPEC.md line numbers (S:n) in
+``/root/reference``.  Readings of garbled or silent passages are listed in
+DESIGN.md §3 ("Readings"); the ones used here are referenced as R<n>.
+
+Conventions (R1, R2, R8, R10):
+  * q, k, v, do are float arrays of shape [B, H, N, d] (or [N, d] for the
+    per-head functions); they are upcast to float64 before any arithmetic.
+  * ``scale`` multiplies QK^T before the softmax (P:160-162 footnote; read as
+    1/sqrt(d) by default, R1).  The caller passes the exact value the kernel
+    receives (a float32), and it is used as float64(float32(scale)).
+  * causal: S_ij = -inf for j > i, top-left aligned, N_q = N_k.
+  * L is the natural-log logsumexp of the *scaled* logits.
+
+Pins: every function here is checked by ``tests/test_oracle.py`` against
+values the paper/spec print, closed forms, invariants and finite differences
+(DESIGN.md §4).  No function in this file is "parity unpinned".
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+__all__ = [
+    "as_f64_scale",
+    "scores",
+    "softmax_rows",
+    "forward_head",
+    "forward",
+    "softmax_backward_row",
+    "backward_head",
+    "backward",
+    "rowsum_dO_O",
+    "forward_rows",
+    "backward_sampled_head",
+]
+
+
+def as_f64_scale(scale: float) -> float:
+    """The exact softmax scale the kernel receives (a float32), as float64 (R1)."""
+    return float(np.float32(scale))
+
+
+# ---------------------------------------------------------------------------
+# Forward: standard attention
+# ---------------------------------------------------------------------------
+
+def scores(q: np.ndarray, k: np.ndarray, scale: float, causal: bool) -> np.ndarray:
+    """S = scale * Q K^T  (scale per footnote P:160-162),
+    with S_ij = -inf for j > i when causal."""
+    q = np.asarray(q, dtype=np.float64)
+    k = np.asarray(k, dtype=np.float64)
+    s = as_f64_scale(scale) * (q @ k.T)
+    if causal:
+        n_q, n_k = s.shape
+        if n_q != n_k:
+            raise ValueError("causal attention is defined here for N_q == N_k only (R8)")
+        s[np.triu_indices(n_q, k=1)] = -np.inf
+    return s
+
+
+def softmax_rows(s: np.ndarray):
+    """Row-wise softmax of P:158 written out as in P:225-227:
+    m_i = max_j S_ij, E = exp(S - m), l_i = sum_j E_ij, P = E / l.
+    Returns (P, m, l)."""
+    m = np.max(s, axis=1)
+    e = np.exp(s - m[:, None])
+    ell = np.sum(e, axis=1)
+    p = e / ell[:, None]
+    return p, m, ell
+
+
+def forward_head(q, k, v, scale: float, causal: bool):
+    """One (b, h) head.  O = softmax(S) V; L = m + log(l).
+
+    Returns (O [N,d], L [N]) in float64."""
+    v = np.asarray(v, dtype=np.float64)
+    s = scores(q, k, scale, causal)
+    p, m, ell = softmax_rows(s)
+    o = p @ v
+    lse = m + np.log(ell)
+    return o, lse
+
+
+def forward(q, k, v, scale: float, causal: bool):
+    """Batched [B, H, N, d]: the same computation per head, in parallel over
+    batch and heads.  Returns (O [B,H,N,d], L [B,H,N]) float64."""
+    q = np.asarray(q)
+    b, h, n, d = q.shape
+    o = np.empty((b, h, n, d), dtype=np.float64)
+    lse = np.empty((b, h, n), dtype=np.float64)
+    for bi in range(b):
+        for hi in range(h):
+            o[bi, hi], lse[bi, hi] = forward_head(q[bi, hi], k[bi, hi], v[bi, hi], scale, causal)
+    return o, lse
+
+
+# ---------------------------------------------------------------------------
+# Backward: standard attention backward
+# ---------------------------------------------------------------------------
+
+def softmax_backward_row(p: np.ndarray, dp: np.ndarray) -> np.ndarray:
+    """ds = (diag(p) - p p^T) dp, written as the matrix product."""
+    p = np.asarray(p, dtype=np.float64)
+    dp = np.asarray(dp, dtype=np.float64)
+    if p.shape != dp.shape or p.ndim != 1:
+        raise ValueError("p and dp must be vectors of equal length")
+    jac = np.diag(p) - np.outer(p, p)
+    return jac @ dp
+
+
+def backward_head(q, k, v, do, scale: float, causal: bool):
+    """One head of the standard backward, with the softmax scale
+    carried by dS (R1):
+
+        dV = P^T dO
+        dP = dO V^T
+        dS = dsoftmax(dP), row-wise
+           = P o (dP - D 1^T),  D_i = sum_j P_ij dP_ij   (Jacobian form)
+        dQ = scale * dS K
+        dK = scale * dS^T Q
+
+    D is computed in the Jacobian form (rowsum(P o dP)), deliberately NOT as
+    rowsum(dO o O), so that the identity between the two is a check.
+    Returns (dQ, dK, dV, D) in float64.
+    """
+    q = np.asarray(q, dtype=np.float64)
+    k = np.asarray(k, dtype=np.float64)
+    v = np.asarray(v, dtype=np.float64)
+    do = np.asarray(do, dtype=np.float64)
+    s = scores(q, k, scale, causal)
+    p, _, _ = softmax_rows(s)
+    dv = p.T @ do
+    dp = do @ v.T
+    dd = np.sum(p * dp, axis=1)
+    ds = p * (dp - dd[:, None])
+    sc = as_f64_scale(scale)
+    dq = sc * (ds @ k)
+    dk = sc * (ds.T @ q)
+    return dq, dk, dv, dd
+
+
+def backward(q, k, v, do, scale: float, causal: bool):
+    """Batched [B,H,N,d] backward.  Returns (dQ, dK, dV, D) float64."""
+    q = np.asarray(q)
+    b, h, n, d = q.shape
+    dq = np.empty((b, h, n, d))
+    dk = np.empty((b, h, n, d))
+    dv = np.empty((b, h, n, d))
+    dd = np.empty((b, h, n))
+    for bi in range(b):
+        for hi in range(h):
+            dq[bi, hi], dk[bi, hi], dv[bi, hi], dd[bi, hi] = backward_head(
+                q[bi, hi], k[bi, hi], v[bi, hi], do[bi, hi], scale, causal)
+    return dq, dk, dv, dd
+
+
+def rowsum_dO_O(o, do) -> np.ndarray:
+    """D = rowsum(dO o O)  (Alg. 2 line 4; D has length N, R5).
+    Works on [..., N, d] arrays; returns [..., N] float64."""
+    o = np.asarray(o, dtype=np.float64)
+    do = np.asarray(do, dtype=np.float64)
+    return np.sum(do * o, axis=-1)
+
+
+# ---------------------------------------------------------------------------
+# Large-N variants: the same per-row definitions, evaluated row by row
+# (O(N) memory per row instead of materialising N x N).  Each output row is
+# computed by exactly the formulas above; rows are independent,
+# so evaluating a chunk of rows at a time reorders nothing within a row.
+# ---------------------------------------------------------------------------
+
+def _row_chunks(n: int, rows_per_chunk: int):
+    for r0 in range(0, n, rows_per_chunk):
+        yield r0, min(n, r0 + rows_per_chunk)
+
+
+def _row_scores(q_rows, row_idx, k, scale, causal):
+    s = as_f64_scale(scale) * (q_rows @ k.T)
+    if causal:
+        cols = np.arange(k.shape[0])
+        s[cols[None, :] > np.asarray(row_idx)[:, None]] = -np.inf
+    return s
+
+
+def forward_rows(q, k, v, scale: float, causal: bool, rows=None, rows_per_chunk: int = 256):
+    """O and L for the given rows of one head (default: all rows), using the
+    definitions of ``forward_head`` row by row.  Returns (rows, O[rows], L[rows])."""
+    q = np.asarray(q, dtype=np.float64)
+    k = np.asarray(k, dtype=np.float64)
+    v = np.asarray(v, dtype=np.float64)
+    n = q.shape[0]
+    rows = np.arange(n) if rows is None else np.asarray(rows)
+    o = np.empty((len(rows), v.shape[1]))
+    lse = np.empty(len(rows))
+    for a, b in _row_chunks(len(rows), rows_per_chunk):
+        idx = rows[a:b]
+        s = _row_scores(q[idx], idx, k, scale, causal)
+        p, m, ell = softmax_rows(s)
+        o[a:b] = p @ v
+        lse[a:b] = m + np.log(ell)
+    return rows, o, lse
+
+
+def backward_sampled_head(q, k, v, do, scale: float, causal: bool, dq_rows, dkv_cols,
+                          rows_per_chunk: int = 256):
+    """Sampled backward for one head at large N (same definition as
+    ``backward_head``):
+
+      pass 1 (all rows i): L_i and D_i = sum_j P_ij dP_ij (Jacobian form);
+      dQ_i = scale * sum_j P_ij (dP_ij - D_i) K_j          for i in dq_rows;
+      dV_j = sum_i P_ij dO_i,  dK_j = scale * sum_i dS_ij Q_i   for j in dkv_cols.
+
+    Returns dict with keys rows, dq, cols, dk, dv, lse (all rows), D (all rows).
+    """
+    q = np.asarray(q, dtype=np.float64)
+    k = np.asarray(k, dtype=np.float64)
+    v = np.asarray(v, dtype=np.float64)
+    do = np.asarray(do, dtype=np.float64)
+    n = q.shape[0]
+    sc = as_f64_scale(scale)
+    lse = np.empty(n)
+    dd = np.empty(n)
+    for a, b in _row_chunks(n, rows_per_chunk):
+        idx = np.arange(a, b)
+        s = _row_scores(q[a:b], idx, k, scale, causal)
+        p, m, ell = softmax_rows(s)
+        lse[a:b] = m + np.log(ell)
+        dp = do[a:b] @ v.T
+        dd[a:b] = np.sum(p * dp, axis=1)
+    dq_rows = np.asarray(dq_rows)
+    s = _row_scores(q[dq_rows], dq_rows, k, scale, causal)
+    p = np.exp(s - lse[dq_rows][:, None])
+    dp = do[dq_rows] @ v.T
+    ds = p * (dp - dd[dq_rows][:, None])
+    dq = sc * (ds @ k)
+    # columns j: P_ij for all rows i, from L (P = exp(S - L), Alg. 2 line 11)
+    dkv_cols = np.asarray(dkv_cols)
+    st = sc * (k[dkv_cols] @ q.T)                      # [cols, N] = S^T for sampled cols
+    if causal:
+        st[np.arange(n)[None, :] < dkv_cols[:, None]] = -np.inf
+    pt = np.exp(st - lse[None, :])
+    dv = pt @ do
+    dpt = v[dkv_cols] @ do.T
+    dst = pt * (dpt - dd[None, :])
+    dk = sc * (dst @ q)
+    return {"rows": dq_rows, "dq": dq, "cols": dkv_cols, "dk": dk, "dv": dv,
+            "lse": lse, "D": dd}
+
+
+def naive_softmax_no_max(s: np.ndarray) -> np.ndarray:
+    """softmax WITHOUT the max subtraction, used only by the overflow test
+     to show why m is tracked."""
+    with np.errstate(over="ignore", invalid="ignore"):
+        e = np.exp(s)
+        return e / np.sum(e, axis=1, keepdims=True)
