@@ -1,0 +1,116 @@
+/*
+ * fa2.h — C ABI of the B200 (sm_100a) FlashAttention-2 hot path.
+ *
+ * The operation (PAPER.md = /root/reference/PAPER.md, cited P:<line>):
+ *   For every batch b < B and head h < H (computed independently),
+ *   with Q, K, V in R^{N x d}:
+ *     S = softmax_scale * Q K^T   (scale per footnote P:160-162)
+ *     causal: S_ij = -inf for j > i, top-left aligned, N_q = N_k
+ *     P = rowwise softmax(S), O = P V
+ *     L_i = m_i + log(l_i) = log sum_j exp(S_ij)  (natural log)
+ *   Backward (Alg. 2):
+ *     D_i = rowsum(dO o O)_i
+ *     P_ij = exp(S_ij - L_i)
+ *     dV = P^T dO, dP = dO V^T, dS = P o (dP - D_i)
+ *     dQ = softmax_scale * dS K,  dK = softmax_scale * dS^T Q
+ *
+ * Layout: q, k, v, o, dout, dq, dk, dv are DEVICE pointers to contiguous
+ *   row-major [B, H, N, d] tensors of `dtype` (each head's N x d matrix is
+ *   contiguous).  lse is a DEVICE pointer to [B, H, N] float32.
+ * Alignment: every tensor pointer must be 16-byte aligned (TMA).
+ * Supported: d in {64, 128}; dtype FA2_BF16 or FA2_FP16; N >= 1 (any N, ragged
+ *   tails are masked); B, H >= 1; B*H <= 2^31-1; softmax_scale finite and > 0.
+ * Ownership: the caller owns every buffer; the library never allocates device
+ *   memory.  Inputs are read-only.  o and lse written by fa2_forward are inputs
+ *   of fa2_backward and must not be modified in between.
+ * Streams: `stream` is a cudaStream_t (0 = legacy default stream).  Calls are
+ *   asynchronous with respect to the host; no host synchronisation happens
+ *   inside the device-pointer entry points.  The library keeps no global mutable
+ *   state besides a per-thread error-detail string, so calls are reentrant.
+ * Errors: argument errors are detected before anything is launched and are
+ *   returned synchronously (nothing is launched).  Launch failures return
+ *   FA2_ERR_CUDA; fa2_last_error_detail() describes the last failure of the
+ *   calling thread.  Asynchronous kernel faults surface at the caller's next
+ *   synchronisation, as with any CUDA library.
+ */
+#ifndef FA2_H_
+#define FA2_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FA2_API __attribute__((visibility("default")))
+#else
+#define FA2_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { FA2_BF16 = 0, FA2_FP16 = 1 } fa2_dtype_t;
+
+typedef enum {
+  FA2_OK = 0,
+  FA2_ERR_INVALID_ARG = 1, /* null pointer, B/H/N < 1, scale not finite or <= 0, misaligned pointer */
+  FA2_ERR_UNSUPPORTED = 2, /* d not in {64,128}, dtype unknown, device is not sm_100 */
+  FA2_ERR_WORKSPACE = 3,   /* workspace null or smaller than fa2_backward_workspace_size() */
+  FA2_ERR_CUDA = 4         /* CUDA runtime/driver error; see fa2_last_error_detail() */
+} fa2_status_t;
+
+/* Forward pass, Alg. 1.  Writes o [B,H,N,d] (dtype) and lse [B,H,N]
+ * (fp32, natural log of the scaled logits). */
+FA2_API fa2_status_t fa2_forward(const void* q, const void* k, const void* v, void* o, float* lse,
+                         int B, int H, int N, int d, int causal, float softmax_scale,
+                         fa2_dtype_t dtype, void* stream);
+
+/* Bytes of device scratch fa2_backward needs: the fp32 dQ accumulator
+ * [B,H,N_pad,d] and D [B,H,N_pad] (fp32), N_pad = N rounded up to 128. */
+FA2_API size_t fa2_backward_workspace_size(int B, int H, int N, int d);
+
+/* Backward pass, Alg. 2: writes dq, dk, dv ([B,H,N,d], dtype).
+ * `workspace` is caller-owned device memory of at least
+ * fa2_backward_workspace_size(B,H,N,d) bytes, 16-byte aligned; its contents on
+ * entry are ignored (the library zeroes what it uses). */
+FA2_API fa2_status_t fa2_backward(const void* q, const void* k, const void* v, const void* o,
+                          const float* lse, const void* dout, void* dq, void* dk, void* dv,
+                          void* workspace, size_t workspace_bytes,
+                          int B, int H, int N, int d, int causal, float softmax_scale,
+                          fa2_dtype_t dtype, void* stream);
+
+/* D = rowsum(dO o O) alone, into d_out [B,H,N] fp32 (device).  Exposed
+ * so the preprocessing step can be checked on its own; fa2_backward runs it
+ * internally. */
+FA2_API fa2_status_t fa2_backward_preprocess(const void* o, const void* dout, float* d_out,
+                                     int B, int H, int N, int d, fa2_dtype_t dtype, void* stream);
+
+/* End-to-end step through HOST buffers: copies q,k,v,dout (pinned host memory
+ * recommended) to the device arena, runs fa2_forward then fa2_backward, and
+ * copies o, lse, dq, dk, dv back to host, all on `stream`; returns after the
+ * stream has been synchronised.  `arena` is caller-owned device memory of at
+ * least fa2_step_arena_size(B,H,N,d) bytes.  Host output pointers may be NULL
+ * to skip that copy. */
+FA2_API size_t fa2_step_arena_size(int B, int H, int N, int d);
+FA2_API fa2_status_t fa2_attention_step_host(const void* q_h, const void* k_h, const void* v_h, const void* dout_h,
+                                     void* o_h, float* lse_h, void* dq_h, void* dk_h, void* dv_h,
+                                     void* arena, size_t arena_bytes,
+                                     int B, int H, int N, int d, int causal, float softmax_scale,
+                                     fa2_dtype_t dtype, void* stream);
+
+/* Host-side tile map (no GPU needed), the grid logic of P:345-351, P:378-386:
+ * for query row block `i` of size Br, the number of key/value blocks of size Bc
+ * that are computed (n_blocks) and the first block index that needs the causal
+ * or ragged mask (first_masked; == n_blocks when none).  Returns FA2_OK or
+ * FA2_ERR_INVALID_ARG. */
+FA2_API fa2_status_t fa2_kv_block_range(int N, int Br, int Bc, int i, int causal, int* n_blocks, int* first_masked);
+
+FA2_API const char* fa2_status_string(fa2_status_t s);
+FA2_API const char* fa2_last_error_detail(void);
+/* Number of kernels the last successful fa2_forward / fa2_backward call launched. */
+FA2_API int fa2_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FA2_H_ */

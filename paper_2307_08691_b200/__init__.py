@@ -1,0 +1,175 @@
+"""B200 (sm_100a) FlashAttention-2 hot path — thin Python binding over the C ABI.
+
+Argument marshalling only: every step of the attention path runs in the CUDA
+kernels of ``libfa2_sm100.so`` (see include/fa2.h).  PyTorch supplies device
+memory and the current stream.  There is no CPU fallback: if the library is
+missing or the device is not sm_100, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+__all__ = ["lib", "forward", "backward", "backward_preprocess", "backward_workspace_size",
+           "attention_step_host", "step_arena_size", "kv_block_range", "FA2Error", "LIB_PATH"]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfa2_sm100.so")
+
+FA2_BF16, FA2_FP16 = 0, 1
+_STATUS = {0: "FA2_OK", 1: "FA2_ERR_INVALID_ARG", 2: "FA2_ERR_UNSUPPORTED", 3: "FA2_ERR_WORKSPACE", 4: "FA2_ERR_CUDA"}
+
+
+class FA2Error(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {detail}")
+        self.status = status
+        self.detail = detail
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libfa2_sm100.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise FA2Error(-1, f"{LIB_PATH} not built (run `python -c 'import __graft_entry__ as g; g.build()'`)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i, f, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_float, ctypes.c_size_t
+        L.fa2_forward.argtypes = [vp, vp, vp, vp, vp, i, i, i, i, i, f, i, vp]
+        L.fa2_forward.restype = i
+        L.fa2_backward.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, i, i, i, i, i, f, i, vp]
+        L.fa2_backward.restype = i
+        L.fa2_backward_preprocess.argtypes = [vp, vp, vp, i, i, i, i, i, vp]
+        L.fa2_backward_preprocess.restype = i
+        L.fa2_backward_workspace_size.argtypes = [i, i, i, i]
+        L.fa2_backward_workspace_size.restype = sz
+        L.fa2_step_arena_size.argtypes = [i, i, i, i]
+        L.fa2_step_arena_size.restype = sz
+        L.fa2_attention_step_host.argtypes = [vp] * 9 + [vp, sz, i, i, i, i, i, f, i, vp]
+        L.fa2_attention_step_host.restype = i
+        L.fa2_kv_block_range.argtypes = [i, i, i, i, i, ctypes.POINTER(i), ctypes.POINTER(i)]
+        L.fa2_kv_block_range.restype = i
+        L.fa2_status_string.argtypes = [i]
+        L.fa2_status_string.restype = ctypes.c_char_p
+        L.fa2_last_error_detail.argtypes = []
+        L.fa2_last_error_detail.restype = ctypes.c_char_p
+        L.fa2_last_launch_count.argtypes = []
+        L.fa2_last_launch_count.restype = i
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise FA2Error(status, lib().fa2_last_error_detail().decode())
+
+
+def _dtype_code(t) -> int:
+    import torch
+    if t.dtype == torch.bfloat16:
+        return FA2_BF16
+    if t.dtype == torch.float16:
+        return FA2_FP16
+    raise FA2Error(2, f"unsupported dtype {t.dtype}")
+
+
+def _stream(stream=None) -> int:
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def _shape(q):
+    if q.dim() != 4:
+        raise FA2Error(1, "expected [B, H, N, d] tensors")
+    return tuple(q.shape)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _need(t, like, name):
+    if t.shape != like.shape or t.dtype != like.dtype or not t.is_contiguous() or t.device != like.device:
+        raise FA2Error(1, f"{name} must be a contiguous {tuple(like.shape)} {like.dtype} tensor on {like.device}")
+
+
+def forward(q, k, v, causal: bool = False, softmax_scale: float | None = None, out=None, lse=None, stream=None):
+    """O, L for [B,H,N,d] bf16/fp16 CUDA tensors (Alg. 1).  Returns (o, lse[B,H,N] fp32)."""
+    import torch
+    B, H, N, d = _shape(q)
+    for t, n in ((k, "k"), (v, "v")):
+        _need(t, q, n)
+    if not q.is_contiguous():
+        raise FA2Error(1, "q must be contiguous")
+    scale = 1.0 / math.sqrt(d) if softmax_scale is None else float(softmax_scale)
+    o = torch.empty_like(q) if out is None else out
+    L = torch.empty((B, H, N), dtype=torch.float32, device=q.device) if lse is None else lse
+    _check(lib().fa2_forward(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(L), B, H, N, d, int(bool(causal)),
+                             scale, _dtype_code(q), ctypes.c_void_p(_stream(stream))))
+    return o, L
+
+
+def backward_workspace_size(B: int, H: int, N: int, d: int) -> int:
+    return int(lib().fa2_backward_workspace_size(B, H, N, d))
+
+
+def backward(q, k, v, o, lse, do, causal: bool = False, softmax_scale: float | None = None,
+             dq=None, dk=None, dv=None, workspace=None, stream=None):
+    """dQ, dK, dV (Alg. 2).  Returns (dq, dk, dv)."""
+    import torch
+    B, H, N, d = _shape(q)
+    for t, n in ((k, "k"), (v, "v"), (o, "o"), (do, "do")):
+        _need(t, q, n)
+    scale = 1.0 / math.sqrt(d) if softmax_scale is None else float(softmax_scale)
+    dq = torch.empty_like(q) if dq is None else dq
+    dk = torch.empty_like(k) if dk is None else dk
+    dv = torch.empty_like(v) if dv is None else dv
+    wsz = backward_workspace_size(B, H, N, d)
+    if workspace is None:
+        workspace = torch.empty(wsz, dtype=torch.uint8, device=q.device)
+    _check(lib().fa2_backward(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk),
+                              _ptr(dv), _ptr(workspace), workspace.numel() * workspace.element_size(),
+                              B, H, N, d, int(bool(causal)), scale, _dtype_code(q),
+                              ctypes.c_void_p(_stream(stream))))
+    return dq, dk, dv
+
+
+def backward_preprocess(o, do, stream=None):
+    """D = rowsum(dO o O), [B,H,N] fp32."""
+    import torch
+    B, H, N, d = _shape(o)
+    _need(do, o, "do")
+    out = torch.empty((B, H, N), dtype=torch.float32, device=o.device)
+    _check(lib().fa2_backward_preprocess(_ptr(o), _ptr(do), _ptr(out), B, H, N, d, _dtype_code(o),
+                                         ctypes.c_void_p(_stream(stream))))
+    return out
+
+
+def step_arena_size(B: int, H: int, N: int, d: int) -> int:
+    return int(lib().fa2_step_arena_size(B, H, N, d))
+
+
+def attention_step_host(q_h, k_h, v_h, do_h, outs, arena, causal: bool, softmax_scale: float | None = None,
+                        stream=None):
+    """One end-to-end fwd+bwd step through HOST (pinned) tensors.  `outs` is a
+    dict with optional host tensors o, lse, dq, dk, dv to receive results."""
+    B, H, N, d = _shape(q_h)
+    scale = 1.0 / math.sqrt(d) if softmax_scale is None else float(softmax_scale)
+    g = outs.get
+    _check(lib().fa2_attention_step_host(_ptr(q_h), _ptr(k_h), _ptr(v_h), _ptr(do_h), _ptr(g("o")),
+                                         _ptr(g("lse")), _ptr(g("dq")), _ptr(g("dk")), _ptr(g("dv")),
+                                         _ptr(arena), arena.numel() * arena.element_size(), B, H, N, d,
+                                         int(bool(causal)), scale, _dtype_code(q_h),
+                                         ctypes.c_void_p(_stream(stream))))
+
+
+def kv_block_range(N: int, Br: int, Bc: int, i: int, causal: bool):
+    """Host tile map: (n_blocks, first_masked) for query row block i."""
+    nb, fm = ctypes.c_int(0), ctypes.c_int(0)
+    _check(lib().fa2_kv_block_range(N, Br, Bc, i, int(bool(causal)), ctypes.byref(nb), ctypes.byref(fm)))
+    return nb.value, fm.value

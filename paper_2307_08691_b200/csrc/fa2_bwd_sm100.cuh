@@ -1,0 +1,494 @@
+// FlashAttention-2 backward pass (Alg. 2) for sm_100a.
+//
+//   fa2_bwd_preprocess : D_i = rowsum(dO o O)_i (Alg. 2 line 4),
+//                        L2_i = L_i * log2(e) (padded rows: +inf), zero dQ_acc.
+//   fa2_bwd_kernel     : one persistent CTA per SM; a work tile is one key/value
+//                        block K_j, V_j of 128 rows (the "column block" worker of
+//                        P:489-496); it walks the query blocks i (B_r rows):
+//       S^T   = K_j Q_i^T                   tcgen05 SS -> TMEM   (Alg. 2 l.10)
+//       dP^T  = V_j dO_i^T                  tcgen05 SS -> TMEM   (l.13)
+//       P^T   = exp(S^T - L_i)              (l.11, one thread = one key row)
+//       dS^T  = P^T o (dP^T - D_i)          (l.14, D_i broadcast per query row)
+//       dV_j += P^T dO_i                    tcgen05 SS, TMEM accumulator (l.12)
+//       dK_j += dS^T Q_i                    tcgen05 SS, TMEM accumulator (l.17)
+//       dQ_i += dS K_j                      tcgen05 SS -> TMEM -> fp32 TMA
+//                                           reduce-add into dQ_acc (l.15-16;
+//                                           the atomic add of P:494-496)
+//     dK_j, dV_j are written once at the end (l.19); the softmax scale is
+//     applied to dK and dQ (dS carries it, R1).
+//   fa2_dq_convert     : dQ = cast(dQ_acc).
+//
+// Orientation: key rows are TMEM lanes (M = 128).  For d = 128 the query block
+// is B_r = 64 and dQ is produced transposed (dQ^T = K^T dS^T, M = d = 128); for
+// d = 64, B_r = 128 and dQ = dS K (M = B_r = 128).  Both keep every MMA at
+// M = 128 and the TMEM budget at 448 of 512 columns.
+//
+// Warp roles (512 threads): warps 0-7 two compute warpgroups (each owns half of
+// the query columns of P^T / dS^T); warps 8-11 dQ readout + reduce-add; warp 12
+// MMA issuer; warp 13 TMA producer; warps 14-15 idle.
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
+#include "sm100_ptx.cuh"
+
+namespace fa2 {
+
+constexpr int kBwdThreads = 512;
+__host__ __device__ constexpr int bwd_bm(int d) { return d == 128 ? 64 : 128; }
+
+struct BwdMaps {
+  CUtensorMap q, k, v, dout, dq_acc;
+};
+
+struct BwdParams {
+  const float* lse;     // unused by the main kernel (L2 in workspace); kept for reference
+  const float* dvec;    // workspace: [BH, npad] D, followed by [BH, npad] L*log2(e)
+  void* dk;
+  void* dv;
+  int BH, N, npad;
+  int num_n_blocks;     // ceil(N / 128)
+  int num_tiles;        // BH * num_n_blocks
+  float scale;
+  float scale_log2;
+};
+
+// ---------------------------------------------------------------------------
+// Preprocess: one warp per row (rows of the padded [BH, npad] grid).
+//   dvec[r] = sum_c dO[r,c] * O[r,c]         (r < N)      else 0
+//   lse2[r] = L[r] * log2(e)                 (r < N)      else +inf
+//   dq_acc[r, :] = 0
+// When dq_acc == nullptr (fa2_backward_preprocess) only dvec is written and
+// npad == N, lse == nullptr.
+// ---------------------------------------------------------------------------
+template <int D, bool BF16>
+__global__ void __launch_bounds__(256)
+fa2_bwd_preprocess(const void* __restrict__ o, const void* __restrict__ dout, float* __restrict__ dvec,
+                   float* __restrict__ dq_acc, int BH, int N, int npad, const float* __restrict__ lse = nullptr,
+                   float* __restrict__ lse2 = nullptr) {
+  const long long row = static_cast<long long>(blockIdx.x) * 8 + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= static_cast<long long>(BH) * npad) return;
+  const int bh = static_cast<int>(row / npad);
+  const int r = static_cast<int>(row % npad);
+  constexpr int PER = D / 32;  // elements per lane (2 or 4)
+  float acc = 0.f;
+  if (r < N) {
+    const size_t base = (static_cast<size_t>(bh) * N + r) * D + lane * PER;
+    if constexpr (PER == 4) {
+      const uint2 a = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(o) + base);
+      const uint2 b = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(dout) + base);
+      const float2 a0 = ptx::unpack2<BF16>(a.x), a1 = ptx::unpack2<BF16>(a.y);
+      const float2 b0 = ptx::unpack2<BF16>(b.x), b1 = ptx::unpack2<BF16>(b.y);
+      acc = a0.x * b0.x + a0.y * b0.y + a1.x * b1.x + a1.y * b1.y;
+    } else {
+      const uint32_t a = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint16_t*>(o) + base);
+      const uint32_t b = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint16_t*>(dout) + base);
+      const float2 a0 = ptx::unpack2<BF16>(a), b0 = ptx::unpack2<BF16>(b);
+      acc = a0.x * b0.x + a0.y * b0.y;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  }
+  if (lane == 0) {
+    dvec[row] = acc;
+    if (lse2 != nullptr) lse2[row] = (r < N) ? lse[static_cast<size_t>(bh) * N + r] * 1.4426950408889634f : INFINITY;
+  }
+  if (dq_acc != nullptr) {
+    float4* z = reinterpret_cast<float4*>(dq_acc + row * D);
+    for (int c = lane; c < D / 4; c += 32) z[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+template <bool BF16>
+__global__ void __launch_bounds__(256)
+fa2_dq_convert(const float* __restrict__ dq_acc, void* __restrict__ dq, int BH, int N, int npad, int D) {
+  const long long i8 = static_cast<long long>(blockIdx.x) * 256 + threadIdx.x;  // index of 8-element group
+  const long long total8 = static_cast<long long>(BH) * N * D / 8;
+  if (i8 >= total8) return;
+  const long long e = i8 * 8;
+  const long long row = e / D;
+  const int c = static_cast<int>(e % D);
+  const int bh = static_cast<int>(row / N);
+  const int r = static_cast<int>(row % N);
+  const float4* src = reinterpret_cast<const float4*>(dq_acc + (static_cast<size_t>(bh) * npad + r) * D + c);
+  const float4 a = src[0], b = src[1];
+  uint4 out;
+  out.x = ptx::pack2<BF16>(a.x, a.y);
+  out.y = ptx::pack2<BF16>(a.z, a.w);
+  out.z = ptx::pack2<BF16>(b.x, b.y);
+  out.w = ptx::pack2<BF16>(b.z, b.w);
+  reinterpret_cast<uint4*>(dq)[i8] = out;
+}
+
+template <int D>
+struct BwdSmem {
+  static constexpr int BM = bwd_bm(D);
+  static constexpr int KV_TILE = 128 * D * 2;     // K_j or V_j
+  static constexpr int Q_TILE = BM * D * 2;       // Q_i or dO_i
+  static constexpr int Q_SUB = BM * 128;          // one 64-column swizzle box of a Q/dO tile
+  static constexpr int DS_TILE = 128 * BM * 2;    // P^T or dS^T (bf16)
+  static constexpr int DQ_TILE = BM * D * 4;      // fp32 staging for the dQ reduce-add
+  static constexpr int STAGES = 2;
+  static constexpr int OFF_K = 0;
+  static constexpr int OFF_V = OFF_K + KV_TILE;
+  static constexpr int OFF_Q = OFF_V + KV_TILE;
+  static constexpr int OFF_DO = OFF_Q + STAGES * Q_TILE;
+  static constexpr int OFF_PT = OFF_DO + STAGES * Q_TILE;
+  static constexpr int OFF_DST = OFF_PT + DS_TILE;
+  static constexpr int OFF_DQ = OFF_DST + DS_TILE;
+  static constexpr int OFF_VEC = OFF_DQ + DQ_TILE;                 // [STAGES][2][BM] floats: L2, D
+  static constexpr int OFF_BAR = OFF_VEC + STAGES * 2 * BM * 4;
+  // kv_full kv_empty q_full[2] q_empty[2] s_full s_consumed ds_ready ds_empty dq_full dq_empty dkv_full dkv_empty
+  static constexpr int NBAR = 14;
+  static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
+  static constexpr int BYTES = OFF_TMEM + 16;
+  static constexpr int ALLOC = BYTES + 1024;
+};
+
+template <int D, bool BF16, bool CAUSAL>
+__global__ void __launch_bounds__(kBwdThreads, 1)
+fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+               const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
+               const __grid_constant__ CUtensorMap tm_dq, const BwdParams p) {
+  using L = BwdSmem<D>;
+  constexpr int BM = L::BM;
+  constexpr bool DQT = (D == 128);          // dQ produced transposed
+  constexpr int NSUB = D / 64;
+  constexpr int HALF = BM / 2;               // query columns per compute warpgroup
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem + L::OFF_K;
+  uint8_t* sV = smem + L::OFF_V;
+  uint8_t* sQ = smem + L::OFF_Q;
+  uint8_t* sDO = smem + L::OFF_DO;
+  uint8_t* sPT = smem + L::OFF_PT;
+  uint8_t* sDST = smem + L::OFF_DST;
+  uint8_t* sDQ = smem + L::OFF_DQ;
+  float* sVec = reinterpret_cast<float*>(smem + L::OFF_VEC);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint64_t* kv_full = bars + 0;
+  uint64_t* kv_empty = bars + 1;
+  uint64_t* q_full = bars + 2;    // [2]
+  uint64_t* q_empty = bars + 4;   // [2]
+  uint64_t* s_full = bars + 6;
+  uint64_t* s_consumed = bars + 7;
+  uint64_t* ds_ready = bars + 8;
+  uint64_t* ds_empty = bars + 9;
+  uint64_t* dq_full = bars + 10;
+  uint64_t* dq_empty = bars + 11;
+  uint64_t* dkv_full = bars + 12;
+  uint64_t* dkv_empty = bars + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(kv_full, 1);
+    ptx::mbar_init(kv_empty, 1);
+    for (int s = 0; s < 2; ++s) { ptx::mbar_init(&q_full[s], 1); ptx::mbar_init(&q_empty[s], 1); }
+    ptx::mbar_init(s_full, 1);
+    ptx::mbar_init(s_consumed, 8);
+    ptx::mbar_init(ds_ready, 8);
+    ptx::mbar_init(ds_empty, 1);
+    ptx::mbar_init(dq_full, 1);
+    ptx::mbar_init(dq_empty, 4);
+    ptx::mbar_init(dkv_full, 1);
+    ptx::mbar_init(dkv_empty, 8);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 13 && lane == 0) {
+    ptx::tma_prefetch_desc(&tm_q); ptx::tma_prefetch_desc(&tm_k); ptx::tma_prefetch_desc(&tm_v);
+    ptx::tma_prefetch_desc(&tm_do); ptx::tma_prefetch_desc(&tm_dq);
+  }
+  if (warp == 0) ptx::tmem_alloc(tmem_slot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t T_ST = 0, T_DPT = BM, T_DV = 2 * BM, T_DK = 2 * BM + D, T_DQ = 2 * BM + 2 * D;
+
+  const int N = p.N;
+  const int n_q_blocks = (N + BM - 1) / BM;
+  const float* gD = p.dvec;
+  const float* gL2 = p.dvec + static_cast<size_t>(p.BH) * p.npad;
+
+  // tile t -> (bh, n_block); heavy (low n_block) first for causal
+  auto decode = [&](int t, int& bh, int& nb) { bh = t / p.num_n_blocks; nb = t % p.num_n_blocks; };
+  auto q_begin = [&](int nb) -> int { return CAUSAL ? (nb * 128) / BM : 0; };
+
+  if (warp < 8) {
+    // ====================== compute warpgroups: P^T, dS^T ======================
+    const int wg = warp / 4;
+    const int r = threadIdx.x % 128;                   // key row within the block == TMEM lane
+    const uint32_t lane_base = static_cast<uint32_t>((warp % 4) * 32) << 16;
+    uint32_t g = 0;          // global query-tile counter
+    int it = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+      int bh, nb;
+      decode(t, bh, nb);
+      const int kv_row = nb * 128 + r;
+      const int i0 = q_begin(nb);
+      for (int i = i0; i < n_q_blocks; ++i, ++g) {
+        const int slot = g & 1;
+        ptx::mbar_wait(&q_full[slot], (g >> 1) & 1);
+        ptx::mbar_wait(s_full, g & 1);
+        ptx::tc_fence_after();
+        const float* vL2 = sVec + slot * 2 * BM;
+        const float* vD = vL2 + BM;
+        const bool need_mask = (CAUSAL && (i * BM < nb * 128 + 128)) || (nb * 128 + 128 > N);
+        // wait until the previous tile's dV/dK/dQ MMAs have read P^T / dS^T
+        if (g > 0) ptx::mbar_wait(ds_empty, (g - 1) & 1);
+#pragma unroll
+        for (int ch = 0; ch < HALF / 32; ++ch) {
+          const int c0 = wg * HALF + ch * 32;          // first query column of this chunk
+          uint32_t sv[32], dpv[32];
+          ptx::tmem_ld_x32(tmem + lane_base + T_ST + c0, sv);
+          ptx::tmem_ld_x32(tmem + lane_base + T_DPT + c0, dpv);
+          ptx::tmem_wait_ld();
+          uint32_t pk[16], dk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            float pp[2], dd[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int c = c0 + 2 * e + h;
+              float pv = ptx::ex2(fmaf(__uint_as_float(sv[2 * e + h]), p.scale_log2, -vL2[c]));
+              if (need_mask) {
+                const int q_row = i * BM + c;
+                if ((CAUSAL && kv_row > q_row) || kv_row >= N) pv = 0.f;
+              }
+              pp[h] = pv;
+              dd[h] = pv * (__uint_as_float(dpv[2 * e + h]) - vD[c]);
+            }
+            pk[e] = ptx::pack2<BF16>(pp[0], pp[1]);
+            dk[e] = ptx::pack2<BF16>(dd[0], dd[1]);
+          }
+          // write 32 columns (64 bytes = 4 x 16-B chunks) of row r, 128-B swizzle
+          const int region = c0 / 64;                    // 64-column (128-B) region
+          const int cc0 = (c0 % 64) / 8;                 // first 16-B chunk within the 128-B row
+          uint8_t* rowP = sPT + region * (128 * 128) + (r / 8) * 1024 + (r % 8) * 128;
+          uint8_t* rowS = sDST + region * (128 * 128) + (r / 8) * 1024 + (r % 8) * 128;
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const int chunk = (cc0 + q4) ^ (r % 8);
+            *reinterpret_cast<uint4*>(rowP + chunk * 16) = make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
+            *reinterpret_cast<uint4*>(rowS + chunk * 16) = make_uint4(dk[4 * q4], dk[4 * q4 + 1], dk[4 * q4 + 2], dk[4 * q4 + 3]);
+          }
+        }
+        // S^T / dP^T fully read (tcgen05.wait::ld above) -> MMA may overwrite them
+        ptx::tc_fence_before();
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) { ptx::mbar_arrive(s_consumed); ptx::mbar_arrive(ds_ready); }
+      }
+      // ---- epilogue: dV_j (warpgroup 0), dK_j * scale (warpgroup 1) ----
+      ptx::mbar_wait(dkv_full, it & 1);
+      ptx::tc_fence_after();
+      {
+        const uint32_t tsrc = tmem + lane_base + (wg == 0 ? T_DV : T_DK);
+        const float mul = wg == 0 ? 1.f : p.scale;
+        uint8_t* dst = reinterpret_cast<uint8_t*>(wg == 0 ? p.dv : p.dk) + (static_cast<size_t>(bh) * N + kv_row) * (D * 2);
+#pragma unroll
+        for (int ch = 0; ch < D / 32; ++ch) {
+          uint32_t v[32];
+          ptx::tmem_ld_x32(tsrc + ch * 32, v);
+          ptx::tmem_wait_ld();
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) pk[e] = ptx::pack2<BF16>(__uint_as_float(v[2 * e]) * mul, __uint_as_float(v[2 * e + 1]) * mul);
+          if (kv_row < N) {
+            uint4* o = reinterpret_cast<uint4*>(dst + ch * 64);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) o[e] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(dkv_empty);
+    }
+  } else if (warp < 12) {
+    // ====================== dQ readout + fp32 reduce-add ======================
+    const int r = threadIdx.x - 256;                    // 0..127 == TMEM lane
+    const uint32_t lane_base = static_cast<uint32_t>((warp % 4) * 32) << 16;
+    const bool leader = (r == 0);
+    uint32_t g = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      int bh, nb;
+      decode(t, bh, nb);
+      const int i0 = q_begin(nb);
+      for (int i = i0; i < n_q_blocks; ++i, ++g) {
+        ptx::mbar_wait(dq_full, g & 1);
+        ptx::tc_fence_after();
+        // staging buffer free? (previous reduce-add has finished reading it)
+        if (leader) ptx::bulk_wait_read<0>();
+        ptx::named_bar_sync(1, 128);
+        if constexpr (DQT) {
+          // TMEM lane r = head-dim column d, columns = 64 query rows
+#pragma unroll
+          for (int ch = 0; ch < BM / 32; ++ch) {
+            uint32_t v[32];
+            ptx::tmem_ld_x32(tmem + lane_base + T_DQ + ch * 32, v);
+            ptx::tmem_wait_ld();
+            const int dcol = r;
+            uint8_t* box = sDQ + (dcol / 32) * (BM * 128);
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              const int q = ch * 32 + e;
+              const int chunk = ((dcol % 32) / 4) ^ (q % 8);
+              *reinterpret_cast<float*>(box + q * 128 + chunk * 16 + (dcol % 4) * 4) = __uint_as_float(v[e]) * p.scale;
+            }
+          }
+        } else {
+          // TMEM lane r = query row, 64 columns = head dim
+#pragma unroll
+          for (int ch = 0; ch < D / 32; ++ch) {
+            uint32_t v[32];
+            ptx::tmem_ld_x32(tmem + lane_base + T_DQ + ch * 32, v);
+            ptx::tmem_wait_ld();
+            uint8_t* row = sDQ + ch * (BM * 128) + r * 128;
+#pragma unroll
+            for (int c4 = 0; c4 < 8; ++c4) {
+              const int chunk = c4 ^ (r % 8);
+              *reinterpret_cast<float4*>(row + chunk * 16) =
+                  make_float4(__uint_as_float(v[4 * c4]) * p.scale, __uint_as_float(v[4 * c4 + 1]) * p.scale,
+                              __uint_as_float(v[4 * c4 + 2]) * p.scale, __uint_as_float(v[4 * c4 + 3]) * p.scale);
+            }
+          }
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(dq_empty);
+        ptx::fence_proxy_async_smem();
+        ptx::named_bar_sync(1, 128);
+        if (leader) {
+#pragma unroll
+          for (int b = 0; b < D / 32; ++b) ptx::tma_reduce_add_3d(&tm_dq, sDQ + b * (BM * 128), b * 32, i * BM, bh);
+          ptx::bulk_commit();
+        }
+      }
+    }
+    if (leader) ptx::bulk_wait<0>();
+  } else if (warp == 12) {
+    // ============================ MMA issuer ============================
+    if (lane == 0) {
+      constexpr uint32_t IDESC_S = ptx::idesc_f16(BF16, 128, BM, false, false);   // S^T, dP^T
+      constexpr uint32_t IDESC_G = ptx::idesc_f16(BF16, 128, D, false, true);     // dV, dK
+      constexpr uint32_t IDESC_Q = ptx::idesc_f16(BF16, 128, 64, true, true);     // dQ^T or dQ
+      const uint32_t aK = ptx::smem_u32(sK), aV = ptx::smem_u32(sV);
+      const uint32_t aQ = ptx::smem_u32(sQ), aDO = ptx::smem_u32(sDO);
+      const uint32_t aPT = ptx::smem_u32(sPT), aDST = ptx::smem_u32(sDST);
+      uint32_t g = 0;
+      int it = 0;
+      uint32_t dkv_uses = 0;
+      auto issue_grads = [&](uint32_t h, bool first_in_tile) {
+        const int slot = h & 1;
+        ptx::mbar_wait(ds_ready, h & 1);
+        ptx::tc_fence_after();
+        // dV += P^T dO_i ; dK += dS^T Q_i   (A: K-major [128 x BM], B: MN-major [BM x D])
+#pragma unroll
+        for (int k = 0; k < BM / 16; ++k) {
+          const uint32_t aoff = (k / 4) * (128 * 128) + (k % 4) * 32;
+          const uint32_t boff = k * 2048;
+          const uint32_t acc = (!first_in_tile || k > 0) ? 1u : 0u;
+          ptx::mma_ss(tmem + T_DV, ptx::sw128_desc(aPT + aoff, 16, 1024),
+                      ptx::sw128_desc(aDO + slot * L::Q_TILE + boff, L::Q_SUB, 1024), IDESC_G, acc);
+          ptx::mma_ss(tmem + T_DK, ptx::sw128_desc(aDST + aoff, 16, 1024),
+                      ptx::sw128_desc(aQ + slot * L::Q_TILE + boff, L::Q_SUB, 1024), IDESC_G, acc);
+        }
+        ptx::mma_commit(&q_empty[slot]);
+        if (h > 0) ptx::mbar_wait(dq_empty, (h - 1) & 1);
+        ptx::tc_fence_after();
+        // dQ^T = K^T dS^T  (A = K_j MN-major, B = dS^T MN-major), or dQ = dS K (A = dS^T as MN-major, B = K_j MN-major)
+#pragma unroll
+        for (int k = 0; k < 128 / 16; ++k) {
+          const uint32_t off = k * 2048;
+          if constexpr (DQT)
+            ptx::mma_ss(tmem + T_DQ, ptx::sw128_desc(aK + off, 128 * 128, 1024), ptx::sw128_desc(aDST + off, 128 * 128, 1024),
+                        IDESC_Q, k > 0 ? 1u : 0u);
+          else
+            ptx::mma_ss(tmem + T_DQ, ptx::sw128_desc(aDST + off, 128 * 128, 1024), ptx::sw128_desc(aK + off, 128 * 128, 1024),
+                        IDESC_Q, k > 0 ? 1u : 0u);
+        }
+        ptx::mma_commit(dq_full);
+        ptx::mma_commit(ds_empty);
+      };
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+        int bh, nb;
+        decode(t, bh, nb);
+        const int i0 = q_begin(nb);
+        ptx::mbar_wait(kv_full, it & 1);
+        ptx::tc_fence_after();
+        bool have_prev = false;
+        for (int i = i0; i < n_q_blocks; ++i, ++g) {
+          const int slot = g & 1;
+          ptx::mbar_wait(&q_full[slot], (g >> 1) & 1);
+          if (g > 0) ptx::mbar_wait(s_consumed, (g - 1) & 1);
+          ptx::tc_fence_after();
+          // S^T = K_j Q_i^T ; dP^T = V_j dO_i^T   (both operands K-major, K = D)
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t akv = (k / 4) * (128 * 128) + (k % 4) * 32;
+            const uint32_t aq = (k / 4) * L::Q_SUB + (k % 4) * 32;
+            ptx::mma_ss(tmem + T_ST, ptx::sw128_desc(aK + akv, 16, 1024),
+                        ptx::sw128_desc(aQ + slot * L::Q_TILE + aq, 16, 1024), IDESC_S, k > 0 ? 1u : 0u);
+            ptx::mma_ss(tmem + T_DPT, ptx::sw128_desc(aV + akv, 16, 1024),
+                        ptx::sw128_desc(aDO + slot * L::Q_TILE + aq, 16, 1024), IDESC_S, k > 0 ? 1u : 0u);
+          }
+          ptx::mma_commit(s_full);
+          if (have_prev) issue_grads(g - 1, i - 1 == i0);
+          else if (dkv_uses > 0) {
+            // first query tile of this work tile: previous dK/dV must be drained first
+            ptx::mbar_wait(dkv_empty, (dkv_uses - 1) & 1);
+          }
+          have_prev = true;
+        }
+        issue_grads(g - 1, (n_q_blocks - 1) == i0);
+        ++dkv_uses;
+        ptx::mma_commit(dkv_full);
+        ptx::mma_commit(kv_empty);
+      }
+    }
+  } else if (warp == 13) {
+    // ============================ TMA producer ============================
+    if (lane == 0) {
+      uint32_t g = 0;
+      int it = 0;
+      const uint64_t pol_q = ptx::l2_policy_evict_last();
+      const uint64_t pol_kv = ptx::l2_policy_evict_first();
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+        int bh, nb;
+        decode(t, bh, nb);
+        const int i0 = q_begin(nb);
+        if (it > 0) ptx::mbar_wait(kv_empty, (it - 1) & 1);
+        ptx::mbar_arrive_expect_tx(kv_full, 2 * L::KV_TILE);
+        for (int s = 0; s < NSUB; ++s) {
+          ptx::tma_load_3d_hint(sK + s * 128 * 128, &tm_k, kv_full, s * 64, nb * 128, bh, pol_kv);
+          ptx::tma_load_3d_hint(sV + s * 128 * 128, &tm_v, kv_full, s * 64, nb * 128, bh, pol_kv);
+        }
+        for (int i = i0; i < n_q_blocks; ++i, ++g) {
+          const int slot = g & 1;
+          if (g >= 2) ptx::mbar_wait(&q_empty[slot], ((g >> 1) - 1) & 1);
+          ptx::mbar_arrive_expect_tx(&q_full[slot], 2 * L::Q_TILE + 2 * BM * 4);
+          for (int s = 0; s < NSUB; ++s) {
+            ptx::tma_load_3d_hint(sQ + slot * L::Q_TILE + s * L::Q_SUB, &tm_q, &q_full[slot], s * 64, i * BM, bh, pol_q);
+            ptx::tma_load_3d_hint(sDO + slot * L::Q_TILE + s * L::Q_SUB, &tm_do, &q_full[slot], s * 64, i * BM, bh, pol_q);
+          }
+          float* vdst = sVec + slot * 2 * BM;
+          const size_t voff = static_cast<size_t>(bh) * p.npad + static_cast<size_t>(i) * BM;
+          ptx::bulk_load_1d(vdst, gL2 + voff, BM * 4, &q_full[slot]);
+          ptx::bulk_load_1d(vdst + BM, gD + voff, BM * 4, &q_full[slot]);
+        }
+      }
+    }
+  }
+  __syncwarp();
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace fa2

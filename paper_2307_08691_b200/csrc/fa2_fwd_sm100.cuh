@@ -1,0 +1,381 @@
+// FlashAttention-2 forward pass (Alg. 1) for sm_100a.
+//
+// One persistent CTA per SM walks a static list of work tiles.  A work tile is
+// (b*h, m_block): 2 query sub-tiles Q0, Q1 of 128 rows each (256 rows, the
+// "outer loop over row blocks").  For each key/value block K_j, V_j
+// (B_c = 128 rows, the inner loop P:354-362):
+//
+//   S_i  = Q_i K_j^T                 tcgen05.mma SS, fp32 accumulator in TMEM
+//   m, P~, l update (online softmax)  softmax warpgroup i, one thread = one row
+//   O_i  = diag(e^{m_old-m_new}) O_i + P~ V_j   tcgen05.mma TS (P~ from TMEM)
+//
+// The O rescale factor is e^{m_old - m_new} (no inverse; R3).  It is
+// applied lazily: the running max a row uses for its exponentials is only
+// moved when the true max exceeds it by more than 2^8 (log2 domain), which is
+// exact because l and O always share that max.  O is divided by
+// l once at the end (tweak 1) and only L = m + log l is stored
+// (tweak 2).  Causal blocks entirely above the diagonal are never
+// visited and the mask is only evaluated on blocks that straddle the diagonal
+// or the ragged tail.
+//
+// Warp roles (384 threads):
+//   warps 0-3   softmax WG 0: rows of Q0 (TMEM lanes 0-127), also O0 rescale + epilogue
+//   warps 4-7   softmax WG 1: rows of Q1
+//   warp  8     MMA issuer (one thread)
+//   warp  9     TMA producer (one thread)
+//   warps 10-11 idle (complete the register-donor warpgroup)
+//
+// TMEM columns: S0 [0,128), S1 [128,256), O0 [256,256+D), O1 [256+D,256+2D);
+// P~_i (16-bit) is written over the first 64 columns of S_i.
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
+#include "sm100_ptx.cuh"
+
+namespace fa2 {
+
+struct FwdParams {
+  void* o;             // [BH, N, D] dtype
+  float* lse;          // [BH, N]
+  int BH, N;
+  int num_m_blocks;    // ceil(N / 256)
+  int num_tiles;       // BH * num_m_blocks
+  float scale_log2;    // softmax_scale * log2(e)
+};
+
+template <int D>
+struct FwdSmem {
+  static constexpr int BM = 128, BN = 128;
+  static constexpr int STAGES = (D == 64) ? 3 : 2;
+  static constexpr int TILE = 128 * D * 2;       // bytes of one 128 x D tile
+  static constexpr int SUB = 128 * 128;          // one 128-row x 64-col swizzle box (16 KB)
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + 2 * TILE;
+  static constexpr int OFF_V = OFF_K + STAGES * TILE;
+  static constexpr int OFF_BAR = OFF_V + STAGES * TILE;
+  // barriers: q_full[2] q_empty[2] k_full[S] k_empty[S] v_full[S] v_empty[S] s_full[2] p_full[2] o_done[2] o_empty[2]
+  static constexpr int NBAR = 2 + 2 + 4 * STAGES + 2 + 2 + 2 + 2;
+  static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
+  static constexpr int BYTES = OFF_TMEM + 16;
+  static constexpr int ALLOC = BYTES + 1024;   // slack for 1024-B alignment
+};
+
+template <int D, bool BF16, bool CAUSAL>
+__global__ void __launch_bounds__(384, 1)
+fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+               const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
+  using L = FwdSmem<D>;
+  constexpr int STAGES = L::STAGES;
+  constexpr int NSUB = D / 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+
+  uint8_t* sQ = smem + L::OFF_Q;
+  uint8_t* sK = smem + L::OFF_K;
+  uint8_t* sV = smem + L::OFF_V;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint64_t* q_full = bars;
+  uint64_t* q_empty = bars + 2;
+  uint64_t* k_full = bars + 4;
+  uint64_t* k_empty = k_full + STAGES;
+  uint64_t* v_full = k_empty + STAGES;
+  uint64_t* v_empty = v_full + STAGES;
+  uint64_t* s_full = v_empty + STAGES;
+  uint64_t* p_full = s_full + 2;
+  uint64_t* o_done = p_full + 2;
+  uint64_t* o_empty = o_done + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&q_full[i], 1);
+      ptx::mbar_init(&q_empty[i], 1);
+      ptx::mbar_init(&s_full[i], 1);
+      ptx::mbar_init(&p_full[i], 4);
+      ptx::mbar_init(&o_done[i], 1);
+      ptx::mbar_init(&o_empty[i], 4);
+    }
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&k_full[s], 1);
+      ptx::mbar_init(&k_empty[s], 1);
+      ptx::mbar_init(&v_full[s], 1);
+      ptx::mbar_init(&v_empty[s], 1);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 9 && lane == 0) {
+    ptx::tma_prefetch_desc(&tm_q);
+    ptx::tma_prefetch_desc(&tm_k);
+    ptx::tma_prefetch_desc(&tm_v);
+  }
+  if (warp == 0) ptx::tmem_alloc(tmem_slot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int N = p.N;
+  const int n_kv_total = (N + 127) / 128;
+
+  // Work-tile decode, shared by all roles.  Heads are contiguous in the tile
+  // order so that the CTAs running concurrently share K/V in L2; for causal the
+  // heavy (late) row blocks of each head come first.
+  auto decode = [&](int t, int& bh, int& mb) {
+    bh = t / p.num_m_blocks;
+    int r = t % p.num_m_blocks;
+    mb = CAUSAL ? (p.num_m_blocks - 1 - r) : r;
+  };
+  // Number of KV blocks query sub-tile i of row block mb visits.
+  auto n_blocks = [&](int mb, int i) -> int {
+    const int r0 = mb * 256 + i * 128;
+    if (r0 >= N) return 0;
+    if (!CAUSAL) return n_kv_total;
+    const int last_row = min(N - 1, r0 + 127);
+    return min(n_kv_total, last_row / 128 + 1);
+  };
+
+  if (warp < 8) {
+    // ======================= softmax warpgroups =======================
+    ptx::setmaxnreg_inc<224>();   // 224*256 + 56*128 == 168*384
+    const int wg = warp / 4;                 // sub-tile index
+    const int row = threadIdx.x % 128;       // TMEM lane == row within sub-tile
+    const uint32_t lane_base = static_cast<uint32_t>((warp % 4) * 32) << 16;
+    const uint32_t tS = tmem + lane_base + wg * 128;
+    const uint32_t tO = tmem + lane_base + 256 + wg * D;
+    uint32_t s_count = 0;   // completed waits on s_full[wg]
+    uint32_t pv_count = 0;  // PV MMAs issued so far for this sub-tile (all tiles)
+    const float sl2 = p.scale_log2;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      int bh, mb;
+      decode(t, bh, mb);
+      const int nb = n_blocks(mb, wg);
+      if (nb == 0) continue;
+      const int row0 = mb * 256 + wg * 128;
+      const int grow = row0 + row;
+      float m_used = -INFINITY;   // running max in log2 units (may lag the true max by <= 8)
+      float l_sum = 0.f;
+      for (int j = 0; j < nb; ++j) {
+        ptx::mbar_wait(&s_full[wg], s_count & 1);
+        ++s_count;
+        ptx::tc_fence_after();
+        uint32_t su[128];
+        ptx::tmem_ld_x32(tS + 0, su + 0);
+        ptx::tmem_ld_x32(tS + 32, su + 32);
+        ptx::tmem_ld_x32(tS + 64, su + 64);
+        ptx::tmem_ld_x32(tS + 96, su + 96);
+        ptx::tmem_wait_ld();
+        float s[128];
+#pragma unroll
+        for (int c = 0; c < 128; ++c) s[c] = __uint_as_float(su[c]);
+        const int c0 = j * 128;
+        const bool need_mask = (c0 + 128 > N) || (CAUSAL && (c0 + 127 > row0));
+        if (need_mask) {
+          const int lim = CAUSAL ? min(N - 1, grow) : (N - 1);
+#pragma unroll
+          for (int c = 0; c < 128; ++c)
+            if (c0 + c > lim) s[c] = -INFINITY;
+        }
+        float mx = s[0];
+#pragma unroll
+        for (int c = 1; c < 128; ++c) mx = fmaxf(mx, s[c]);
+        const float m_new = fmaxf(m_used, mx * sl2);
+        const bool rescale = (m_new - m_used) > 8.0f;   // also true when m_used == -inf and m_new finite
+        float alpha = 1.f;
+        if (rescale) {
+          alpha = ptx::ex2(m_used - m_new);             // 0 when m_used == -inf
+          m_used = m_new;
+        }
+        const float base = (m_used == -INFINITY) ? 0.f : m_used;
+        float rs = 0.f;
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const float p0 = ptx::ex2(fmaf(s[ch * 32 + 2 * e], sl2, -base));
+            const float p1 = ptx::ex2(fmaf(s[ch * 32 + 2 * e + 1], sl2, -base));
+            rs += p0 + p1;
+            pk[e] = ptx::pack2<BF16>(p0, p1);
+          }
+          ptx::tmem_st_x16(tS + ch * 16, pk);
+        }
+        l_sum = l_sum * alpha + rs;
+        // Rescale the un-normalised O accumulator before P~_j V_j is added
+        // (needs PV_{j-1} finished; it was issued before S_j, so it usually is).
+        if (j > 0 && __any_sync(0xffffffffu, rescale)) {
+          ptx::mbar_wait(&o_done[wg], (pv_count - 1) & 1);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int ch = 0; ch < D / 32; ++ch) {
+            uint32_t o[32];
+            ptx::tmem_ld_x32(tO + ch * 32, o);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            ptx::tmem_st_x32(tO + ch * 32, o);
+          }
+        }
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&p_full[wg]);
+        ++pv_count;
+      }
+      // ---- epilogue: O = O / l, L = m + log l (natural log) ----
+      ptx::mbar_wait(&o_done[wg], (pv_count - 1) & 1);
+      ptx::tc_fence_after();
+      const float inv_l = 1.f / l_sum;
+      uint8_t* orow = reinterpret_cast<uint8_t*>(p.o) + (static_cast<size_t>(bh) * N + grow) * (D * 2);
+#pragma unroll
+      for (int ch = 0; ch < D / 32; ++ch) {
+        uint32_t o[32];
+        ptx::tmem_ld_x32(tO + ch * 32, o);
+        ptx::tmem_wait_ld();
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          pk[e] = ptx::pack2<BF16>(__uint_as_float(o[2 * e]) * inv_l, __uint_as_float(o[2 * e + 1]) * inv_l);
+        if (grow < N) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + ch * 64);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) dst[e] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+        }
+      }
+      if (grow < N) p.lse[static_cast<size_t>(bh) * N + grow] = (m_used + ptx::lg2(l_sum)) * 0.69314718055994531f;
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&o_empty[wg]);
+    }
+  } else {
+    ptx::setmaxnreg_dec<56>();
+    if (warp == 8 && lane == 0) {
+      // ============================ MMA issuer ============================
+      constexpr uint32_t IDESC_S = ptx::idesc_f16(BF16, 128, 128, false, false);
+      constexpr uint32_t IDESC_O = ptx::idesc_f16(BF16, 128, D, false, true);
+      const uint32_t q_addr = ptx::smem_u32(sQ);
+      const uint32_t k_addr = ptx::smem_u32(sK);
+      const uint32_t v_addr = ptx::smem_u32(sV);
+      int kslot = 0, vslot = 0;
+      uint32_t kphase = 0, vphase = 0;
+      uint32_t p_count[2] = {0, 0};
+      uint32_t o_uses[2] = {0, 0};
+      int it = 0;
+      auto mma_s = [&](int i, int slot) {
+        const uint32_t qa = q_addr + i * L::TILE;
+        const uint32_t ka = k_addr + slot * L::TILE;
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k / 4) * L::SUB + (k % 4) * 32;
+          ptx::mma_ss(tmem + i * 128, ptx::sw128_desc(qa + off, 16, 1024), ptx::sw128_desc(ka + off, 16, 1024),
+                      IDESC_S, k > 0 ? 1u : 0u);
+        }
+      };
+      auto mma_pv = [&](int i, int slot, bool acc) {
+        const uint32_t va = v_addr + slot * L::TILE;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          ptx::mma_ts(tmem + 256 + i * D, tmem + i * 128 + k * 8, ptx::sw128_desc(va + k * 2048, L::SUB, 1024),
+                      IDESC_O, (acc || k > 0) ? 1u : 0u);
+        }
+      };
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+        int bh, mb;
+        decode(t, bh, mb);
+        const int nb0 = n_blocks(mb, 0), nb1 = n_blocks(mb, 1);
+        const int nkv = max(nb0, nb1);
+        ptx::mbar_wait(&q_full[0], it & 1);
+        ptx::mbar_wait(&q_full[1], it & 1);
+        ptx::tc_fence_after();
+        if (nkv > 0) {
+          ptx::mbar_wait(&k_full[kslot], kphase);
+          ptx::tc_fence_after();
+          if (nb0 > 0) { mma_s(0, kslot); ptx::mma_commit(&s_full[0]); }
+          if (nb1 > 0) { mma_s(1, kslot); ptx::mma_commit(&s_full[1]); }
+          ptx::mma_commit(&k_empty[kslot]);
+          if (++kslot == STAGES) { kslot = 0; kphase ^= 1; }
+        }
+        for (int j = 0; j < nkv; ++j) {
+          ptx::mbar_wait(&v_full[vslot], vphase);
+          const bool next = (j + 1) < nkv;
+          bool k_ready = false;
+          for (int i = 0; i < 2; ++i) {
+            const int nbi = i == 0 ? nb0 : nb1;
+            if (j < nbi) {
+              if (j == 0) {
+                if (o_uses[i] > 0) ptx::mbar_wait(&o_empty[i], (o_uses[i] - 1) & 1);
+                ++o_uses[i];
+              }
+              ptx::mbar_wait(&p_full[i], p_count[i] & 1);
+              ++p_count[i];
+              ptx::tc_fence_after();
+              mma_pv(i, vslot, j > 0);
+              ptx::mma_commit(&o_done[i]);
+            }
+            if (j + 1 < nbi) {
+              if (!k_ready) {
+                ptx::mbar_wait(&k_full[kslot], kphase);
+                ptx::tc_fence_after();
+                k_ready = true;
+              }
+              mma_s(i, kslot);
+              ptx::mma_commit(&s_full[i]);
+            }
+          }
+          ptx::mma_commit(&v_empty[vslot]);
+          if (++vslot == STAGES) { vslot = 0; vphase ^= 1; }
+          if (next) {
+            if (!k_ready) {  // K_{j+1} was not needed by either sub-tile (cannot happen, kept for ring balance)
+              ptx::mbar_wait(&k_full[kslot], kphase);
+            }
+            ptx::mma_commit(&k_empty[kslot]);
+            if (++kslot == STAGES) { kslot = 0; kphase ^= 1; }
+          }
+        }
+        ptx::mma_commit(&q_empty[0]);
+        ptx::mma_commit(&q_empty[1]);
+      }
+    } else if (warp == 9 && lane == 0) {
+      // ============================ TMA producer ============================
+      int kslot = 0, vslot = 0;
+      uint32_t kphase = 0, vphase = 0;
+      int it = 0;
+      const uint64_t pol_kv = ptx::l2_policy_evict_last();
+      const uint64_t pol_q = ptx::l2_policy_evict_first();
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+        int bh, mb;
+        decode(t, bh, mb);
+        const int nkv = max(n_blocks(mb, 0), n_blocks(mb, 1));
+        for (int i = 0; i < 2; ++i) {
+          if (it > 0) ptx::mbar_wait(&q_empty[i], (it - 1) & 1);
+          ptx::mbar_arrive_expect_tx(&q_full[i], L::TILE);
+          for (int s = 0; s < NSUB; ++s)
+            ptx::tma_load_3d_hint(sQ + i * L::TILE + s * L::SUB, &tm_q, &q_full[i], s * 64, mb * 256 + i * 128, bh, pol_q);
+        }
+        for (int j = 0; j < nkv; ++j) {
+          ptx::mbar_wait(&k_empty[kslot], kphase ^ 1);
+          ptx::mbar_arrive_expect_tx(&k_full[kslot], L::TILE);
+          for (int s = 0; s < NSUB; ++s)
+            ptx::tma_load_3d_hint(sK + kslot * L::TILE + s * L::SUB, &tm_k, &k_full[kslot], s * 64, j * 128, bh, pol_kv);
+          if (++kslot == STAGES) { kslot = 0; kphase ^= 1; }
+          ptx::mbar_wait(&v_empty[vslot], vphase ^ 1);
+          ptx::mbar_arrive_expect_tx(&v_full[vslot], L::TILE);
+          for (int s = 0; s < NSUB; ++s)
+            ptx::tma_load_3d_hint(sV + vslot * L::TILE + s * L::SUB, &tm_v, &v_full[vslot], s * 64, j * 128, bh, pol_kv);
+          if (++vslot == STAGES) { vslot = 0; vphase ^= 1; }
+        }
+      }
+    }
+  }
+  __syncwarp();
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace fa2

@@ -1,0 +1,46 @@
+"""Helpers shared by the GPU parity tests (comparison rules of DESIGN.md §4)."""
+import math
+
+import numpy as np
+import torch
+
+# BASELINE.json north_star tolerances
+TOL = {
+    "bf16": {"O": 1e-2, "grad": 5e-2, "L": 1e-3},
+    "fp16": {"O": 2e-3, "grad": 1e-2, "L": 1e-3},
+}
+MANT = {"bf16": 7, "fp16": 10}
+
+
+def half_ulp(ref: np.ndarray, dtype: str) -> np.ndarray:
+    """Half a unit in the last place of the dtype at |ref| (R14): the error a
+    correctly rounded output of the exact value may already carry."""
+    a = np.abs(ref)
+    e = np.floor(np.log2(np.maximum(a, 2.0 ** -14)))
+    return 2.0 ** (e - MANT[dtype] - 1)
+
+
+def o_excess(o_gpu: torch.Tensor, o_ref: np.ndarray, dtype: str) -> float:
+    err = np.abs(o_gpu.double().cpu().numpy() - o_ref)
+    return float(np.max(err - half_ulp(o_ref, dtype)))
+
+
+def max_abs(a, b) -> float:
+    a = a.double().cpu().numpy() if isinstance(a, torch.Tensor) else a
+    b = b.double().cpu().numpy() if isinstance(b, torch.Tensor) else b
+    return float(np.max(np.abs(a - b)))
+
+
+def grad_ok(g_gpu: torch.Tensor, g_ref: np.ndarray, dtype: str):
+    """Per-tensor rule (R15): max-abs error <= c * max|g_ref|."""
+    err = max_abs(g_gpu, g_ref)
+    lim = TOL[dtype]["grad"] * float(np.max(np.abs(g_ref)))
+    return err <= lim + 1e-30, err, lim
+
+
+def to_np(t: torch.Tensor) -> np.ndarray:
+    return t.double().cpu().numpy()
+
+
+def scale_for(d: int) -> float:
+    return 1.0 / math.sqrt(d)

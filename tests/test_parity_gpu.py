@@ -1,0 +1,155 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) vs the CPU fp64 oracle on
+the same seeded, dtype-rounded inputs."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2307_08691_b200 as fa2
+import workloads as W
+from oracle import ref_attention as R
+from tests.gpu_util import TOL, grad_ok, max_abs, o_excess, scale_for, to_np
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [  # (B, H, N, d)
+    (1, 1, 128, 64),      # BASELINE config 0
+    (1, 1, 1, 64),
+    (2, 3, 17, 64),
+    (1, 2, 255, 128),
+    (1, 2, 256, 128),
+    (2, 2, 257, 64),
+    (1, 2, 600, 128),
+    (1, 1, 1000, 64),
+    (1, 1, 2048, 128),
+]
+
+
+def run_fwd(q, k, v, causal, scale):
+    o, lse = fa2.forward(q.cuda(), k.cuda(), v.cuda(), causal=causal, softmax_scale=scale)
+    torch.cuda.synchronize()
+    return o.cpu(), lse.cpu()
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "x".join(map(str, s)))
+def test_forward_parity(shape, causal, dtype):
+    B, H, N, d = shape
+    q, k, v, _ = W.qkv(B, H, N, d, dtype, seed=100 + N + d, with_do=False)
+    sc = scale_for(d)
+    o, lse = run_fwd(q, k, v, causal, sc)
+    o_ref, l_ref = R.forward(to_np(q), to_np(k), to_np(v), sc, causal)
+    assert torch.isfinite(o.float()).all() and torch.isfinite(lse).all()
+    ex = o_excess(o, o_ref, dtype)
+    el = max_abs(lse, l_ref)
+    assert ex <= TOL[dtype]["O"], f"O excess {ex}"
+    assert el <= TOL[dtype]["L"], f"L err {el}"
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "x".join(map(str, s)))
+def test_backward_parity(shape, causal, dtype):
+    B, H, N, d = shape
+    q, k, v, do = W.qkv(B, H, N, d, dtype, seed=200 + N + d)
+    sc = scale_for(d)
+    qc, kc, vc, doc = q.cuda(), k.cuda(), v.cuda(), do.cuda()
+    o, lse = fa2.forward(qc, kc, vc, causal=causal, softmax_scale=sc)
+    dq, dk, dv = fa2.backward(qc, kc, vc, o, lse, doc, causal=causal, softmax_scale=sc)
+    torch.cuda.synchronize()
+    gq, gk, gv, _ = R.backward(to_np(q), to_np(k), to_np(v), to_np(do), sc, causal)
+    for name, g, ref in (("dq", dq, gq), ("dk", dk, gk), ("dv", dv, gv)):
+        assert torch.isfinite(g.float()).all(), name
+        ok, err, lim = grad_ok(g, ref, dtype)
+        assert ok, f"{name}: err {err} > {lim}"
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_preprocess_D(d):
+    B, H, N = 2, 2, 300
+    q, k, v, do = W.qkv(B, H, N, d, "bf16", seed=7)
+    o = W.randn((B, H, N, d), 99, "bf16")
+    D = fa2.backward_preprocess(o.cuda(), do.cuda())
+    torch.cuda.synchronize()
+    ref = R.rowsum_dO_O(to_np(o), to_np(do))
+    assert max_abs(D.cpu(), ref) <= 1e-4 * max(1.0, float(np.max(np.abs(ref))))
+
+
+def test_forward_deterministic():
+    q, k, v, _ = W.qkv(2, 4, 1000, 128, "bf16", seed=5, with_do=False)
+    a = fa2.forward(q.cuda(), k.cuda(), v.cuda(), causal=True)
+    b = fa2.forward(q.cuda(), k.cuda(), v.cuda(), causal=True)
+    torch.cuda.synchronize()
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("d", [64, 128])
+def test_identical_keys(causal, d):
+    N = 300
+    q, k, v = W.identical_keys(N, d, "bf16", seed=3)
+    sc = scale_for(d)
+    o, lse = run_fwd(q, k, v, causal, sc)
+    vv = to_np(v)[0, 0]
+    want = (np.cumsum(vv, 0) / np.arange(1, N + 1)[:, None]) if causal else np.tile(vv.mean(0), (N, 1))
+    assert o_excess(o[0:1, 0:1], want[None, None], "bf16") <= TOL["bf16"]["O"]
+    do = W.randn((1, 1, N, d), 11, "bf16")
+    o2, l2 = fa2.forward(q.cuda(), k.cuda(), v.cuda(), causal=causal, softmax_scale=sc)
+    dq, dk, dv = fa2.backward(q.cuda(), k.cuda(), v.cuda(), o2, l2, do.cuda(), causal=causal, softmax_scale=sc)
+    torch.cuda.synchronize()
+    # identical keys: every logit of a row is equal, so dQ = 0 exactly in exact arithmetic
+    gq, _, _, _ = R.backward(to_np(q), to_np(k), to_np(v), to_np(do), sc, causal)
+    assert np.max(np.abs(gq)) < 1e-10
+    assert float(dq.abs().max()) <= 5e-2 * float(dv.abs().max())
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_one_hot_large_logit(causal):
+    N, d, jstar = 256, 64, 37
+    q, k, v = W.one_hot_logit(N, d, jstar, alpha=32.0, dtype="bf16")
+    o, lse = run_fwd(q, k, v, causal, 1.0 / 8.0)   # s * alpha^2 = 128
+    rows = slice(jstar, N) if causal else slice(0, N)
+    ref = to_np(v)[0, 0, jstar]
+    assert np.max(np.abs(to_np(o)[0, 0, rows] - ref)) <= 1e-6 + np.max(np.abs(ref)) * 2 ** -8
+
+
+def test_overflow_logits_finite():
+    """Logits up to +300: exp would overflow fp32 without the max."""
+    N, d = 300, 64
+    q = torch.zeros(1, 1, N, d); q[..., 0] = 17.0
+    k = torch.zeros(1, 1, N, d); k[..., 0] = 17.0 * torch.linspace(0.5, 1.0, N)
+    v = W.randn((1, 1, N, d), 4, "bf16")
+    q, k = q.bfloat16(), k.bfloat16()
+    o, lse = run_fwd(q, k, v, False, 1.0)
+    assert torch.isfinite(o.float()).all() and torch.isfinite(lse).all()
+    o_ref, l_ref = R.forward(to_np(q), to_np(k), to_np(v), 1.0, False)
+    assert float(l_ref.max()) > 250
+    assert o_excess(o, o_ref, "bf16") <= 1e-2
+    assert max_abs(lse, l_ref) <= 1e-3 * max(1.0, float(np.abs(l_ref).max()))
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_step_host_matches_device_path(causal):
+    B, H, N, d = 1, 2, 384, 128
+    q, k, v, do = W.qkv(B, H, N, d, "bf16", seed=9)
+    pin = [t.pin_memory() for t in (q, k, v, do)]
+    outs = {"o": torch.empty_like(q).pin_memory(), "lse": torch.empty(B, H, N).pin_memory(),
+            "dq": torch.empty_like(q).pin_memory(), "dk": torch.empty_like(q).pin_memory(),
+            "dv": torch.empty_like(q).pin_memory()}
+    arena = torch.empty(fa2.step_arena_size(B, H, N, d), dtype=torch.uint8, device="cuda")
+    fa2.attention_step_host(*pin, outs, arena, causal)
+    o, lse = fa2.forward(q.cuda(), k.cuda(), v.cuda(), causal=causal)
+    dq, dk, dv = fa2.backward(q.cuda(), k.cuda(), v.cuda(), o, lse, do.cuda(), causal=causal)
+    torch.cuda.synchronize()
+    assert torch.equal(outs["o"], o.cpu()) and torch.equal(outs["lse"], lse.cpu())
+    assert torch.equal(outs["dk"], dk.cpu()) and torch.equal(outs["dv"], dv.cpu())
+    assert max_abs(outs["dq"], dq) <= 1e-2 * float(dq.abs().max())
+
+
+def test_launch_count_and_errors():
+    q, k, v, do = W.qkv(1, 1, 128, 64, "bf16", seed=1)
+    qc = q.cuda()
+    fa2.forward(qc, k.cuda(), v.cuda())
+    assert fa2.lib().fa2_last_launch_count() == 1
+    with pytest.raises(fa2.FA2Error):
+        fa2.forward(qc.float(), k.cuda().float(), v.cuda().float())
