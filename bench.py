@@ -1,0 +1,421 @@
+"""Benchmark of the B200 FlashAttention-2 hot path (fwd + bwd step).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--sweep]
+
+Under torchrun (N > 1) each rank runs the same per-GPU workload (weak scaling
+over batch x heads, no collective in the data path); the step time is the max
+over ranks.  Rank 0 prints ONE JSON line.
+
+Workload (BASELINE.json configs[2], "paper fwd+bwd benchmark"): hidden 2048,
+d = 128 (H = 16), N = 8192, batch = 16k / N = 2, bf16, non-causal; synthetic
+N(0,1) inputs resident in HBM (320 MiB of q,k,v,o,dO per step, larger than the
+126 MB L2, so no explicit flush).  FLOPs follow the paper:
+4 N^2 d H B per forward, x2.5 backward, /2 causal.
+
+--impl reference times the CPU fp64 oracle (oracle/) on the host cores on a
+bounded sample of the same workload (one (b,h) head per step) — the only
+"reference" this tier has.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "attention fwd/bwd/fwd+bwd TFLOP/s (d=64/128, N=512–16k), % of B200 bf16 peak"
+NOMINAL_PEAK_TFLOPS = 2250.0
+
+
+def flops(B, H, N, d, causal, pass_):
+    f = 4.0 * N * N * d * H * B
+    if causal:
+        f /= 2
+    return f * {"fwd": 1.0, "bwd": 2.5, "fwd_bwd": 3.5}[pass_]
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return {"bf16_tflops": j.get("bf16_tflops", 1590.0), "bf16_tflops_sustained": j.get("bf16_tflops_sustained"),
+                "hbm_gbs": j.get("hbm_gbs", 6650.0), "source": "MEASURED_PEAKS.json (of measured)"}
+    return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0,
+            "source": "B200_PROFILING.md fallback (of fallback)"}
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML polling thread)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, dev_index: int):
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+def dist_setup(gpus: int):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline and --impl reference)
+# ---------------------------------------------------------------------------
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max((i.get("num_threads", 0) for i in threadpool_info() if i.get("user_api") == "blas"), default=None)
+    except Exception:
+        return None
+
+
+def oracle_head_step(N, d, causal, seed):
+    """One bounded sample: fwd + bwd of ONE (b,h) head of the workload through
+    the fp64 oracle, on the same dtype-rounded N(0,1) inputs.  Returns seconds."""
+    import workloads as W
+    from oracle import ref_attention as R
+    q, k, v, do = W.qkv(1, 1, N, d, "bf16", seed=seed)
+    f = lambda t: t[0, 0].double().numpy()
+    qq, kk, vv, dd = f(q), f(k), f(v), f(do)
+    sc = 1.0 / math.sqrt(d)
+    t0 = time.perf_counter()
+    R.forward_head(qq, kk, vv, sc, causal)
+    R.backward_head(qq, kk, vv, dd, sc, causal)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(cfg, budget_s=20.0):
+    N, d, causal = cfg["N"], cfg["d"], cfg["causal"]
+    fl = flops(1, 1, N, d, causal, "fwd_bwd")
+    times = []
+    t_start = time.perf_counter()
+    while not times or (time.perf_counter() - t_start < budget_s and len(times) < 5):
+        times.append(oracle_head_step(N, d, causal, seed=len(times)))
+    t = statistics.median(times)
+    return {"value": fl / t / 1e12, "unit": "TFLOP/s", "cores": blas_threads() or os.cpu_count(),
+            "kind": "oracle",
+            "sample": f"fp64 numpy oracle, fwd+bwd of one (b,h) head at N={N}, d={d}, causal={causal} "
+                      f"({len(times)} runs, median {t:.2f} s); the full step is {cfg['B'] * cfg['H']} such heads"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, world, rank, local):
+    import torch
+    import paper_2307_08691_b200 as fa2
+
+    cfg = dict(B=args.batch, H=args.heads, N=args.seqlen, d=args.head_dim, causal=bool(args.causal))
+    B, H, N, d, causal = cfg["B"], cfg["H"], cfg["N"], cfg["d"], cfg["causal"]
+    dev = torch.device("cuda", local if world > 1 else 0)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1000 + rank)
+    mk = lambda: torch.randn(B, H, N, d, device=dev, dtype=torch.bfloat16, generator=g)
+    q, k, v, do = mk(), mk(), mk(), mk()
+    o = torch.empty_like(q)
+    lse = torch.empty(B, H, N, device=dev, dtype=torch.float32)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
+    ws = torch.empty(fa2.backward_workspace_size(B, H, N, d), dtype=torch.uint8, device=dev)
+    sc = 1.0 / math.sqrt(d)
+    stream = torch.cuda.current_stream()
+    launches = [0]
+
+    def step():
+        fa2.forward(q, k, v, causal=causal, softmax_scale=sc, out=o, lse=lse)
+        launches[0] += fa2.lib().fa2_last_launch_count()
+        fa2.backward(q, k, v, o, lse, do, causal=causal, softmax_scale=sc, dq=dq, dk=dk, dv=dv, workspace=ws)
+        launches[0] += fa2.lib().fa2_last_launch_count()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # per-step kernel events (hook inside the library, same stream as the kernels)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
+    for es in evs:
+        for e in es:
+            e.record(stream)
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches[0] = 0
+    sampler = ClockSampler(local if world > 1 else 0)
+    barrier(world)
+    torch.cuda.synchronize()
+    with sampler:
+        start.record(stream)
+        keep = []
+        for i in range(args.steps):
+            keep.append(fa2.set_timing_events(evs[i]))
+            step()
+        fa2.set_timing_events(None)
+        end.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    ms_local = start.elapsed_time(end) / args.steps
+    ms = max_over_ranks(ms_local, world)
+    k_ms = {"fwd": [], "bwd_pre": [], "bwd_main": [], "bwd_dq": []}
+    for es in evs:
+        k_ms["fwd"].append(es[0].elapsed_time(es[1]))
+        k_ms["bwd_pre"].append(es[2].elapsed_time(es[3]))
+        k_ms["bwd_main"].append(es[3].elapsed_time(es[4]))
+        k_ms["bwd_dq"].append(es[4].elapsed_time(es[5]))
+    k_avg = {kk: statistics.mean(vv) for kk, vv in k_ms.items()}
+
+    fl_step = flops(B, H, N, d, causal, "fwd_bwd")
+    value = fl_step * world / (ms * 1e-3) / 1e12
+    peaks = measured_peaks()
+    fl_bwd = flops(B, H, N, d, causal, "bwd")
+    fl_fwd = flops(B, H, N, d, causal, "fwd")
+    dominant = "bwd_main" if k_avg["bwd_main"] >= k_avg["fwd"] else "fwd"
+    dom_fl = fl_bwd if dominant == "bwd_main" else fl_fwd
+    achieved = dom_fl / (k_avg[dominant] * 1e-3) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(dominant)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "kernel": "fa2_bwd_kernel" if dominant == "bwd_main" else "fa2_fwd_kernel",
+                "achieved": round(achieved, 1), "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": round(achieved / peaks["bf16_tflops"], 4), "traffic": traffic,
+                "peak_source": peaks["source"] + ", burst bf16 GEMM",
+                "algorithmic_flops_per_launch": dom_fl,
+                "kernel_ms": {kk: round(vv, 4) for kk, vv in k_avg.items()},
+                "kernel_share_of_step": {kk: round(vv / ms_local, 4) for kk, vv in k_avg.items()}}
+    passes = {"fwd_tflops": round(fl_fwd / (k_avg["fwd"] * 1e-3) / 1e12, 1),
+              "bwd_tflops": round(fl_bwd / ((k_avg["bwd_pre"] + k_avg["bwd_main"] + k_avg["bwd_dq"]) * 1e-3) / 1e12, 1),
+              "fwd_bwd_tflops": round(fl_step / (ms_local * 1e-3) / 1e12, 1)}
+
+    # ---- e2e: the same step through the host-buffer C-ABI entry point ----
+    e2e = run_e2e(fa2, cfg, dev, world, args)
+
+    out = {"metric": METRIC, "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "bf16", "data": "synthetic N(0,1), seeded",
+           "config": {"workload": f"paper fwd+bwd benchmark (BASELINE configs[2]): hidden 2048, d={d}, H={H}, "
+                                  f"N={N}, batch={B}, bf16, {'causal' if causal else 'non-causal'}; fwd+bwd per step",
+                      "B": B, "H": H, "N": N, "d": d, "causal": causal, "per_gpu": True,
+                      "l2": "inputs larger than L2 (q,k,v,o,dO = %d MiB per step > 126 MB); no flush" %
+                            (5 * B * H * N * d * 2 // 2 ** 20),
+                      "parallelism": f"batch x heads, {world} independent replica(s), no collective"},
+           "pct_of_nominal_peak": round(100 * value / world / NOMINAL_PEAK_TFLOPS, 2),
+           "passes": passes,
+           "clocks": sampler.summary(),
+           "gpu_launches": launches[0],
+           "roofline": roofline,
+           "e2e": e2e}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(cfg, budget_s=args.cpu_budget)
+    if args.sweep and rank == 0:
+        out["sweep"] = run_sweep(fa2, dev)
+    return out
+
+
+def run_e2e(fa2, cfg, dev, world, args):
+    import torch
+    B, H, N, d, causal = cfg["B"], cfg["H"], cfg["N"], cfg["d"], cfg["causal"]
+    g = torch.Generator()
+    g.manual_seed(7)
+    host = [torch.randn(B, H, N, d, generator=g).bfloat16().pin_memory() for _ in range(4)]
+    outs = {"o": torch.empty(B, H, N, d, dtype=torch.bfloat16).pin_memory(),
+            "lse": torch.empty(B, H, N, dtype=torch.float32).pin_memory(),
+            "dq": torch.empty(B, H, N, d, dtype=torch.bfloat16).pin_memory(),
+            "dk": torch.empty(B, H, N, d, dtype=torch.bfloat16).pin_memory(),
+            "dv": torch.empty(B, H, N, d, dtype=torch.bfloat16).pin_memory()}
+    arena = torch.empty(fa2.step_arena_size(B, H, N, d), dtype=torch.uint8, device=dev)
+    steps = max(3, min(args.steps, 10))
+    for _ in range(2):
+        fa2.attention_step_host(*host, outs, arena, causal)
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        fa2.attention_step_host(*host, outs, arena, causal)   # synchronises the stream before returning
+    dt = (time.perf_counter() - t0) / steps
+    dt = max_over_ranks(dt, world)
+    t_bytes = B * H * N * d * 2
+    return {"value": round(flops(B, H, N, d, causal, "fwd_bwd") * world / dt / 1e12, 2), "unit": "TFLOP/s",
+            "ms_per_step": round(dt * 1e3, 3), "h2d_bytes_per_step": 4 * t_bytes,
+            "d2h_bytes_per_step": 4 * t_bytes + B * H * N * 4,
+            "api": "fa2_attention_step_host (pinned host buffers in/out, wall clock incl. copies)"}
+
+
+def run_sweep(fa2, dev):
+    """Paper sweep: N = 512..16k, batch = 16k/N, hidden 2048."""
+    import torch
+    res = []
+    for d, H in ((64, 32), (128, 16)):
+        for causal in (False, True):
+            for N in (512, 1024, 2048, 4096, 8192, 16384):
+                B = 16384 // N
+                mk = lambda: torch.randn(B, H, N, d, device=dev, dtype=torch.bfloat16)
+                q, k, v, do = mk(), mk(), mk(), mk()
+                o, lse = fa2.forward(q, k, v, causal=causal)
+                ws = torch.empty(fa2.backward_workspace_size(B, H, N, d), dtype=torch.uint8, device=dev)
+                dq, dk, dv = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
+
+                def tm(fn, reps=10):
+                    for _ in range(3):
+                        fn()
+                    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    s.record()
+                    for _ in range(reps):
+                        fn()
+                    e.record()
+                    torch.cuda.synchronize()
+                    return s.elapsed_time(e) / reps
+
+                t_f = tm(lambda: fa2.forward(q, k, v, causal=causal, out=o, lse=lse))
+                t_b = tm(lambda: fa2.backward(q, k, v, o, lse, do, causal=causal, dq=dq, dk=dk, dv=dv, workspace=ws))
+                res.append({"d": d, "H": H, "N": N, "B": B, "causal": causal,
+                            "fwd_tflops": round(flops(B, H, N, d, causal, "fwd") / t_f / 1e9, 1),
+                            "bwd_tflops": round(flops(B, H, N, d, causal, "bwd") / t_b / 1e9, 1),
+                            "fwd_bwd_tflops": round(flops(B, H, N, d, causal, "fwd_bwd") / (t_f + t_b) / 1e9, 1)})
+                del q, k, v, do, o, lse, ws, dq, dk, dv
+    return res
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the CPU fp64 oracle on the host cores
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return None
+    N, d, causal = args.seqlen, args.head_dim, bool(args.causal)
+    for _ in range(args.warmup):
+        oracle_head_step(N, d, causal, seed=0)
+    ts = [oracle_head_step(N, d, causal, seed=i + 1) for i in range(args.steps)]
+    t = statistics.mean(ts)
+    value = flops(1, 1, N, d, causal, "fwd_bwd") / t / 1e12
+    cores = blas_threads() or os.cpu_count()
+    sample = (f"fp64 numpy oracle (oracle/ref_attention.py), each step = fwd+bwd of one (b,h) head of the workload "
+              f"(N={N}, d={d}, causal={causal}); full step = {args.batch * args.heads} heads")
+    return {"metric": METRIC, "value": round(value, 6), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(t * 1e3, 2), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic N(0,1), seeded", "impl": "reference",
+            "config": {"workload": f"paper fwd+bwd benchmark (BASELINE configs[2]): hidden 2048, d={d}, "
+                                   f"H={args.heads}, N={N}, batch={args.batch}, bf16-rounded inputs; "
+                                   f"one head per step (bounded sample)",
+                       "B": args.batch, "H": args.heads, "N": N, "d": d, "causal": causal},
+            "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": round(value, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--seqlen", type=int, default=8192)
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--heads", type=int, default=16)
+    ap.add_argument("--head-dim", type=int, default=128)
+    ap.add_argument("--causal", type=int, default=0)
+    ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    if args.batch is None:
+        args.batch = max(1, 16384 // args.seqlen)
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        out = run_reference(args)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    world, rank, local = dist_setup(args.gpus)
+    out = run_ours(args, world, rank, local)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

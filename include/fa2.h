@@ -66,7 +66,8 @@ FA2_API fa2_status_t fa2_forward(const void* q, const void* k, const void* v, vo
                          fa2_dtype_t dtype, void* stream);
 
 /* Bytes of device scratch fa2_backward needs: the fp32 dQ accumulator
- * [B,H,N_pad,d] and D [B,H,N_pad] (fp32), N_pad = N rounded up to 128. */
+ * [B,H,N_pad,d], D [B,H,N_pad] and L*log2(e) [B,H,N_pad] (fp32), where N_pad is
+ * N rounded up to a multiple of 128. */
 FA2_API size_t fa2_backward_workspace_size(int B, int H, int N, int d);
 
 /* Backward pass, Alg. 2: writes dq, dk, dv ([B,H,N,d], dtype).
@@ -104,6 +105,15 @@ FA2_API fa2_status_t fa2_attention_step_host(const void* q_h, const void* k_h, c
  * or ragged mask (first_masked; == n_blocks when none).  Returns FA2_OK or
  * FA2_ERR_INVALID_ARG. */
 FA2_API fa2_status_t fa2_kv_block_range(int N, int Br, int Bc, int i, int causal, int* n_blocks, int* first_masked);
+
+/* Optional benchmark timing hook (per calling thread).  `events` points to 6
+ * cudaEvent_t created by the caller (or is NULL to disable).  While set,
+ * fa2_forward records events[0] / events[1] on `stream` immediately before /
+ * after its kernel, and fa2_backward records events[2] before the D
+ * preprocessing kernel, events[3] before the main backward kernel, events[4]
+ * after it and events[5] after the dQ conversion kernel.  The array must stay
+ * valid until the calls that use it have been issued. */
+FA2_API void fa2_set_timing_events(void* const* events);
 
 FA2_API const char* fa2_status_string(fa2_status_t s);
 FA2_API const char* fa2_last_error_detail(void);

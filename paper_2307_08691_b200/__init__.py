@@ -12,7 +12,7 @@ import math
 import os
 
 __all__ = ["lib", "forward", "backward", "backward_preprocess", "backward_workspace_size",
-           "attention_step_host", "step_arena_size", "kv_block_range", "FA2Error", "LIB_PATH"]
+           "attention_step_host", "step_arena_size", "kv_block_range", "set_timing_events", "FA2Error", "LIB_PATH"]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libfa2_sm100.so")
@@ -57,6 +57,8 @@ def lib() -> ctypes.CDLL:
         L.fa2_status_string.restype = ctypes.c_char_p
         L.fa2_last_error_detail.argtypes = []
         L.fa2_last_error_detail.restype = ctypes.c_char_p
+        L.fa2_set_timing_events.argtypes = [vp]
+        L.fa2_set_timing_events.restype = None
         L.fa2_last_launch_count.argtypes = []
         L.fa2_last_launch_count.restype = i
         _lib = L
@@ -166,6 +168,18 @@ def attention_step_host(q_h, k_h, v_h, do_h, outs, arena, causal: bool, softmax_
                                          _ptr(arena), arena.numel() * arena.element_size(), B, H, N, d,
                                          int(bool(causal)), scale, _dtype_code(q_h),
                                          ctypes.c_void_p(_stream(stream))))
+
+
+def set_timing_events(events):
+    """Benchmark hook: `events` is a list of 6 torch.cuda.Event (created with
+    enable_timing=True) or None.  See fa2_set_timing_events in include/fa2.h.
+    Returns the ctypes array, which the caller must keep alive while in use."""
+    if events is None:
+        lib().fa2_set_timing_events(None)
+        return None
+    arr = (ctypes.c_void_p * 6)(*[ctypes.c_void_p(e.cuda_event) for e in events])
+    lib().fa2_set_timing_events(ctypes.cast(arr, ctypes.c_void_p))
+    return arr
 
 
 def kv_block_range(N: int, Br: int, Bc: int, i: int, causal: bool):

@@ -17,6 +17,11 @@ namespace {
 
 thread_local std::string g_detail;
 thread_local int g_launches = 0;
+thread_local cudaEvent_t const* g_events = nullptr;   // benchmark timing hook (fa2_set_timing_events)
+
+inline void mark(int i, cudaStream_t st) {
+  if (g_events != nullptr) cudaEventRecord(g_events[i], st);
+}
 
 fa2_status_t fail(fa2_status_t s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 fa2_status_t fail(fa2_status_t s, const char* fmt, ...) {
@@ -127,7 +132,9 @@ fa2_status_t launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUte
   fa2_status_t s = set_smem(kern, smem);
   if (s != FA2_OK) return s;
   const int grid = p.num_tiles < sms ? p.num_tiles : sms;
+  mark(0, st);
   kern<<<grid, 384, smem, st>>>(mq, mk, mv, p);
+  mark(1, st);
   FA2_CUDA(cudaGetLastError());
   return FA2_OK;
 }
@@ -198,7 +205,9 @@ fa2_status_t launch_bwd(const fa2::BwdMaps& maps, const fa2::BwdParams& p, int s
   fa2_status_t s = set_smem(kern, smem);
   if (s != FA2_OK) return s;
   const int grid = p.num_tiles < sms ? p.num_tiles : sms;
+  mark(3, st);
   kern<<<grid, fa2::kBwdThreads, smem, st>>>(maps.q, maps.k, maps.v, maps.dout, maps.dq_acc, p);
+  mark(4, st);
   FA2_CUDA(cudaGetLastError());
   return FA2_OK;
 }
@@ -217,6 +226,7 @@ fa2_status_t backward_impl(const void* q, const void* k, const void* v, const vo
   float* dq_acc = reinterpret_cast<float*>(ws);
   float* dvec = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + ws_dq_bytes(B, H, N, d));
   float* lse2 = dvec + static_cast<size_t>(BH) * npad;
+  mark(2, st);
   fa2_status_t s = preprocess_impl(o, dout, lse, dvec, lse2, dq_acc, BH, N, static_cast<int>(npad), d, dtype, st);
   if (s != FA2_OK) return s;
   fa2::BwdMaps maps;
@@ -256,6 +266,7 @@ fa2_status_t backward_impl(const void* q, const void* k, const void* v, const vo
     if (bf16) fa2::fa2_dq_convert<true><<<grid, 256, 0, st>>>(dq_acc, dq, BH, N, static_cast<int>(npad), d);
     else fa2::fa2_dq_convert<false><<<grid, 256, 0, st>>>(dq_acc, dq, BH, N, static_cast<int>(npad), d);
     FA2_CUDA(cudaGetLastError());
+    mark(5, st);
   }
   return FA2_OK;
 }
@@ -276,6 +287,7 @@ const char* fa2_status_string(fa2_status_t s) {
 }
 
 const char* fa2_last_error_detail(void) { return g_detail.c_str(); }
+void fa2_set_timing_events(void* const* events) { g_events = reinterpret_cast<cudaEvent_t const*>(events); }
 int fa2_last_launch_count(void) { return g_launches; }
 
 fa2_status_t fa2_kv_block_range(int N, int Br, int Bc, int i, int causal, int* n_blocks, int* first_masked) {

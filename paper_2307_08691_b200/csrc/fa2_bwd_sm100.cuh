@@ -221,6 +221,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     const int wg = warp / 4;
     const int r = threadIdx.x % 128;                   // key row within the block == TMEM lane
     const uint32_t lane_base = static_cast<uint32_t>((warp % 4) * 32) << 16;
+    const uint32_t sVec_a = ptx::smem_u32(sVec), sPT_a = ptx::smem_u32(sPT), sDST_a = ptx::smem_u32(sDST);
     uint32_t g = 0;          // global query-tile counter
     int it = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
@@ -233,11 +234,10 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         ptx::mbar_wait(&q_full[slot], (g >> 1) & 1);
         ptx::mbar_wait(s_full, g & 1);
         ptx::tc_fence_after();
-        const float* vL2 = sVec + slot * 2 * BM;
-        const float* vD = vL2 + BM;
+        const uint32_t vL2 = sVec_a + slot * 2 * BM * 4;     // L_i * log2(e) for the BM query rows
+        const uint32_t vD = vL2 + BM * 4;                     // D_i
         const bool need_mask = (CAUSAL && (i * BM < nb * 128 + 128)) || (nb * 128 + 128 > N);
-        // wait until the previous tile's dV/dK/dQ MMAs have read P^T / dS^T
-        if (g > 0) ptx::mbar_wait(ds_empty, (g - 1) & 1);
+        uint32_t pk[HALF / 2], dk[HALF / 2];
 #pragma unroll
         for (int ch = 0; ch < HALF / 32; ++ch) {
           const int c0 = wg * HALF + ch * 32;          // first query column of this chunk
@@ -245,41 +245,50 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           ptx::tmem_ld_x32(tmem + lane_base + T_ST + c0, sv);
           ptx::tmem_ld_x32(tmem + lane_base + T_DPT + c0, dpv);
           ptx::tmem_wait_ld();
-          uint32_t pk[16], dk[16];
+          if (ch == HALF / 32 - 1) {
+            // every TMEM read of S^T / dP^T for this tile is done: the MMA warp may overwrite them
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(s_consumed);
+          }
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
             float pp[2], dd[2];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int c = c0 + 2 * e + h;
-              float pv = ptx::ex2(fmaf(__uint_as_float(sv[2 * e + h]), p.scale_log2, -vL2[c]));
+              float pv = ptx::ex2(fmaf(__uint_as_float(sv[2 * e + h]), p.scale_log2, -ptx::lds_f32(vL2 + c * 4)));
               if (need_mask) {
                 const int q_row = i * BM + c;
                 if ((CAUSAL && kv_row > q_row) || kv_row >= N) pv = 0.f;
               }
               pp[h] = pv;
-              dd[h] = pv * (__uint_as_float(dpv[2 * e + h]) - vD[c]);
+              dd[h] = pv * (__uint_as_float(dpv[2 * e + h]) - ptx::lds_f32(vD + c * 4));
             }
-            pk[e] = ptx::pack2<BF16>(pp[0], pp[1]);
-            dk[e] = ptx::pack2<BF16>(dd[0], dd[1]);
-          }
-          // write 32 columns (64 bytes = 4 x 16-B chunks) of row r, 128-B swizzle
-          const int region = c0 / 64;                    // 64-column (128-B) region
-          const int cc0 = (c0 % 64) / 8;                 // first 16-B chunk within the 128-B row
-          uint8_t* rowP = sPT + region * (128 * 128) + (r / 8) * 1024 + (r % 8) * 128;
-          uint8_t* rowS = sDST + region * (128 * 128) + (r / 8) * 1024 + (r % 8) * 128;
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            const int chunk = (cc0 + q4) ^ (r % 8);
-            *reinterpret_cast<uint4*>(rowP + chunk * 16) = make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
-            *reinterpret_cast<uint4*>(rowS + chunk * 16) = make_uint4(dk[4 * q4], dk[4 * q4 + 1], dk[4 * q4 + 2], dk[4 * q4 + 3]);
+            pk[ch * 16 + e] = ptx::pack2<BF16>(pp[0], pp[1]);
+            dk[ch * 16 + e] = ptx::pack2<BF16>(dd[0], dd[1]);
           }
         }
-        // S^T / dP^T fully read (tcgen05.wait::ld above) -> MMA may overwrite them
-        ptx::tc_fence_before();
+        // the previous tile's dV/dK/dQ MMAs must have finished reading P^T / dS^T
+        if (g > 0) ptx::mbar_wait(ds_empty, (g - 1) & 1);
+#pragma unroll
+        for (int ch = 0; ch < HALF / 32; ++ch) {
+          // 32 columns (64 bytes = 4 x 16-B chunks) of row r, 128-B swizzle
+          const int c0 = wg * HALF + ch * 32;
+          const int region = c0 / 64;                    // 64-column (128-B) region
+          const int cc0 = (c0 % 64) / 8;                 // first 16-B chunk within the 128-B row
+          const uint32_t roff = region * (128 * 128) + (r / 8) * 1024 + (r % 8) * 128;
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const uint32_t off = roff + (((cc0 + q4) ^ (r % 8)) * 16);
+            const int b = ch * 16 + 4 * q4;
+            ptx::sts_v4(sPT_a + off, pk[b], pk[b + 1], pk[b + 2], pk[b + 3]);
+            ptx::sts_v4(sDST_a + off, dk[b], dk[b + 1], dk[b + 2], dk[b + 3]);
+          }
+        }
         ptx::fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) { ptx::mbar_arrive(s_consumed); ptx::mbar_arrive(ds_ready); }
+        if (lane == 0) ptx::mbar_arrive(ds_ready);
       }
       // ---- epilogue: dV_j (warpgroup 0), dK_j * scale (warpgroup 1) ----
       ptx::mbar_wait(dkv_full, it & 1);
@@ -312,6 +321,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     const int r = threadIdx.x - 256;                    // 0..127 == TMEM lane
     const uint32_t lane_base = static_cast<uint32_t>((warp % 4) * 32) << 16;
     const bool leader = (r == 0);
+    const uint32_t sDQ_a = ptx::smem_u32(sDQ);
     uint32_t g = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
       int bh, nb;
@@ -320,45 +330,37 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       for (int i = i0; i < n_q_blocks; ++i, ++g) {
         ptx::mbar_wait(dq_full, g & 1);
         ptx::tc_fence_after();
-        // staging buffer free? (previous reduce-add has finished reading it)
-        if (leader) ptx::bulk_wait_read<0>();
-        ptx::named_bar_sync(1, 128);
-        if constexpr (DQT) {
-          // TMEM lane r = head-dim column d, columns = 64 query rows
-#pragma unroll
-          for (int ch = 0; ch < BM / 32; ++ch) {
-            uint32_t v[32];
-            ptx::tmem_ld_x32(tmem + lane_base + T_DQ + ch * 32, v);
-            ptx::tmem_wait_ld();
-            const int dcol = r;
-            uint8_t* box = sDQ + (dcol / 32) * (BM * 128);
-#pragma unroll
-            for (int e = 0; e < 32; ++e) {
-              const int q = ch * 32 + e;
-              const int chunk = ((dcol % 32) / 4) ^ (q % 8);
-              *reinterpret_cast<float*>(box + q * 128 + chunk * 16 + (dcol % 4) * 4) = __uint_as_float(v[e]) * p.scale;
-            }
-          }
-        } else {
-          // TMEM lane r = query row, 64 columns = head dim
-#pragma unroll
-          for (int ch = 0; ch < D / 32; ++ch) {
-            uint32_t v[32];
-            ptx::tmem_ld_x32(tmem + lane_base + T_DQ + ch * 32, v);
-            ptx::tmem_wait_ld();
-            uint8_t* row = sDQ + ch * (BM * 128) + r * 128;
-#pragma unroll
-            for (int c4 = 0; c4 < 8; ++c4) {
-              const int chunk = c4 ^ (r % 8);
-              *reinterpret_cast<float4*>(row + chunk * 16) =
-                  make_float4(__uint_as_float(v[4 * c4]) * p.scale, __uint_as_float(v[4 * c4 + 1]) * p.scale,
-                              __uint_as_float(v[4 * c4 + 2]) * p.scale, __uint_as_float(v[4 * c4 + 3]) * p.scale);
-            }
-          }
-        }
+        uint32_t v[64];
+        ptx::tmem_ld_x32(tmem + lane_base + T_DQ, v);
+        ptx::tmem_ld_x32(tmem + lane_base + T_DQ + 32, v + 32);
+        ptx::tmem_wait_ld();
+        // dQ accumulator in TMEM is free for the next tile's dQ MMA
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(dq_empty);
+        // staging buffer free? (the previous reduce-add has finished reading it)
+        if (leader) ptx::bulk_wait_read<0>();
+        ptx::named_bar_sync(1, 128);
+        if constexpr (DQT) {
+          // TMEM lane r = head-dim column d; 64 columns = the BM = 64 query rows
+          const uint32_t box = sDQ_a + (r / 32) * (BM * 128) + (r % 4) * 4;
+#pragma unroll
+          for (int q = 0; q < 64; ++q)
+            ptx::sts_f32(box + q * 128 + ((((r % 32) / 4) ^ (q % 8)) * 16), __uint_as_float(v[q]) * p.scale);
+        } else {
+          // TMEM lane r = query row; 64 columns = head dim (two 32-column fp32 boxes)
+#pragma unroll
+          for (int ch = 0; ch < 2; ++ch) {
+            const uint32_t row = sDQ_a + ch * (BM * 128) + r * 128;
+#pragma unroll
+            for (int c4 = 0; c4 < 8; ++c4) {
+              const uint32_t* w = v + ch * 32 + 4 * c4;
+              ptx::sts_v4(row + ((c4 ^ (r % 8)) * 16), __float_as_uint(__uint_as_float(w[0]) * p.scale),
+                          __float_as_uint(__uint_as_float(w[1]) * p.scale), __float_as_uint(__uint_as_float(w[2]) * p.scale),
+                          __float_as_uint(__uint_as_float(w[3]) * p.scale));
+            }
+          }
+        }
         ptx::fence_proxy_async_smem();
         ptx::named_bar_sync(1, 128);
         if (leader) {

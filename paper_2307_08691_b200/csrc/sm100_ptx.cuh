@@ -52,7 +52,7 @@ FA2_DEVICE bool mbar_try_wait(uint32_t bar_addr, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 10000;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok) : "r"(bar_addr), "r"(parity) : "memory");
   return ok != 0;
@@ -74,6 +74,16 @@ FA2_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
 #else
   while (!mbar_try_wait(a, parity)) {}
 #endif
+}
+
+FA2_DEVICE float lds_f32(uint32_t addr) {
+  float v; asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr)); return v;
+}
+FA2_DEVICE void sts_f32(uint32_t addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" :: "r"(addr), "f"(v) : "memory");
+}
+FA2_DEVICE void sts_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" :: "r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
 // ----------------------------------------------------------------------------
