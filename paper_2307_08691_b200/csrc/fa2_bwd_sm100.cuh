@@ -123,26 +123,27 @@ fa2_dq_convert(const float* __restrict__ dq_acc, void* __restrict__ dq, int BH, 
 template <int D>
 struct BwdSmem {
   static constexpr int BM = bwd_bm(D);
+  static constexpr bool DST_TMEM = (D == 128);    // dS^T also kept in TMEM (A operand of the dK MMA)
   static constexpr int KV_TILE = 128 * D * 2;     // K_j or V_j
   static constexpr int Q_TILE = BM * D * 2;       // Q_i or dO_i
   static constexpr int Q_SUB = BM * 128;          // one 64-column swizzle box of a Q/dO tile
-  static constexpr int DS_TILE = 128 * BM * 2;    // P^T or dS^T (bf16)
+  static constexpr int DS_TILE = 128 * BM * 2;    // dS^T (bf16), B operand of the dQ MMA
   static constexpr int DQ_TILE = BM * D * 4;      // fp32 staging for the dQ reduce-add
-  static constexpr int STAGES = 2;
+  static constexpr int STAGES = 3;                // Q_i / dO_i / L_i / D_i ring
   static constexpr int OFF_K = 0;
   static constexpr int OFF_V = OFF_K + KV_TILE;
   static constexpr int OFF_Q = OFF_V + KV_TILE;
   static constexpr int OFF_DO = OFF_Q + STAGES * Q_TILE;
-  static constexpr int OFF_PT = OFF_DO + STAGES * Q_TILE;
-  static constexpr int OFF_DST = OFF_PT + DS_TILE;
+  static constexpr int OFF_DST = OFF_DO + STAGES * Q_TILE;
   static constexpr int OFF_DQ = OFF_DST + DS_TILE;
   static constexpr int OFF_VEC = OFF_DQ + DQ_TILE;                 // [STAGES][2][BM] floats: L2, D
   static constexpr int OFF_BAR = OFF_VEC + STAGES * 2 * BM * 4;
-  // kv_full kv_empty q_full[2] q_empty[2] s_full s_consumed ds_ready ds_empty dq_full dq_empty dkv_full dkv_empty
-  static constexpr int NBAR = 14;
+  // kv_full kv_empty q_full[S] q_empty[S] s_full s_consumed ds_ready ds_empty dq_full dq_empty dkv_full dkv_empty
+  static constexpr int NBAR = 10 + 2 * STAGES;
   static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
   static constexpr int BYTES = OFF_TMEM + 16;
   static constexpr int ALLOC = BYTES + 1024;
+  static_assert(ALLOC <= 232448, "shared memory budget");
 };
 
 template <int D, bool BF16, bool CAUSAL>
@@ -152,7 +153,9 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
                const __grid_constant__ CUtensorMap tm_dq, const BwdParams p) {
   using L = BwdSmem<D>;
   constexpr int BM = L::BM;
+  constexpr int STAGES = L::STAGES;
   constexpr bool DQT = (D == 128);          // dQ produced transposed
+  constexpr bool DST_TMEM = L::DST_TMEM;
   constexpr int NSUB = D / 64;
   constexpr int HALF = BM / 2;               // query columns per compute warpgroup
   extern __shared__ uint8_t smem_raw[];
@@ -161,23 +164,22 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   uint8_t* sV = smem + L::OFF_V;
   uint8_t* sQ = smem + L::OFF_Q;
   uint8_t* sDO = smem + L::OFF_DO;
-  uint8_t* sPT = smem + L::OFF_PT;
   uint8_t* sDST = smem + L::OFF_DST;
   uint8_t* sDQ = smem + L::OFF_DQ;
   float* sVec = reinterpret_cast<float*>(smem + L::OFF_VEC);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   uint64_t* kv_full = bars + 0;
   uint64_t* kv_empty = bars + 1;
-  uint64_t* q_full = bars + 2;    // [2]
-  uint64_t* q_empty = bars + 4;   // [2]
-  uint64_t* s_full = bars + 6;
-  uint64_t* s_consumed = bars + 7;
-  uint64_t* ds_ready = bars + 8;
-  uint64_t* ds_empty = bars + 9;
-  uint64_t* dq_full = bars + 10;
-  uint64_t* dq_empty = bars + 11;
-  uint64_t* dkv_full = bars + 12;
-  uint64_t* dkv_empty = bars + 13;
+  uint64_t* q_full = bars + 2;              // [STAGES]
+  uint64_t* q_empty = q_full + STAGES;      // [STAGES]
+  uint64_t* s_full = q_empty + STAGES;
+  uint64_t* s_consumed = s_full + 1;
+  uint64_t* ds_ready = s_full + 2;
+  uint64_t* ds_empty = s_full + 3;
+  uint64_t* dq_full = s_full + 4;
+  uint64_t* dq_empty = s_full + 5;
+  uint64_t* dkv_full = s_full + 6;
+  uint64_t* dkv_empty = s_full + 7;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
 
   const int warp = threadIdx.x / 32;
@@ -185,7 +187,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   if (threadIdx.x == 0) {
     ptx::mbar_init(kv_full, 1);
     ptx::mbar_init(kv_empty, 1);
-    for (int s = 0; s < 2; ++s) { ptx::mbar_init(&q_full[s], 1); ptx::mbar_init(&q_empty[s], 1); }
+    for (int s = 0; s < STAGES; ++s) { ptx::mbar_init(&q_full[s], 1); ptx::mbar_init(&q_empty[s], 1); }
     ptx::mbar_init(s_full, 1);
     ptx::mbar_init(s_consumed, 8);
     ptx::mbar_init(ds_ready, 8);
@@ -205,14 +207,18 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // TMEM columns.  d=128 (BM=64): S^T 0, dP^T 64, dV 128, dK 256, dQ^T 384, P^T 448, dS^T 480 (= 512)
+  //                d=64 (BM=128): S^T 0, dP^T 128, dV 256, dK 320, dQ 384, P^T 448 (= 512)
   constexpr uint32_t T_ST = 0, T_DPT = BM, T_DV = 2 * BM, T_DK = 2 * BM + D, T_DQ = 2 * BM + 2 * D;
+  constexpr uint32_t T_PT = T_DQ + 64, T_DST = T_PT + BM / 2;
+  static_assert(T_PT + BM / 2 + (DST_TMEM ? BM / 2 : 0) <= 512, "TMEM budget");
 
   const int N = p.N;
   const int n_q_blocks = (N + BM - 1) / BM;
   const float* gD = p.dvec;
   const float* gL2 = p.dvec + static_cast<size_t>(p.BH) * p.npad;
 
-  // tile t -> (bh, n_block); heavy (low n_block) first for causal
+  // tile t -> (bh, n_block); for causal, low n_block (more query blocks) first
   auto decode = [&](int t, int& bh, int& nb) { bh = t / p.num_n_blocks; nb = t % p.num_n_blocks; };
   auto q_begin = [&](int nb) -> int { return CAUSAL ? (nb * 128) / BM : 0; };
 
@@ -221,7 +227,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     const int wg = warp / 4;
     const int r = threadIdx.x % 128;                   // key row within the block == TMEM lane
     const uint32_t lane_base = static_cast<uint32_t>((warp % 4) * 32) << 16;
-    const uint32_t sVec_a = ptx::smem_u32(sVec), sPT_a = ptx::smem_u32(sPT), sDST_a = ptx::smem_u32(sDST);
+    const uint32_t sVec_a = ptx::smem_u32(sVec), sDST_a = ptx::smem_u32(sDST);
     uint32_t g = 0;          // global query-tile counter
     int it = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
@@ -230,8 +236,8 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       const int kv_row = nb * 128 + r;
       const int i0 = q_begin(nb);
       for (int i = i0; i < n_q_blocks; ++i, ++g) {
-        const int slot = g & 1;
-        ptx::mbar_wait(&q_full[slot], (g >> 1) & 1);
+        const int slot = g % STAGES;
+        ptx::mbar_wait(&q_full[slot], (g / STAGES) & 1);
         ptx::mbar_wait(s_full, g & 1);
         ptx::tc_fence_after();
         const uint32_t vL2 = sVec_a + slot * 2 * BM * 4;     // L_i * log2(e) for the BM query rows
@@ -271,22 +277,26 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         }
         // the previous tile's dV/dK/dQ MMAs must have finished reading P^T / dS^T
         if (g > 0) ptx::mbar_wait(ds_empty, (g - 1) & 1);
+        ptx::tc_fence_after();
 #pragma unroll
         for (int ch = 0; ch < HALF / 32; ++ch) {
-          // 32 columns (64 bytes = 4 x 16-B chunks) of row r, 128-B swizzle
           const int c0 = wg * HALF + ch * 32;
+          // P^T (and dS^T) rows into TMEM: A operands of the dV (dK) MMAs, 2 values per column
+          ptx::tmem_st_x16(tmem + lane_base + T_PT + c0 / 2, pk + ch * 16);
+          if constexpr (DST_TMEM) ptx::tmem_st_x16(tmem + lane_base + T_DST + c0 / 2, dk + ch * 16);
+          // dS^T row into SMEM (B operand of the dQ MMA): 32 columns = 4 x 16-B chunks, 128-B swizzle
           const int region = c0 / 64;                    // 64-column (128-B) region
           const int cc0 = (c0 % 64) / 8;                 // first 16-B chunk within the 128-B row
           const uint32_t roff = region * (128 * 128) + (r / 8) * 1024 + (r % 8) * 128;
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
-            const uint32_t off = roff + (((cc0 + q4) ^ (r % 8)) * 16);
             const int b = ch * 16 + 4 * q4;
-            ptx::sts_v4(sPT_a + off, pk[b], pk[b + 1], pk[b + 2], pk[b + 3]);
-            ptx::sts_v4(sDST_a + off, dk[b], dk[b + 1], dk[b + 2], dk[b + 3]);
+            ptx::sts_v4(sDST_a + roff + (((cc0 + q4) ^ (r % 8)) * 16), dk[b], dk[b + 1], dk[b + 2], dk[b + 3]);
           }
         }
+        ptx::tmem_wait_st();
         ptx::fence_proxy_async_smem();
+        ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(ds_ready);
       }
@@ -379,24 +389,27 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       constexpr uint32_t IDESC_Q = ptx::idesc_f16(BF16, 128, 64, true, true);     // dQ^T or dQ
       const uint32_t aK = ptx::smem_u32(sK), aV = ptx::smem_u32(sV);
       const uint32_t aQ = ptx::smem_u32(sQ), aDO = ptx::smem_u32(sDO);
-      const uint32_t aPT = ptx::smem_u32(sPT), aDST = ptx::smem_u32(sDST);
+      const uint32_t aDST = ptx::smem_u32(sDST);
       uint32_t g = 0;
       int it = 0;
       uint32_t dkv_uses = 0;
       auto issue_grads = [&](uint32_t h, bool first_in_tile) {
-        const int slot = h & 1;
+        const int slot = h % STAGES;
         ptx::mbar_wait(ds_ready, h & 1);
         ptx::tc_fence_after();
-        // dV += P^T dO_i ; dK += dS^T Q_i   (A: K-major [128 x BM], B: MN-major [BM x D])
+        // dV += P^T dO_i (A = P^T in TMEM);  dK += dS^T Q_i (A = dS^T in TMEM or SMEM); B: MN-major [BM x D]
 #pragma unroll
         for (int k = 0; k < BM / 16; ++k) {
-          const uint32_t aoff = (k / 4) * (128 * 128) + (k % 4) * 32;
           const uint32_t boff = k * 2048;
           const uint32_t acc = (!first_in_tile || k > 0) ? 1u : 0u;
-          ptx::mma_ss(tmem + T_DV, ptx::sw128_desc(aPT + aoff, 16, 1024),
-                      ptx::sw128_desc(aDO + slot * L::Q_TILE + boff, L::Q_SUB, 1024), IDESC_G, acc);
-          ptx::mma_ss(tmem + T_DK, ptx::sw128_desc(aDST + aoff, 16, 1024),
-                      ptx::sw128_desc(aQ + slot * L::Q_TILE + boff, L::Q_SUB, 1024), IDESC_G, acc);
+          ptx::mma_ts(tmem + T_DV, tmem + T_PT + k * 8, ptx::sw128_desc(aDO + slot * L::Q_TILE + boff, L::Q_SUB, 1024),
+                      IDESC_G, acc);
+          if constexpr (DST_TMEM)
+            ptx::mma_ts(tmem + T_DK, tmem + T_DST + k * 8, ptx::sw128_desc(aQ + slot * L::Q_TILE + boff, L::Q_SUB, 1024),
+                        IDESC_G, acc);
+          else
+            ptx::mma_ss(tmem + T_DK, ptx::sw128_desc(aDST + (k / 4) * (128 * 128) + (k % 4) * 32, 16, 1024),
+                        ptx::sw128_desc(aQ + slot * L::Q_TILE + boff, L::Q_SUB, 1024), IDESC_G, acc);
         }
         ptx::mma_commit(&q_empty[slot]);
         if (h > 0) ptx::mbar_wait(dq_empty, (h - 1) & 1);
@@ -423,8 +436,8 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         ptx::tc_fence_after();
         bool have_prev = false;
         for (int i = i0; i < n_q_blocks; ++i, ++g) {
-          const int slot = g & 1;
-          ptx::mbar_wait(&q_full[slot], (g >> 1) & 1);
+          const int slot = g % STAGES;
+          ptx::mbar_wait(&q_full[slot], (g / STAGES) & 1);
           if (g > 0) ptx::mbar_wait(s_consumed, (g - 1) & 1);
           ptx::tc_fence_after();
           // S^T = K_j Q_i^T ; dP^T = V_j dO_i^T   (both operands K-major, K = D)
@@ -469,8 +482,8 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           ptx::tma_load_3d_hint(sV + s * 128 * 128, &tm_v, kv_full, s * 64, nb * 128, bh, pol_kv);
         }
         for (int i = i0; i < n_q_blocks; ++i, ++g) {
-          const int slot = g & 1;
-          if (g >= 2) ptx::mbar_wait(&q_empty[slot], ((g >> 1) - 1) & 1);
+          const int slot = g % STAGES;
+          if (g >= STAGES) ptx::mbar_wait(&q_empty[slot], ((g / STAGES) - 1) & 1);
           ptx::mbar_arrive_expect_tx(&q_full[slot], 2 * L::Q_TILE + 2 * BM * 4);
           for (int s = 0; s < NSUB; ++s) {
             ptx::tma_load_3d_hint(sQ + slot * L::Q_TILE + s * L::Q_SUB, &tm_q, &q_full[slot], s * 64, i * BM, bh, pol_q);
