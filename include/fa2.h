@@ -115,6 +115,11 @@ FA2_API fa2_status_t fa2_kv_block_range(int N, int Br, int Bc, int i, int causal
  * valid until the calls that use it have been issued. */
 FA2_API void fa2_set_timing_events(void* const* events);
 
+/* Debug only: when `dev_buf` (device memory, >= 16384 x uint64) is non-NULL,
+ * the calling thread's fa2_forward launches record clock64() timestamps of the
+ * first work tile of CTA 0 into it (layout documented in fa2_fwd_sm100.cuh). */
+FA2_API void fa2_debug_set_trace(void* dev_buf);
+
 FA2_API const char* fa2_status_string(fa2_status_t s);
 FA2_API const char* fa2_last_error_detail(void);
 /* Number of kernels the last successful fa2_forward / fa2_backward call launched. */

@@ -15,7 +15,7 @@ __all__ = ["lib", "forward", "backward", "backward_preprocess", "backward_worksp
            "attention_step_host", "step_arena_size", "kv_block_range", "set_timing_events", "FA2Error", "LIB_PATH"]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfa2_sm100.so")
+LIB_PATH = os.environ.get("FA2_LIB_PATH") or os.path.join(HERE, "libfa2_sm100.so")
 
 FA2_BF16, FA2_FP16 = 0, 1
 _STATUS = {0: "FA2_OK", 1: "FA2_ERR_INVALID_ARG", 2: "FA2_ERR_UNSUPPORTED", 3: "FA2_ERR_WORKSPACE", 4: "FA2_ERR_CUDA"}
@@ -57,6 +57,8 @@ def lib() -> ctypes.CDLL:
         L.fa2_status_string.restype = ctypes.c_char_p
         L.fa2_last_error_detail.argtypes = []
         L.fa2_last_error_detail.restype = ctypes.c_char_p
+        L.fa2_debug_set_trace.argtypes = [vp]
+        L.fa2_debug_set_trace.restype = None
         L.fa2_set_timing_events.argtypes = [vp]
         L.fa2_set_timing_events.restype = None
         L.fa2_last_launch_count.argtypes = []

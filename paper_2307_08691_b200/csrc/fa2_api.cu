@@ -18,6 +18,7 @@ namespace {
 thread_local std::string g_detail;
 thread_local int g_launches = 0;
 thread_local cudaEvent_t const* g_events = nullptr;   // benchmark timing hook (fa2_set_timing_events)
+thread_local unsigned long long* g_trace = nullptr;     // debug timeline buffer (fa2_debug_set_trace)
 
 inline void mark(int i, cudaStream_t st) {
   if (g_events != nullptr) cudaEventRecord(g_events[i], st);
@@ -162,6 +163,7 @@ fa2_status_t forward_impl(const void* q, const void* k, const void* v, void* o, 
   p.num_m_blocks = (N + 255) / 256;
   p.num_tiles = BH * p.num_m_blocks;
   p.scale_log2 = scale * 1.4426950408889634f;
+  p.trace = g_trace;
   const bool bf16 = dtype == FA2_BF16;
   if (d == 64)
     s = bf16 ? dispatch_fwd_causal<64, true>(causal, mq, mk, mv, p, sms, st)
@@ -287,6 +289,7 @@ const char* fa2_status_string(fa2_status_t s) {
 }
 
 const char* fa2_last_error_detail(void) { return g_detail.c_str(); }
+void fa2_debug_set_trace(void* dev_buf) { g_trace = reinterpret_cast<unsigned long long*>(dev_buf); }
 void fa2_set_timing_events(void* const* events) { g_events = reinterpret_cast<cudaEvent_t const*>(events); }
 int fa2_last_launch_count(void) { return g_launches; }
 

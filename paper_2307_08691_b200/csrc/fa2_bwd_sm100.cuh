@@ -382,87 +382,94 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     }
     if (leader) ptx::bulk_wait<0>();
   } else if (warp == 12) {
-    // ============================ MMA issuer ============================
-    if (lane == 0) {
-      constexpr uint32_t IDESC_S = ptx::idesc_f16(BF16, 128, BM, false, false);   // S^T, dP^T
-      constexpr uint32_t IDESC_G = ptx::idesc_f16(BF16, 128, D, false, true);     // dV, dK
-      constexpr uint32_t IDESC_Q = ptx::idesc_f16(BF16, 128, 64, true, true);     // dQ^T or dQ
-      const uint32_t aK = ptx::smem_u32(sK), aV = ptx::smem_u32(sV);
-      const uint32_t aQ = ptx::smem_u32(sQ), aDO = ptx::smem_u32(sDO);
-      const uint32_t aDST = ptx::smem_u32(sDST);
-      uint32_t g = 0;
-      int it = 0;
-      uint32_t dkv_uses = 0;
-      auto issue_grads = [&](uint32_t h, bool first_in_tile) {
-        const int slot = h % STAGES;
-        ptx::mbar_wait(ds_ready, h & 1);
-        ptx::tc_fence_after();
+    // ================== MMA issuer: whole warp, one elected lane issues ==================
+    constexpr uint32_t IDESC_S = ptx::idesc_f16(BF16, 128, BM, false, false);   // S^T, dP^T
+    constexpr uint32_t IDESC_G = ptx::idesc_f16(BF16, 128, D, false, true);     // dV, dK
+    constexpr uint32_t IDESC_Q = ptx::idesc_f16(BF16, 128, 64, true, true);     // dQ^T or dQ
+    // base descriptors; per-MMA descriptors add (byte offset >> 4) to the start-address field
+    const uint64_t dK_k = ptx::sw128_desc(ptx::smem_u32(sK), 16, 1024);         // K_j, K-major
+    const uint64_t dV_k = ptx::sw128_desc(ptx::smem_u32(sV), 16, 1024);         // V_j, K-major
+    const uint64_t dK_mn = ptx::sw128_desc(ptx::smem_u32(sK), 128 * 128, 1024); // K_j, MN-major
+    const uint64_t dQ_k = ptx::sw128_desc(ptx::smem_u32(sQ), 16, 1024);
+    const uint64_t dO_k = ptx::sw128_desc(ptx::smem_u32(sDO), 16, 1024);
+    const uint64_t dQ_mn = ptx::sw128_desc(ptx::smem_u32(sQ), L::Q_SUB, 1024);
+    const uint64_t dO_mn = ptx::sw128_desc(ptx::smem_u32(sDO), L::Q_SUB, 1024);
+    const uint64_t dS_k = ptx::sw128_desc(ptx::smem_u32(sDST), 16, 1024);
+    const uint64_t dS_mn = ptx::sw128_desc(ptx::smem_u32(sDST), 128 * 128, 1024);
+    uint32_t g = 0;
+    int it = 0;
+    uint32_t dkv_uses = 0;
+    auto issue_grads = [&](uint32_t h, bool first_in_tile) {
+      const uint32_t slot = h % STAGES;
+      ptx::mbar_wait(ds_ready, h & 1);
+      ptx::tc_fence_after();
+      if (ptx::elect_one()) {
         // dV += P^T dO_i (A = P^T in TMEM);  dK += dS^T Q_i (A = dS^T in TMEM or SMEM); B: MN-major [BM x D]
 #pragma unroll
         for (int k = 0; k < BM / 16; ++k) {
-          const uint32_t boff = k * 2048;
+          const uint32_t boff = (slot * L::Q_TILE + k * 2048) >> 4;
           const uint32_t acc = (!first_in_tile || k > 0) ? 1u : 0u;
-          ptx::mma_ts(tmem + T_DV, tmem + T_PT + k * 8, ptx::sw128_desc(aDO + slot * L::Q_TILE + boff, L::Q_SUB, 1024),
-                      IDESC_G, acc);
+          ptx::mma_ts(tmem + T_DV, tmem + T_PT + k * 8, dO_mn + boff, IDESC_G, acc);
           if constexpr (DST_TMEM)
-            ptx::mma_ts(tmem + T_DK, tmem + T_DST + k * 8, ptx::sw128_desc(aQ + slot * L::Q_TILE + boff, L::Q_SUB, 1024),
-                        IDESC_G, acc);
+            ptx::mma_ts(tmem + T_DK, tmem + T_DST + k * 8, dQ_mn + boff, IDESC_G, acc);
           else
-            ptx::mma_ss(tmem + T_DK, ptx::sw128_desc(aDST + (k / 4) * (128 * 128) + (k % 4) * 32, 16, 1024),
-                        ptx::sw128_desc(aQ + slot * L::Q_TILE + boff, L::Q_SUB, 1024), IDESC_G, acc);
+            ptx::mma_ss(tmem + T_DK, dS_k + (((k / 4) * (128 * 128) + (k % 4) * 32) >> 4), dQ_mn + boff, IDESC_G, acc);
         }
         ptx::mma_commit(&q_empty[slot]);
-        if (h > 0) ptx::mbar_wait(dq_empty, (h - 1) & 1);
-        ptx::tc_fence_after();
-        // dQ^T = K^T dS^T  (A = K_j MN-major, B = dS^T MN-major), or dQ = dS K (A = dS^T as MN-major, B = K_j MN-major)
+      }
+      __syncwarp();
+      if (h > 0) ptx::mbar_wait(dq_empty, (h - 1) & 1);
+      ptx::tc_fence_after();
+      if (ptx::elect_one()) {
+        // dQ^T = K^T dS^T (A = K_j MN-major, B = dS^T MN-major), or dQ = dS K (A = dS^T as MN-major, B = K_j MN-major)
 #pragma unroll
         for (int k = 0; k < 128 / 16; ++k) {
-          const uint32_t off = k * 2048;
-          if constexpr (DQT)
-            ptx::mma_ss(tmem + T_DQ, ptx::sw128_desc(aK + off, 128 * 128, 1024), ptx::sw128_desc(aDST + off, 128 * 128, 1024),
-                        IDESC_Q, k > 0 ? 1u : 0u);
-          else
-            ptx::mma_ss(tmem + T_DQ, ptx::sw128_desc(aDST + off, 128 * 128, 1024), ptx::sw128_desc(aK + off, 128 * 128, 1024),
-                        IDESC_Q, k > 0 ? 1u : 0u);
+          const uint32_t off = (k * 2048) >> 4;
+          if constexpr (DQT) ptx::mma_ss(tmem + T_DQ, dK_mn + off, dS_mn + off, IDESC_Q, k > 0 ? 1u : 0u);
+          else ptx::mma_ss(tmem + T_DQ, dS_mn + off, dK_mn + off, IDESC_Q, k > 0 ? 1u : 0u);
         }
         ptx::mma_commit(dq_full);
         ptx::mma_commit(ds_empty);
-      };
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-        int bh, nb;
-        decode(t, bh, nb);
-        const int i0 = q_begin(nb);
-        ptx::mbar_wait(kv_full, it & 1);
+      }
+      __syncwarp();
+    };
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+      int bh, nb;
+      decode(t, bh, nb);
+      const int i0 = q_begin(nb);
+      ptx::mbar_wait(kv_full, it & 1);
+      bool have_prev = false;
+      for (int i = i0; i < n_q_blocks; ++i, ++g) {
+        const uint32_t slot = g % STAGES;
+        ptx::mbar_wait(&q_full[slot], (g / STAGES) & 1);
+        if (g > 0) ptx::mbar_wait(s_consumed, (g - 1) & 1);
         ptx::tc_fence_after();
-        bool have_prev = false;
-        for (int i = i0; i < n_q_blocks; ++i, ++g) {
-          const int slot = g % STAGES;
-          ptx::mbar_wait(&q_full[slot], (g / STAGES) & 1);
-          if (g > 0) ptx::mbar_wait(s_consumed, (g - 1) & 1);
-          ptx::tc_fence_after();
+        if (ptx::elect_one()) {
           // S^T = K_j Q_i^T ; dP^T = V_j dO_i^T   (both operands K-major, K = D)
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) {
-            const uint32_t akv = (k / 4) * (128 * 128) + (k % 4) * 32;
-            const uint32_t aq = (k / 4) * L::Q_SUB + (k % 4) * 32;
-            ptx::mma_ss(tmem + T_ST, ptx::sw128_desc(aK + akv, 16, 1024),
-                        ptx::sw128_desc(aQ + slot * L::Q_TILE + aq, 16, 1024), IDESC_S, k > 0 ? 1u : 0u);
-            ptx::mma_ss(tmem + T_DPT, ptx::sw128_desc(aV + akv, 16, 1024),
-                        ptx::sw128_desc(aDO + slot * L::Q_TILE + aq, 16, 1024), IDESC_S, k > 0 ? 1u : 0u);
+            const uint32_t akv = ((k / 4) * (128 * 128) + (k % 4) * 32) >> 4;
+            const uint32_t aq = (slot * L::Q_TILE + (k / 4) * L::Q_SUB + (k % 4) * 32) >> 4;
+            ptx::mma_ss(tmem + T_ST, dK_k + akv, dQ_k + aq, IDESC_S, k > 0 ? 1u : 0u);
+            ptx::mma_ss(tmem + T_DPT, dV_k + akv, dO_k + aq, IDESC_S, k > 0 ? 1u : 0u);
           }
           ptx::mma_commit(s_full);
-          if (have_prev) issue_grads(g - 1, i - 1 == i0);
-          else if (dkv_uses > 0) {
-            // first query tile of this work tile: previous dK/dV must be drained first
-            ptx::mbar_wait(dkv_empty, (dkv_uses - 1) & 1);
-          }
-          have_prev = true;
         }
-        issue_grads(g - 1, (n_q_blocks - 1) == i0);
-        ++dkv_uses;
+        __syncwarp();
+        if (have_prev) issue_grads(g - 1, i - 1 == i0);
+        else if (dkv_uses > 0) {
+          // first query tile of this work tile: previous dK/dV must be drained first
+          ptx::mbar_wait(dkv_empty, (dkv_uses - 1) & 1);
+        }
+        have_prev = true;
+      }
+      issue_grads(g - 1, (n_q_blocks - 1) == i0);
+      ++dkv_uses;
+      if (ptx::elect_one()) {
         ptx::mma_commit(dkv_full);
         ptx::mma_commit(kv_empty);
       }
+      __syncwarp();
     }
   } else if (warp == 13) {
     // ============================ TMA producer ============================

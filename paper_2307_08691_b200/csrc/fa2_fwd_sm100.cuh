@@ -30,9 +30,17 @@
 #pragma once
 #include <cuda_fp16.h>
 #include <cuda_bf16.h>
+#include <type_traits>
 #include "sm100_ptx.cuh"
 
 namespace fa2 {
+
+// Column pairs (out of every 16) whose exponential runs as a polynomial on the
+// FMA pipe instead of MUFU.EX2 (unmasked blocks only).
+#ifndef FA2_FWD_EMU_PAIRS
+#define FA2_FWD_EMU_PAIRS 4
+#endif
+constexpr int kFwdEmuPairs = FA2_FWD_EMU_PAIRS;
 
 struct FwdParams {
   void* o;             // [BH, N, D] dtype
@@ -41,7 +49,16 @@ struct FwdParams {
   int num_m_blocks;    // ceil(N / 256)
   int num_tiles;       // BH * num_m_blocks
   float scale_log2;    // softmax_scale * log2(e)
+  unsigned long long* trace;  // optional clock64 trace (CTA 0, first tile), nullptr in production
 };
+
+// Debug timeline: trace[(ev * 2 + who) * 64 + j] = clock64() for CTA 0's first
+// work tile (j < 64).  who = sub-tile / MMA-side index.
+#define FA2_TRACE(ev, who, j)                                                          \
+  do {                                                                                 \
+    if (p.trace != nullptr && blockIdx.x == 0 && (j) < 64)                             \
+      p.trace[((ev) * 2 + (who)) * 64 + (j)] = clock64();                              \
+  } while (0)
 
 template <int D>
 struct FwdSmem {
@@ -160,6 +177,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       for (int j = 0; j < nb; ++j) {
         ptx::mbar_wait(&s_full[wg], s_count & 1);
         ++s_count;
+        if (threadIdx.x % 128 == 0 && t == (int)blockIdx.x) FA2_TRACE(0, wg, j);
         ptx::tc_fence_after();
         uint32_t su[128];
         ptx::tmem_ld_x32(tS + 0, su + 0);
@@ -181,6 +199,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         float mx = s[0];
 #pragma unroll
         for (int c = 1; c < 128; ++c) mx = fmaxf(mx, s[c]);
+        if (threadIdx.x % 128 == 0 && t == (int)blockIdx.x) FA2_TRACE(1, wg, j);
         const float m_new = fmaxf(m_used, mx * sl2);
         const bool rescale = (m_new - m_used) > 8.0f;   // also true when m_used == -inf and m_new finite
         float alpha = 1.f;
@@ -189,20 +208,35 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           m_used = m_new;
         }
         const float base = (m_used == -INFINITY) ? 0.f : m_used;
-        float rs = 0.f;
+        const float2 sl2x2 = make_float2(sl2, sl2), nb2 = make_float2(-base, -base);
+        float2 rs2 = make_float2(0.f, 0.f);
+        // exponent x = s * scale * log2(e) - m (FFMA2), P~ = 2^x.  On unmasked blocks
+        // EMU of every 16 column pairs use the FMA-pipe polynomial, the rest MUFU.EX2.
+        auto exp_block = [&](auto emu_tag) {
+          constexpr int EMU = decltype(emu_tag)::value;
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-          uint32_t pk[16];
+          for (int ch = 0; ch < 4; ++ch) {
+            uint32_t pk[16];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const float p0 = ptx::ex2(fmaf(s[ch * 32 + 2 * e], sl2, -base));
-            const float p1 = ptx::ex2(fmaf(s[ch * 32 + 2 * e + 1], sl2, -base));
-            rs += p0 + p1;
-            pk[e] = ptx::pack2<BF16>(p0, p1);
+            for (int e = 0; e < 16; ++e) {
+              const float2 x = ptx::ffma2(make_float2(s[ch * 32 + 2 * e], s[ch * 32 + 2 * e + 1]), sl2x2, nb2);
+              float2 pr;
+              if (e % 16 < EMU) {
+                pr = ptx::exp2_poly2(x);
+              } else {
+                pr.x = ptx::ex2(x.x);
+                pr.y = ptx::ex2(x.y);
+              }
+              rs2 = ptx::fadd2(rs2, pr);
+              pk[e] = ptx::pack2<BF16>(pr.x, pr.y);
+            }
+            ptx::tmem_st_x16(tS + ch * 16, pk);
           }
-          ptx::tmem_st_x16(tS + ch * 16, pk);
-        }
-        l_sum = l_sum * alpha + rs;
+        };
+        if (need_mask) exp_block(std::integral_constant<int, 0>{});
+        else exp_block(std::integral_constant<int, kFwdEmuPairs>{});
+        l_sum = l_sum * alpha + (rs2.x + rs2.y);
+        if (threadIdx.x % 128 == 0 && t == (int)blockIdx.x) FA2_TRACE(2, wg, j);
         // Rescale the un-normalised O accumulator before P~_j V_j is added
         // (needs PV_{j-1} finished; it was issued before S_j, so it usually is).
         if (j > 0 && __any_sync(0xffffffffu, rescale)) {
@@ -222,6 +256,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&p_full[wg]);
+        if (threadIdx.x % 128 == 0 && t == (int)blockIdx.x) FA2_TRACE(3, wg, j);
         ++pv_count;
       }
       // ---- epilogue: O = O / l, L = m + log l (natural log) ----
@@ -251,35 +286,31 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     }
   } else {
     ptx::setmaxnreg_dec<56>();
-    if (warp == 8 && lane == 0) {
-      // ============================ MMA issuer ============================
+    if (warp == 8) {
+      // ================== MMA issuer: whole warp, one elected lane issues ==================
       constexpr uint32_t IDESC_S = ptx::idesc_f16(BF16, 128, 128, false, false);
       constexpr uint32_t IDESC_O = ptx::idesc_f16(BF16, 128, D, false, true);
-      const uint32_t q_addr = ptx::smem_u32(sQ);
-      const uint32_t k_addr = ptx::smem_u32(sK);
-      const uint32_t v_addr = ptx::smem_u32(sV);
+      // base descriptors; per-MMA descriptors add (byte offset >> 4) to the start-address field
+      const uint64_t dQ = ptx::sw128_desc(ptx::smem_u32(sQ), 16, 1024);
+      const uint64_t dK = ptx::sw128_desc(ptx::smem_u32(sK), 16, 1024);
+      const uint64_t dV = ptx::sw128_desc(ptx::smem_u32(sV), L::SUB, 1024);
       int kslot = 0, vslot = 0;
       uint32_t kphase = 0, vphase = 0;
-      uint32_t p_count[2] = {0, 0};
-      uint32_t o_uses[2] = {0, 0};
+      uint32_t p_count0 = 0, p_count1 = 0, o_uses0 = 0, o_uses1 = 0;
       int it = 0;
       auto mma_s = [&](int i, int slot) {
-        const uint32_t qa = q_addr + i * L::TILE;
-        const uint32_t ka = k_addr + slot * L::TILE;
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k / 4) * L::SUB + (k % 4) * 32;
-          ptx::mma_ss(tmem + i * 128, ptx::sw128_desc(qa + off, 16, 1024), ptx::sw128_desc(ka + off, 16, 1024),
-                      IDESC_S, k > 0 ? 1u : 0u);
+          ptx::mma_ss(tmem + i * 128, dQ + ((i * L::TILE + off) >> 4), dK + ((slot * L::TILE + off) >> 4), IDESC_S,
+                      k > 0 ? 1u : 0u);
         }
       };
       auto mma_pv = [&](int i, int slot, bool acc) {
-        const uint32_t va = v_addr + slot * L::TILE;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          ptx::mma_ts(tmem + 256 + i * D, tmem + i * 128 + k * 8, ptx::sw128_desc(va + k * 2048, L::SUB, 1024),
-                      IDESC_O, (acc || k > 0) ? 1u : 0u);
-        }
+        for (int k = 0; k < 8; ++k)
+          ptx::mma_ts(tmem + 256 + i * D, tmem + i * 128 + k * 8, dV + ((slot * L::TILE + k * 2048) >> 4), IDESC_O,
+                      (acc || k > 0) ? 1u : 0u);
       };
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
         int bh, mb;
@@ -288,54 +319,59 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         const int nkv = max(nb0, nb1);
         ptx::mbar_wait(&q_full[0], it & 1);
         ptx::mbar_wait(&q_full[1], it & 1);
-        ptx::tc_fence_after();
         if (nkv > 0) {
           ptx::mbar_wait(&k_full[kslot], kphase);
           ptx::tc_fence_after();
-          if (nb0 > 0) { mma_s(0, kslot); ptx::mma_commit(&s_full[0]); }
-          if (nb1 > 0) { mma_s(1, kslot); ptx::mma_commit(&s_full[1]); }
-          ptx::mma_commit(&k_empty[kslot]);
+          if (ptx::elect_one()) {
+            if (nb0 > 0) { mma_s(0, kslot); ptx::mma_commit(&s_full[0]); }
+            if (nb1 > 0) { mma_s(1, kslot); ptx::mma_commit(&s_full[1]); }
+            ptx::mma_commit(&k_empty[kslot]);
+          }
+          __syncwarp();
           if (++kslot == STAGES) { kslot = 0; kphase ^= 1; }
         }
         for (int j = 0; j < nkv; ++j) {
           ptx::mbar_wait(&v_full[vslot], vphase);
-          const bool next = (j + 1) < nkv;
           bool k_ready = false;
-          for (int i = 0; i < 2; ++i) {
-            const int nbi = i == 0 ? nb0 : nb1;
-            if (j < nbi) {
+          // sub-tile i: O_i += P_i V_j (after softmax i signals P_i), then S_i = Q_i K_{j+1}^T
+          auto step = [&](int i, int nbi, uint32_t& p_count, uint32_t& o_uses) {
+            const bool do_pv = j < nbi, do_s = j + 1 < nbi;
+            if (do_pv) {
               if (j == 0) {
-                if (o_uses[i] > 0) ptx::mbar_wait(&o_empty[i], (o_uses[i] - 1) & 1);
-                ++o_uses[i];
+                if (o_uses > 0) ptx::mbar_wait(&o_empty[i], (o_uses - 1) & 1);
+                ++o_uses;
               }
-              ptx::mbar_wait(&p_full[i], p_count[i] & 1);
-              ++p_count[i];
-              ptx::tc_fence_after();
-              mma_pv(i, vslot, j > 0);
-              ptx::mma_commit(&o_done[i]);
+              ptx::mbar_wait(&p_full[i], p_count & 1);
+              ++p_count;
+              if (it == 0) FA2_TRACE(4, i, j);
             }
-            if (j + 1 < nbi) {
-              if (!k_ready) {
-                ptx::mbar_wait(&k_full[kslot], kphase);
-                ptx::tc_fence_after();
-                k_ready = true;
-              }
-              mma_s(i, kslot);
-              ptx::mma_commit(&s_full[i]);
-            }
-          }
-          ptx::mma_commit(&v_empty[vslot]);
-          if (++vslot == STAGES) { vslot = 0; vphase ^= 1; }
-          if (next) {
-            if (!k_ready) {  // K_{j+1} was not needed by either sub-tile (cannot happen, kept for ring balance)
+            if (do_s && !k_ready) {
               ptx::mbar_wait(&k_full[kslot], kphase);
+              k_ready = true;
             }
-            ptx::mma_commit(&k_empty[kslot]);
-            if (++kslot == STAGES) { kslot = 0; kphase ^= 1; }
+            ptx::tc_fence_after();
+            if (ptx::elect_one()) {
+              if (do_pv) { mma_pv(i, vslot, j > 0); ptx::mma_commit(&o_done[i]); }
+              if (do_s) { mma_s(i, kslot); ptx::mma_commit(&s_full[i]); }
+            }
+            __syncwarp();
+            if (do_s && it == 0) FA2_TRACE(5, i, j);
+          };
+          step(0, nb0, p_count0, o_uses0);
+          step(1, nb1, p_count1, o_uses1);
+          if (ptx::elect_one()) {
+            ptx::mma_commit(&v_empty[vslot]);
+            if (k_ready) ptx::mma_commit(&k_empty[kslot]);
           }
+          __syncwarp();
+          if (++vslot == STAGES) { vslot = 0; vphase ^= 1; }
+          if (k_ready && ++kslot == STAGES) { kslot = 0; kphase ^= 1; }
         }
-        ptx::mma_commit(&q_empty[0]);
-        ptx::mma_commit(&q_empty[1]);
+        if (ptx::elect_one()) {
+          ptx::mma_commit(&q_empty[0]);
+          ptx::mma_commit(&q_empty[1]);
+        }
+        __syncwarp();
       }
     } else if (warp == 9 && lane == 0) {
       // ============================ TMA producer ============================

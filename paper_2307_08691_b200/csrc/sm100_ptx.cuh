@@ -274,6 +274,54 @@ __host__ __device__ constexpr uint32_t idesc_f16(bool bf16, int M, int N, bool a
 FA2_DEVICE float ex2(float x) { float y; asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 FA2_DEVICE float lg2(float x) { float y; asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 
+// Packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2 / FMUL2, two lanes per instruction).
+FA2_DEVICE float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.ftz.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
+FA2_DEVICE float2 fadd2(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.ftz.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+FA2_DEVICE float2 fmul2(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.ftz.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+
+// 2^x for two values on the FMA pipe (offloads the MUFU unit, which is the
+// co-bottleneck of the forward at d=128).  x is clamped to
+// >= -125; x + 1.5*2^23 rounds x to the nearest integer j (RN), f = x - j is in
+// [-0.5, 0.5], 2^f is a degree-3 polynomial (relative error 2.2e-4, below half
+// an ulp of bf16 and fp16 P), and j is added to the exponent field.
+FA2_DEVICE float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = fadd2(x, magic);
+  const float2 j = fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = fadd2(x, make_float2(-j.x, -j.y));
+  float2 p = ffma2(make_float2(0.05286731570959091f, 0.05286731570959091f), f,
+                   make_float2(0.242152139544487f, 0.242152139544487f));
+  p = ffma2(p, f, make_float2(0.6935868263244629f, 0.6935868263244629f));
+  p = ffma2(p, f, make_float2(0.9999627470970154f, 0.9999627470970154f));
+  float2 r;
+  r.x = __int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23));
+  r.y = __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23));
+  return r;
+}
+
 // Pack two fp32 into a 32-bit word of two 16-bit values (lo = a, hi = b), RN.
 template <bool BF16> FA2_DEVICE uint32_t pack2(float a, float b);
 template <> FA2_DEVICE uint32_t pack2<true>(float a, float b) {
