@@ -254,6 +254,7 @@ fa2_status_t backward_impl(const void* q, const void* k, const void* v, const vo
   p.num_tiles = BH * p.num_n_blocks;
   p.scale = scale;
   p.scale_log2 = scale * 1.4426950408889634f;
+  p.trace = g_trace;
   const bool bf16 = dtype == FA2_BF16;
   if (d == 64)
     s = bf16 ? dispatch_bwd_causal<64, true>(causal, maps, p, sms, st) : dispatch_bwd_causal<64, false>(causal, maps, p, sms, st);

@@ -50,7 +50,14 @@ struct BwdParams {
   int num_tiles;        // BH * num_n_blocks
   float scale;
   float scale_log2;
+  unsigned long long* trace;  // optional clock64 trace (CTA 0, first work tile), nullptr in production
 };
+
+// Debug timeline: trace[ev * 64 + h] = clock64() for CTA 0's first 64 query tiles.
+#define FA2_BTRACE(ev, h)                                                                       \
+  do {                                                                                          \
+    if (p.trace != nullptr && blockIdx.x == 0 && (h) < 64) p.trace[(ev) * 64 + (h)] = clock64(); \
+  } while (0)
 
 // ---------------------------------------------------------------------------
 // Preprocess: one warp per row (rows of the padded [BH, npad] grid).
@@ -239,6 +246,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         const int slot = g % STAGES;
         ptx::mbar_wait(&q_full[slot], (g / STAGES) & 1);
         ptx::mbar_wait(s_full, g & 1);
+        if (threadIdx.x == 0) FA2_BTRACE(0, g);
         ptx::tc_fence_after();
         const uint32_t vL2 = sVec_a + slot * 2 * BM * 4;     // L_i * log2(e) for the BM query rows
         const uint32_t vD = vL2 + BM * 4;                     // D_i
@@ -256,6 +264,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(s_consumed);
+            if (threadIdx.x == 0) FA2_BTRACE(1, g);
           }
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
@@ -277,6 +286,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         }
         // the previous tile's dV/dK/dQ MMAs must have finished reading P^T / dS^T
         if (g > 0) ptx::mbar_wait(ds_empty, (g - 1) & 1);
+        if (threadIdx.x == 0) FA2_BTRACE(2, g);
         ptx::tc_fence_after();
 #pragma unroll
         for (int ch = 0; ch < HALF / 32; ++ch) {
@@ -299,6 +309,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(ds_ready);
+        if (threadIdx.x == 0) FA2_BTRACE(3, g);
       }
       // ---- epilogue: dV_j (warpgroup 0), dK_j * scale (warpgroup 1) ----
       ptx::mbar_wait(dkv_full, it & 1);
@@ -339,6 +350,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       const int i0 = q_begin(nb);
       for (int i = i0; i < n_q_blocks; ++i, ++g) {
         ptx::mbar_wait(dq_full, g & 1);
+        if (leader) FA2_BTRACE(7, g);
         ptx::tc_fence_after();
         uint32_t v[64];
         ptx::tmem_ld_x32(tmem + lane_base + T_DQ, v);
@@ -377,6 +389,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 #pragma unroll
           for (int b = 0; b < D / 32; ++b) ptx::tma_reduce_add_3d(&tm_dq, sDQ + b * (BM * 128), b * 32, i * BM, bh);
           ptx::bulk_commit();
+          FA2_BTRACE(8, g);
         }
       }
     }
@@ -402,6 +415,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     auto issue_grads = [&](uint32_t h, bool first_in_tile) {
       const uint32_t slot = h % STAGES;
       ptx::mbar_wait(ds_ready, h & 1);
+      FA2_BTRACE(5, h);
       ptx::tc_fence_after();
       if (ptx::elect_one()) {
         // dV += P^T dO_i (A = P^T in TMEM);  dK += dS^T Q_i (A = dS^T in TMEM or SMEM); B: MN-major [BM x D]
@@ -432,6 +446,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         ptx::mma_commit(ds_empty);
       }
       __syncwarp();
+      FA2_BTRACE(6, h);
     };
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
       int bh, nb;
@@ -443,6 +458,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         const uint32_t slot = g % STAGES;
         ptx::mbar_wait(&q_full[slot], (g / STAGES) & 1);
         if (g > 0) ptx::mbar_wait(s_consumed, (g - 1) & 1);
+        FA2_BTRACE(9, g);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
           // S^T = K_j Q_i^T ; dP^T = V_j dO_i^T   (both operands K-major, K = D)
@@ -456,6 +472,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           ptx::mma_commit(s_full);
         }
         __syncwarp();
+        FA2_BTRACE(4, g);
         if (have_prev) issue_grads(g - 1, i - 1 == i0);
         else if (dkv_uses > 0) {
           // first query tile of this work tile: previous dK/dV must be drained first

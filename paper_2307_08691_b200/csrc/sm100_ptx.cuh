@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cuda.h>
+#include <cuda_fp16.h>
 
 #ifndef FA2_DEVICE
 #define FA2_DEVICE __device__ __forceinline__
