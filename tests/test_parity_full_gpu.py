@@ -1,0 +1,68 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (persistent grid over all B*H*row-blocks), checked against the CPU oracle
+on sampled outputs the oracle computes row by row (oracle.forward_rows,
+oracle.backward_sampled_head).  DESIGN.md §4."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2307_08691_b200 as fa2
+import workloads as W
+from oracle import ref_attention as R
+from tests.gpu_util import TOL, half_ulp, scale_for
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+FULL = [  # name, B, H, N, d, causal, dtype, check backward
+    ("PS128_N8192", 2, 16, 8192, 128, False, "bf16", True),      # bench.py workload (configs[2])
+    ("PS64_N16384_causal", 1, 32, 16384, 64, True, "bf16", True),  # configs[1] largest N
+    ("PS64_N512", 32, 32, 512, 64, False, "bf16", True),         # configs[1] smallest N
+    ("GPT_N8192_causal", 8, 20, 8192, 128, True, "bf16", True),  # configs[3]
+    ("LC_N32768_causal", 1, 16, 32768, 128, True, "fp16", True), # configs[4]
+    ("LC_N65536_causal", 1, 16, 65536, 128, True, "fp16", False),
+]
+
+
+def _rows(N, rng, k=12):
+    r = {0, 1, 127, 128, N // 2, N - 129, N - 1}
+    r |= set(rng.integers(0, N, size=k).tolist())
+    return np.array(sorted(x for x in r if 0 <= x < N))
+
+
+@pytest.mark.parametrize("case", FULL, ids=[c[0] for c in FULL])
+def test_full_size_sampled(case):
+    name, B, H, N, d, causal, dtype, check_bwd = case
+    torch.cuda.empty_cache()
+    q, k, v, do = W.qkv(B, H, N, d, dtype, seed=500 + [c[0] for c in FULL].index(name))
+    sc = scale_for(d)
+    qc, kc, vc, doc = q.cuda(), k.cuda(), v.cuda(), do.cuda()
+    o, lse = fa2.forward(qc, kc, vc, causal=causal, softmax_scale=sc)
+    if check_bwd:
+        dq, dk, dv = fa2.backward(qc, kc, vc, o, lse, doc, causal=causal, softmax_scale=sc)
+    torch.cuda.synchronize()
+    assert torch.isfinite(o).all() and torch.isfinite(lse).all()
+    rng = np.random.default_rng(0)
+    heads = sorted({(0, 0), (B - 1, H - 1), (B // 2, H // 3)})
+    f64 = lambda t: t.double().numpy()
+    for (b, h) in heads:
+        qh, kh, vh = f64(q[b, h]), f64(k[b, h]), f64(v[b, h])
+        rows = _rows(N, rng)
+        _, o_ref, l_ref = R.forward_rows(qh, kh, vh, sc, causal, rows=rows)
+        o_gpu = o[b, h, rows].double().cpu().numpy()
+        ex = float(np.max(np.abs(o_gpu - o_ref) - half_ulp(o_ref, dtype)))
+        el = float(np.max(np.abs(lse[b, h, rows].double().cpu().numpy() - l_ref)))
+        assert ex <= TOL[dtype]["O"], (name, b, h, "O", ex)
+        assert el <= TOL[dtype]["L"], (name, b, h, "L", el)
+    if check_bwd:
+        b, h = heads[-1]
+        rows = _rows(N, rng, 6)
+        cols = _rows(N, rng, 6)
+        sm = R.backward_sampled_head(f64(q[b, h]), f64(k[b, h]), f64(v[b, h]), f64(do[b, h]), sc, causal,
+                                     dq_rows=rows, dkv_cols=cols, rows_per_chunk=1024)
+        got = {"dq": dq[b, h, rows], "dk": dk[b, h, cols], "dv": dv[b, h, cols]}
+        floor = 2.0 ** -8 * max(float(np.max(np.abs(sm[x]))) for x in ("dq", "dk", "dv"))
+        for x in ("dq", "dk", "dv"):
+            ref = sm[x]
+            err = float(np.max(np.abs(got[x].double().cpu().numpy() - ref)))
+            lim = TOL[dtype]["grad"] * max(float(np.max(np.abs(ref))), floor)
+            assert err <= lim, (name, x, err, lim)
