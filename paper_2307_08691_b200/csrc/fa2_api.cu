@@ -12,6 +12,7 @@
 #include "../../include/fa2.h"
 #include "fa2_fwd_sm100.cuh"
 #include "fa2_bwd_sm100.cuh"
+#include "fa2_bwd128_sm100.cuh"
 
 namespace {
 
@@ -202,8 +203,9 @@ fa2_status_t preprocess_impl(const void* o, const void* dout, const float* lse, 
 
 template <int D, bool BF16, bool CAUSAL>
 fa2_status_t launch_bwd(const fa2::BwdMaps& maps, const fa2::BwdParams& p, int sms, cudaStream_t st) {
-  auto kern = fa2::fa2_bwd_kernel<D, BF16, CAUSAL>;
-  constexpr int smem = fa2::BwdSmem<D>::ALLOC;
+  // d = 128: double-region TMEM pipeline (fa2_bwd128_sm100.cuh); d = 64: fa2_bwd_kernel
+  auto kern = D == 128 ? fa2::fa2_bwd128_kernel<BF16, CAUSAL> : fa2::fa2_bwd_kernel<D, BF16, CAUSAL>;
+  constexpr int smem = D == 128 ? fa2::Bwd128Smem::ALLOC : fa2::BwdSmem<D>::ALLOC;
   fa2_status_t s = set_smem(kern, smem);
   if (s != FA2_OK) return s;
   const int grid = p.num_tiles < sms ? p.num_tiles : sms;
@@ -247,6 +249,7 @@ fa2_status_t backward_impl(const void* q, const void* k, const void* v, const vo
   p.dvec = dvec;
   p.dk = dk;
   p.dv = dv;
+  p.dq_acc = dq_acc;
   p.BH = BH;
   p.N = N;
   p.npad = static_cast<int>(npad);

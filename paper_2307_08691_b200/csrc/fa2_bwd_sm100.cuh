@@ -45,6 +45,7 @@ struct BwdParams {
   const float* dvec;    // workspace: [BH, npad] D, followed by [BH, npad] L*log2(e)
   void* dk;
   void* dv;
+  float* dq_acc;        // fp32 dQ accumulator ([BH, npad, D], or [BH, D, npad] when transposed)
   int BH, N, npad;
   int num_n_blocks;     // ceil(N / 128)
   int num_tiles;        // BH * num_n_blocks
@@ -432,7 +433,9 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         ptx::mma_commit(&q_empty[slot]);
       }
       __syncwarp();
+      FA2_BTRACE(12, h);
       if (h > 0) ptx::mbar_wait(dq_empty, (h - 1) & 1);
+      FA2_BTRACE(13, h);
       ptx::tc_fence_after();
       if (ptx::elect_one()) {
         // dQ^T = K^T dS^T (A = K_j MN-major, B = dS^T MN-major), or dQ = dS K (A = dS^T as MN-major, B = K_j MN-major)
@@ -456,7 +459,9 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       bool have_prev = false;
       for (int i = i0; i < n_q_blocks; ++i, ++g) {
         const uint32_t slot = g % STAGES;
+        FA2_BTRACE(10, g);
         ptx::mbar_wait(&q_full[slot], (g / STAGES) & 1);
+        FA2_BTRACE(11, g);
         if (g > 0) ptx::mbar_wait(s_consumed, (g - 1) & 1);
         FA2_BTRACE(9, g);
         ptx::tc_fence_after();

@@ -19,17 +19,15 @@ fa2.lib().fa2_debug_set_trace(None)
 torch.cuda.synchronize()
 t = tr.cpu().view(-1, 64)
 names = ["c:s_full", "c:s_cons", "c:ds_empty", "c:ds_ready", "m:S_iss", "m:ds_rdy", "m:dQ_iss", "q:dq_full", "q:red_iss", "m:S_start"]
-base = int(t[9][0])
+base = int(t[0][0])
 print("h  | " + " ".join(f"{n:>10s}" for n in names))
 for h in range(0, 64, 7):
-    print(f"{h:2d} | " + " ".join(f"{int(t[e][h]) - base:10d}" for e in range(10)))
+    print(f"{h:2d} | " + " ".join(f"{(int(t[e][h]) - base) if int(t[e][h]) else 0:10d}" for e in range(10)))
 rng = range(8, 60)
 def avg(a, b, lag=0):
     return statistics.mean(int(t[b][h + lag]) - int(t[a][h]) for h in rng)
-print("period (S issue start):", avg(9, 9, 1))
-print("mma: S_start->S_issued", avg(9, 4), " S_issued->ds_ready(h-1) seen", avg(4, 5, -1) if False else "", )
-print("compute: s_full->s_consumed", avg(0, 1), " s_consumed->ds_empty ok", avg(1, 2), " ds_empty->ds_ready", avg(2, 3))
-print("mma: S_start(h) -> s_full seen by compute(h)", avg(9, 0))
-print("mma: ds_ready(h) arrive -> mma sees", avg(3, 5), "  grads issue (h):", avg(5, 6))
-print("dq: dq_full seen - dQ issued", avg(6, 7), "  dq reduce issued - dq_full", avg(7, 8))
-print("mma: dQ_iss(h) -> S_start(h+2)", avg(6, 9, 2))
+print("period (compute s_full):", avg(0, 0, 1))
+print("compute: s_full -> ds_ready arrive", avg(0, 3))
+print("mma: ds_ready arrive -> seen", avg(3, 5), "  grads issue", avg(5, 6))
+print("mma: dQ issued(h) -> S/dP(h+2) issued", avg(6, 4, 2), "   S/dP(h) issued -> compute sees s_full(h)", avg(4, 0))
+print("dq: dQ issued -> dq_full seen", avg(6, 7), "  dq_full -> reduce issued", avg(7, 8))
