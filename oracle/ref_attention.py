@@ -265,3 +265,45 @@ def naive_softmax_no_max(s: np.ndarray) -> np.ndarray:
     with np.errstate(over="ignore", invalid="ignore"):
         e = np.exp(s)
         return e / np.sum(e, axis=1, keepdims=True)
+
+
+# ---------------------------------------------------------------------------
+# MQA / GQA: query head h uses key/value head h // group, where
+# group = H / H_kv; "implicitly manipulate the indices into the head" for the
+# forward, and "sum the gradients dK and dV across different heads that were
+# implicitly duplicated" for the backward.
+# ---------------------------------------------------------------------------
+
+def forward_gqa(q, k, v, scale: float, causal: bool):
+    """q [B,H,N,d], k/v [B,H_kv,N,d] -> (O [B,H,N,d], L [B,H,N])."""
+    q = np.asarray(q)
+    b, h, n, d = q.shape
+    h_kv = np.asarray(k).shape[1]
+    if h % h_kv:
+        raise ValueError("H must be a multiple of H_kv")
+    group = h // h_kv
+    o = np.empty((b, h, n, d))
+    lse = np.empty((b, h, n))
+    for bi in range(b):
+        for hi in range(h):
+            o[bi, hi], lse[bi, hi] = forward_head(q[bi, hi], k[bi, hi // group], v[bi, hi // group], scale, causal)
+    return o, lse
+
+
+def backward_gqa(q, k, v, do, scale: float, causal: bool):
+    """Returns (dQ [B,H,N,d], dK [B,H_kv,N,d], dV [B,H_kv,N,d]); dK/dV of a
+    key/value head are the sums over the query heads of its group."""
+    q = np.asarray(q)
+    b, h, n, d = q.shape
+    h_kv = np.asarray(k).shape[1]
+    group = h // h_kv
+    dq = np.empty((b, h, n, d))
+    dk = np.zeros((b, h_kv, n, d))
+    dv = np.zeros((b, h_kv, n, d))
+    for bi in range(b):
+        for hi in range(h):
+            g = hi // group
+            dq[bi, hi], dkh, dvh, _ = backward_head(q[bi, hi], k[bi, g], v[bi, g], do[bi, hi], scale, causal)
+            dk[bi, g] += dkh
+            dv[bi, g] += dvh
+    return dq, dk, dv

@@ -416,3 +416,49 @@ def test_batched_wrappers():
             assert np.array_equal(o[b, h], o1) and np.array_equal(lse[b, h], l1)
             g = R.backward_head(q[b, h], k[b, h], v[b, h], do[b, h], 0.5, True)
             assert np.array_equal(dq[b, h], g[0]) and np.array_equal(dv[b, h], g[2])
+
+
+# --------------------------------------------------------------------------
+# MQA / GQA
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("h,h_kv", [(4, 4), (4, 2), (6, 1)])
+def test_gqa_equals_explicit_duplication(h, h_kv, causal):
+    """GQA through index manipulation == MHA on explicitly repeated K/V, with
+    dK/dV of the duplicated heads summed back (the paper's two statements)."""
+    r = rng(50 + h + h_kv)
+    b, n, d = 2, 11, 4
+    q = r.normal(size=(b, h, n, d))
+    k = r.normal(size=(b, h_kv, n, d))
+    v = r.normal(size=(b, h_kv, n, d))
+    do = r.normal(size=(b, h, n, d))
+    grp = h // h_kv
+    kr, vr = np.repeat(k, grp, axis=1), np.repeat(v, grp, axis=1)
+    o, lse = R.forward_gqa(q, k, v, 0.5, causal)
+    o2, l2 = R.forward(q, kr, vr, 0.5, causal)
+    assert np.array_equal(o, o2) and np.array_equal(lse, l2)
+    dq, dk, dv = R.backward_gqa(q, k, v, do, 0.5, causal)
+    dq2, dk2, dv2, _ = R.backward(q, kr, vr, do, 0.5, causal)
+    assert np.max(np.abs(dq - dq2)) < 1e-13
+    assert np.max(np.abs(dk - dk2.reshape(b, h_kv, grp, n, d).sum(2))) < 1e-12
+    assert np.max(np.abs(dv - dv2.reshape(b, h_kv, grp, n, d).sum(2))) < 1e-12
+
+
+def test_gqa_finite_differences():
+    r = rng(61)
+    b, h, h_kv, n, d = 1, 4, 2, 7, 3
+    q = r.normal(size=(b, h, n, d))
+    k = r.normal(size=(b, h_kv, n, d))
+    v = r.normal(size=(b, h_kv, n, d))
+    g = r.normal(size=(b, h, n, d))
+    dq, dk, dv = R.backward_gqa(q, k, v, g, 0.7, True)
+    f = lambda qq, kk, vv: float(np.sum(R.forward_gqa(qq, kk, vv, 0.7, True)[0] * g))
+    eps = 1e-6
+    for which, grad, idx in ((1, dk, (0, 1, 3, 2)), (2, dv, (0, 0, 5, 1)), (0, dq, (0, 3, 6, 0))):
+        args = [q.copy(), k.copy(), v.copy()]
+        args[which][idx] += eps
+        fp = f(*args)
+        args[which][idx] -= 2 * eps
+        fm = f(*args)
+        assert abs((fp - fm) / (2 * eps) - grad[idx]) < 1e-7
