@@ -80,6 +80,21 @@ FA2_API fa2_status_t fa2_backward(const void* q, const void* k, const void* v, c
                           int B, int H, int N, int d, int causal, float softmax_scale,
                           fa2_dtype_t dtype, void* stream);
 
+/* Multi-query / grouped-query attention: q, o, dout, dq are
+ * [B,H,N,d]; k, v, dk, dv are [B,H_kv,N,d] with H a multiple of H_kv.  Query
+ * head h attends with key/value head h / (H/H_kv) ("implicitly manipulate the
+ * indices into the head"); dk, dv are the sums over the H/H_kv query heads of
+ * each group (computed inside one work tile, no atomics).  H_kv == H is
+ * exactly fa2_forward / fa2_backward.  Workspace: fa2_backward_workspace_size(B,H,N,d). */
+FA2_API fa2_status_t fa2_forward_gqa(const void* q, const void* k, const void* v, void* o, float* lse,
+                                     int B, int H, int H_kv, int N, int d, int causal, float softmax_scale,
+                                     fa2_dtype_t dtype, void* stream);
+FA2_API fa2_status_t fa2_backward_gqa(const void* q, const void* k, const void* v, const void* o,
+                                      const float* lse, const void* dout, void* dq, void* dk, void* dv,
+                                      void* workspace, size_t workspace_bytes,
+                                      int B, int H, int H_kv, int N, int d, int causal, float softmax_scale,
+                                      fa2_dtype_t dtype, void* stream);
+
 /* D = rowsum(dO o O) alone, into d_out [B,H,N] fp32 (device).  Exposed
  * so the preprocessing step can be checked on its own; fa2_backward runs it
  * internally. */

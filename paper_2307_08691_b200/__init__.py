@@ -41,6 +41,10 @@ def lib() -> ctypes.CDLL:
         vp, i, f, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_float, ctypes.c_size_t
         L.fa2_forward.argtypes = [vp, vp, vp, vp, vp, i, i, i, i, i, f, i, vp]
         L.fa2_forward.restype = i
+        L.fa2_forward_gqa.argtypes = [vp, vp, vp, vp, vp, i, i, i, i, i, i, f, i, vp]
+        L.fa2_forward_gqa.restype = i
+        L.fa2_backward_gqa.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, i, i, i, i, i, i, f, i, vp]
+        L.fa2_backward_gqa.restype = i
         L.fa2_backward.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, i, i, i, i, i, f, i, vp]
         L.fa2_backward.restype = i
         L.fa2_backward_preprocess.argtypes = [vp, vp, vp, i, i, i, i, i, vp]
@@ -97,24 +101,34 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
 
 
-def _need(t, like, name):
-    if t.shape != like.shape or t.dtype != like.dtype or not t.is_contiguous() or t.device != like.device:
-        raise FA2Error(1, f"{name} must be a contiguous {tuple(like.shape)} {like.dtype} tensor on {like.device}")
+def _need(t, like, name, heads=None):
+    shape = tuple(like.shape) if heads is None else (like.shape[0], heads, like.shape[2], like.shape[3])
+    if tuple(t.shape) != shape or t.dtype != like.dtype or not t.is_contiguous() or t.device != like.device:
+        raise FA2Error(1, f"{name} must be a contiguous {shape} {like.dtype} tensor on {like.device}")
+
+
+def _kv_heads(q, k):
+    hkv = k.shape[1] if k.dim() == 4 else -1
+    if hkv < 1 or q.shape[1] % hkv:
+        raise FA2Error(1, f"key/value heads ({hkv}) must divide query heads ({q.shape[1]})")
+    return hkv
 
 
 def forward(q, k, v, causal: bool = False, softmax_scale: float | None = None, out=None, lse=None, stream=None):
-    """O, L for [B,H,N,d] bf16/fp16 CUDA tensors (Alg. 1).  Returns (o, lse[B,H,N] fp32)."""
+    """O, L for [B,H,N,d] bf16/fp16 CUDA tensors (Alg. 1).  k, v may have
+    H_kv < H heads (MQA/GQA).  Returns (o, lse[B,H,N] fp32)."""
     import torch
     B, H, N, d = _shape(q)
+    Hkv = _kv_heads(q, k)
     for t, n in ((k, "k"), (v, "v")):
-        _need(t, q, n)
+        _need(t, q, n, Hkv)
     if not q.is_contiguous():
         raise FA2Error(1, "q must be contiguous")
     scale = 1.0 / math.sqrt(d) if softmax_scale is None else float(softmax_scale)
     o = torch.empty_like(q) if out is None else out
     L = torch.empty((B, H, N), dtype=torch.float32, device=q.device) if lse is None else lse
-    _check(lib().fa2_forward(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(L), B, H, N, d, int(bool(causal)),
-                             scale, _dtype_code(q), ctypes.c_void_p(_stream(stream))))
+    _check(lib().fa2_forward_gqa(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(L), B, H, Hkv, N, d, int(bool(causal)),
+                                 scale, _dtype_code(q), ctypes.c_void_p(_stream(stream))))
     return o, L
 
 
@@ -124,10 +138,14 @@ def backward_workspace_size(B: int, H: int, N: int, d: int) -> int:
 
 def backward(q, k, v, o, lse, do, causal: bool = False, softmax_scale: float | None = None,
              dq=None, dk=None, dv=None, workspace=None, stream=None):
-    """dQ, dK, dV (Alg. 2, P:403-442).  Returns (dq, dk, dv)."""
+    """dQ, dK, dV (Alg. 2).  With H_kv < H key/value heads, dK/dV are
+    summed over each group of query heads.  Returns (dq, dk, dv)."""
     import torch
     B, H, N, d = _shape(q)
-    for t, n in ((k, "k"), (v, "v"), (o, "o"), (do, "do")):
+    Hkv = _kv_heads(q, k)
+    for t, n in ((k, "k"), (v, "v")):
+        _need(t, q, n, Hkv)
+    for t, n in ((o, "o"), (do, "do")):
         _need(t, q, n)
     scale = 1.0 / math.sqrt(d) if softmax_scale is None else float(softmax_scale)
     dq = torch.empty_like(q) if dq is None else dq
@@ -136,10 +154,10 @@ def backward(q, k, v, o, lse, do, causal: bool = False, softmax_scale: float | N
     wsz = backward_workspace_size(B, H, N, d)
     if workspace is None:
         workspace = torch.empty(wsz, dtype=torch.uint8, device=q.device)
-    _check(lib().fa2_backward(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk),
-                              _ptr(dv), _ptr(workspace), workspace.numel() * workspace.element_size(),
-                              B, H, N, d, int(bool(causal)), scale, _dtype_code(q),
-                              ctypes.c_void_p(_stream(stream))))
+    _check(lib().fa2_backward_gqa(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk),
+                                  _ptr(dv), _ptr(workspace), workspace.numel() * workspace.element_size(),
+                                  B, H, Hkv, N, d, int(bool(causal)), scale, _dtype_code(q),
+                                  ctypes.c_void_p(_stream(stream))))
     return dq, dk, dv
 
 

@@ -147,19 +147,22 @@ fa2_status_t dispatch_fwd_causal(bool causal, const CUtensorMap& mq, const CUten
   return causal ? launch_fwd<D, BF16, true>(mq, mk, mv, p, sms, st) : launch_fwd<D, BF16, false>(mq, mk, mv, p, sms, st);
 }
 
-fa2_status_t forward_impl(const void* q, const void* k, const void* v, void* o, float* lse, int B, int H, int N,
-                          int d, int causal, float scale, fa2_dtype_t dtype, cudaStream_t st, int sms) {
+fa2_status_t forward_impl(const void* q, const void* k, const void* v, void* o, float* lse, int B, int H, int Hkv,
+                          int N, int d, int causal, float scale, fa2_dtype_t dtype, cudaStream_t st, int sms) {
   const int BH = B * H;
   CUtensorMap mq, mk, mv;
   const CUtensorMapDataType dt = tma_dtype(dtype);
   fa2_status_t s;
   if ((s = make_map_3d(&mq, q, dt, 2, d, N, BH, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
-  if ((s = make_map_3d(&mk, k, dt, 2, d, N, BH, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
-  if ((s = make_map_3d(&mv, v, dt, 2, d, N, BH, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
+  if ((s = make_map_3d(&mk, k, dt, 2, d, N, B * Hkv, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
+  if ((s = make_map_3d(&mv, v, dt, 2, d, N, B * Hkv, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
   fa2::FwdParams p;
   p.o = o;
   p.lse = lse;
   p.BH = BH;
+  p.H = H;
+  p.Hkv = Hkv;
+  p.group = H / Hkv;
   p.N = N;
   p.num_m_blocks = (N + 255) / 256;
   p.num_tiles = BH * p.num_m_blocks;
@@ -223,8 +226,8 @@ fa2_status_t dispatch_bwd_causal(bool causal, const fa2::BwdMaps& maps, const fa
 }
 
 fa2_status_t backward_impl(const void* q, const void* k, const void* v, const void* o, const float* lse,
-                           const void* dout, void* dq, void* dk, void* dv, void* ws, int B, int H, int N, int d,
-                           int causal, float scale, fa2_dtype_t dtype, cudaStream_t st, int sms) {
+                           const void* dout, void* dq, void* dk, void* dv, void* ws, int B, int H, int Hkv, int N,
+                           int d, int causal, float scale, fa2_dtype_t dtype, cudaStream_t st, int sms) {
   const int BH = B * H;
   const size_t npad = pad128(N);
   float* dq_acc = reinterpret_cast<float*>(ws);
@@ -238,8 +241,8 @@ fa2_status_t backward_impl(const void* q, const void* k, const void* v, const vo
   const int bm = fa2::bwd_bm(d);
   if ((s = make_map_3d(&maps.q, q, dt, 2, d, N, BH, 64, bm, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
   if ((s = make_map_3d(&maps.dout, dout, dt, 2, d, N, BH, 64, bm, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
-  if ((s = make_map_3d(&maps.k, k, dt, 2, d, N, BH, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
-  if ((s = make_map_3d(&maps.v, v, dt, 2, d, N, BH, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
+  if ((s = make_map_3d(&maps.k, k, dt, 2, d, N, B * Hkv, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
+  if ((s = make_map_3d(&maps.v, v, dt, 2, d, N, B * Hkv, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
   // fp32 dQ accumulator [BH, npad, d]; reduce-add boxes of 32 columns x BM rows (128-B swizzle rows)
   if ((s = make_map_3d(&maps.dq_acc, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, d, static_cast<int>(npad), BH, 32,
                        bm, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK)
@@ -251,10 +254,13 @@ fa2_status_t backward_impl(const void* q, const void* k, const void* v, const vo
   p.dv = dv;
   p.dq_acc = dq_acc;
   p.BH = BH;
+  p.H = H;
+  p.Hkv = Hkv;
+  p.group = H / Hkv;
   p.N = N;
   p.npad = static_cast<int>(npad);
   p.num_n_blocks = (N + 127) / 128;
-  p.num_tiles = BH * p.num_n_blocks;
+  p.num_tiles = B * Hkv * p.num_n_blocks;   // one work tile per (key/value head, key block)
   p.scale = scale;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.trace = g_trace;
@@ -318,17 +324,24 @@ fa2_status_t fa2_kv_block_range(int N, int Br, int Bc, int i, int causal, int* n
   return FA2_OK;
 }
 
-fa2_status_t fa2_forward(const void* q, const void* k, const void* v, void* o, float* lse, int B, int H, int N, int d,
-                         int causal, float softmax_scale, fa2_dtype_t dtype, void* stream) {
+fa2_status_t fa2_forward_gqa(const void* q, const void* k, const void* v, void* o, float* lse, int B, int H, int H_kv,
+                             int N, int d, int causal, float softmax_scale, fa2_dtype_t dtype, void* stream) {
   g_detail.clear();
   fa2_status_t s = check_common(B, H, N, d, softmax_scale, dtype, true);
   if (s != FA2_OK) return s;
+  if (H_kv < 1 || H % H_kv != 0) return fail(FA2_ERR_INVALID_ARG, "H=%d must be a positive multiple of H_kv=%d", H, H_kv);
   if ((s = check_ptrs({q, k, v, o, lse})) != FA2_OK) return s;
   DeviceInfo di;
   if ((s = device_info(di)) != FA2_OK) return s;
-  s = forward_impl(q, k, v, o, lse, B, H, N, d, causal, softmax_scale, dtype, static_cast<cudaStream_t>(stream), di.sms);
+  s = forward_impl(q, k, v, o, lse, B, H, H_kv, N, d, causal, softmax_scale, dtype, static_cast<cudaStream_t>(stream),
+                   di.sms);
   if (s == FA2_OK) g_launches = 1;
   return s;
+}
+
+fa2_status_t fa2_forward(const void* q, const void* k, const void* v, void* o, float* lse, int B, int H, int N, int d,
+                         int causal, float softmax_scale, fa2_dtype_t dtype, void* stream) {
+  return fa2_forward_gqa(q, k, v, o, lse, B, H, H, N, d, causal, softmax_scale, dtype, stream);
 }
 
 size_t fa2_backward_workspace_size(int B, int H, int N, int d) {
@@ -340,9 +353,18 @@ fa2_status_t fa2_backward(const void* q, const void* k, const void* v, const voi
                           const void* dout, void* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes,
                           int B, int H, int N, int d, int causal, float softmax_scale, fa2_dtype_t dtype,
                           void* stream) {
+  return fa2_backward_gqa(q, k, v, o, lse, dout, dq, dk, dv, workspace, workspace_bytes, B, H, H, N, d, causal,
+                          softmax_scale, dtype, stream);
+}
+
+fa2_status_t fa2_backward_gqa(const void* q, const void* k, const void* v, const void* o, const float* lse,
+                              const void* dout, void* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes,
+                              int B, int H, int H_kv, int N, int d, int causal, float softmax_scale, fa2_dtype_t dtype,
+                              void* stream) {
   g_detail.clear();
   fa2_status_t s = check_common(B, H, N, d, softmax_scale, dtype, true);
   if (s != FA2_OK) return s;
+  if (H_kv < 1 || H % H_kv != 0) return fail(FA2_ERR_INVALID_ARG, "H=%d must be a positive multiple of H_kv=%d", H, H_kv);
   if ((s = check_ptrs({q, k, v, o, lse, dout, dq, dk, dv})) != FA2_OK) return s;
   if (workspace == nullptr || !aligned16(workspace))
     return fail(FA2_ERR_WORKSPACE, "workspace is NULL or not 16-byte aligned");
@@ -351,7 +373,7 @@ fa2_status_t fa2_backward(const void* q, const void* k, const void* v, const voi
                 fa2_backward_workspace_size(B, H, N, d));
   DeviceInfo di;
   if ((s = device_info(di)) != FA2_OK) return s;
-  s = backward_impl(q, k, v, o, lse, dout, dq, dk, dv, workspace, B, H, N, d, causal, softmax_scale, dtype,
+  s = backward_impl(q, k, v, o, lse, dout, dq, dk, dv, workspace, B, H, H_kv, N, d, causal, softmax_scale, dtype,
                     static_cast<cudaStream_t>(stream), di.sms);
   if (s == FA2_OK) g_launches = 3;
   return s;
@@ -418,8 +440,8 @@ fa2_status_t fa2_attention_step_host(const void* q_h, const void* k_h, const voi
   FA2_CUDA(cudaMemcpyAsync(k, k_h, t, cudaMemcpyHostToDevice, st));
   FA2_CUDA(cudaMemcpyAsync(v, v_h, t, cudaMemcpyHostToDevice, st));
   FA2_CUDA(cudaMemcpyAsync(dout, dout_h, t, cudaMemcpyHostToDevice, st));
-  if ((s = forward_impl(q, k, v, o, lse, B, H, N, d, causal, softmax_scale, dtype, st, di.sms)) != FA2_OK) return s;
-  if ((s = backward_impl(q, k, v, o, lse, dout, dq, dk, dv, ws, B, H, N, d, causal, softmax_scale, dtype, st,
+  if ((s = forward_impl(q, k, v, o, lse, B, H, H, N, d, causal, softmax_scale, dtype, st, di.sms)) != FA2_OK) return s;
+  if ((s = backward_impl(q, k, v, o, lse, dout, dq, dk, dv, ws, B, H, H, N, d, causal, softmax_scale, dtype, st,
                          di.sms)) != FA2_OK)
     return s;
   if (o_h) FA2_CUDA(cudaMemcpyAsync(o_h, o, t, cudaMemcpyDeviceToHost, st));

@@ -124,7 +124,10 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
       int bh, nb;
       decode(t, bh, nb);
       const int kv_row = nb * 128 + r;
-      for (int i = q_begin(nb); i < n_q_blocks; ++i, ++g) {
+      const int i0 = q_begin(nb), nqt = n_q_blocks - i0;
+      const int bq0 = (bh / p.Hkv) * p.H + (bh % p.Hkv) * p.group;   // first query head of this kv head
+      for (int x = 0; x < nqt * p.group; ++x, ++g) {
+        const int i = i0 + x % nqt, bhq = bq0 + x / nqt;            // query tile, query head
         const uint32_t slot = g % STAGES, b = g & 1;
         ptx::mbar_wait(&q_full[slot], (g / STAGES) & 1);
         ptx::mbar_wait(&s_full[b], (g >> 1) & 1);
@@ -212,7 +215,10 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
       int bh, nb;
       decode(t, bh, nb);
-      for (int i = q_begin(nb); i < n_q_blocks; ++i, ++g) {
+      const int i0 = q_begin(nb), nqt = n_q_blocks - i0;
+      const int bq0 = (bh / p.Hkv) * p.H + (bh % p.Hkv) * p.group;   // first query head of this kv head
+      for (int x = 0; x < nqt * p.group; ++x, ++g) {
+        const int i = i0 + x % nqt, bhq = bq0 + x / nqt;            // query tile, query head
         const uint32_t b = g & 1;
         ptx::mbar_wait(&dq_full[b], (g >> 1) & 1);
         if (leader) FA2_BTRACE(7, g);
@@ -236,7 +242,7 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
         ptx::named_bar_sync(1, 128);
         if (leader) {
 #pragma unroll
-          for (int bx = 0; bx < D / 32; ++bx) ptx::tma_reduce_add_3d(&tm_dq, sDQ + bx * (BM * 128), bx * 32, i * BM, bh);
+          for (int bx = 0; bx < D / 32; ++bx) ptx::tma_reduce_add_3d(&tm_dq, sDQ + bx * (BM * 128), bx * 32, i * BM, bhq);
           ptx::bulk_commit();
           FA2_BTRACE(8, g);
         }
@@ -289,7 +295,8 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
       int bh, nb;
       decode(t, bh, nb);
       const int i0 = q_begin(nb);
-      const uint32_t g0 = g, n = static_cast<uint32_t>(n_q_blocks - i0);
+      // query tiles of every query head of this key/value head's group (GQA)
+      const uint32_t g0 = g, n = static_cast<uint32_t>((n_q_blocks - i0) * p.group);
       ptx::mbar_wait(kv_full, it & 1);
       // prologue: S^T / dP^T of the first two query tiles
       for (uint32_t x = g0; x < g0 + 2 && x < g0 + n; ++x) {
@@ -364,16 +371,19 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
           ptx::tma_load_3d_hint(sK + s * 128 * 128, &tm_k, kv_full, s * 64, nb * 128, bh, pol_kv);
           ptx::tma_load_3d_hint(sV + s * 128 * 128, &tm_v, kv_full, s * 64, nb * 128, bh, pol_kv);
         }
-        for (int i = q_begin(nb); i < n_q_blocks; ++i, ++g) {
+        const int i0 = q_begin(nb), nqt = n_q_blocks - i0;
+        const int bq0 = (bh / p.Hkv) * p.H + (bh % p.Hkv) * p.group;
+        for (int x = 0; x < nqt * p.group; ++x, ++g) {
+          const int i = i0 + x % nqt, bhq = bq0 + x / nqt;
           const int slot = g % STAGES;
           if (g >= STAGES) ptx::mbar_wait(&q_empty[slot], ((g / STAGES) - 1) & 1);
           ptx::mbar_arrive_expect_tx(&q_full[slot], 2 * L::Q_TILE + 2 * BM * 4);
           for (int s = 0; s < NSUB; ++s) {
-            ptx::tma_load_3d_hint(sQ + slot * L::Q_TILE + s * L::Q_SUB, &tm_q, &q_full[slot], s * 64, i * BM, bh, pol_q);
-            ptx::tma_load_3d_hint(sDO + slot * L::Q_TILE + s * L::Q_SUB, &tm_do, &q_full[slot], s * 64, i * BM, bh, pol_q);
+            ptx::tma_load_3d_hint(sQ + slot * L::Q_TILE + s * L::Q_SUB, &tm_q, &q_full[slot], s * 64, i * BM, bhq, pol_q);
+            ptx::tma_load_3d_hint(sDO + slot * L::Q_TILE + s * L::Q_SUB, &tm_do, &q_full[slot], s * 64, i * BM, bhq, pol_q);
           }
           float* vdst = sVec + slot * 2 * BM;
-          const size_t voff = static_cast<size_t>(bh) * p.npad + static_cast<size_t>(i) * BM;
+          const size_t voff = static_cast<size_t>(bhq) * p.npad + static_cast<size_t>(i) * BM;
           ptx::bulk_load_1d(vdst, gL2 + voff, BM * 4, &q_full[slot]);
           ptx::bulk_load_1d(vdst + BM, gD + voff, BM * 4, &q_full[slot]);
         }

@@ -46,7 +46,8 @@ struct BwdParams {
   void* dk;
   void* dv;
   float* dq_acc;        // fp32 dQ accumulator ([BH, npad, D], or [BH, D, npad] when transposed)
-  int BH, N, npad;
+  int BH, N, npad;      // BH = B * H (query heads)
+  int H, Hkv, group;    // query heads, key/value heads, H / Hkv (GQA; group == 1 for MHA)
   int num_n_blocks;     // ceil(N / 128)
   int num_tiles;        // BH * num_n_blocks
   float scale;
@@ -242,8 +243,10 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       int bh, nb;
       decode(t, bh, nb);
       const int kv_row = nb * 128 + r;
-      const int i0 = q_begin(nb);
-      for (int i = i0; i < n_q_blocks; ++i, ++g) {
+      const int i0 = q_begin(nb), nqt = n_q_blocks - i0;
+      const int bq0 = (bh / p.Hkv) * p.H + (bh % p.Hkv) * p.group;   // first query head of this kv head
+      for (int x = 0; x < nqt * p.group; ++x, ++g) {
+        const int i = i0 + x % nqt, bhq = bq0 + x / nqt;            // query tile, query head
         const int slot = g % STAGES;
         ptx::mbar_wait(&q_full[slot], (g / STAGES) & 1);
         ptx::mbar_wait(s_full, g & 1);
@@ -348,8 +351,10 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
       int bh, nb;
       decode(t, bh, nb);
-      const int i0 = q_begin(nb);
-      for (int i = i0; i < n_q_blocks; ++i, ++g) {
+      const int i0 = q_begin(nb), nqt = n_q_blocks - i0;
+      const int bq0 = (bh / p.Hkv) * p.H + (bh % p.Hkv) * p.group;   // first query head of this kv head
+      for (int x = 0; x < nqt * p.group; ++x, ++g) {
+        const int i = i0 + x % nqt, bhq = bq0 + x / nqt;            // query tile, query head
         ptx::mbar_wait(dq_full, g & 1);
         if (leader) FA2_BTRACE(7, g);
         ptx::tc_fence_after();
@@ -388,7 +393,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         ptx::named_bar_sync(1, 128);
         if (leader) {
 #pragma unroll
-          for (int b = 0; b < D / 32; ++b) ptx::tma_reduce_add_3d(&tm_dq, sDQ + b * (BM * 128), b * 32, i * BM, bh);
+          for (int b = 0; b < D / 32; ++b) ptx::tma_reduce_add_3d(&tm_dq, sDQ + b * (BM * 128), b * 32, i * BM, bhq);
           ptx::bulk_commit();
           FA2_BTRACE(8, g);
         }
@@ -457,7 +462,8 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       const int i0 = q_begin(nb);
       ptx::mbar_wait(kv_full, it & 1);
       bool have_prev = false;
-      for (int i = i0; i < n_q_blocks; ++i, ++g) {
+      const int cnt = (n_q_blocks - i0) * p.group;   // query tiles of every query head of the group
+      for (int x = 0; x < cnt; ++x, ++g) {
         const uint32_t slot = g % STAGES;
         FA2_BTRACE(10, g);
         ptx::mbar_wait(&q_full[slot], (g / STAGES) & 1);
@@ -478,14 +484,14 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         }
         __syncwarp();
         FA2_BTRACE(4, g);
-        if (have_prev) issue_grads(g - 1, i - 1 == i0);
+        if (have_prev) issue_grads(g - 1, x - 1 == 0);
         else if (dkv_uses > 0) {
           // first query tile of this work tile: previous dK/dV must be drained first
           ptx::mbar_wait(dkv_empty, (dkv_uses - 1) & 1);
         }
         have_prev = true;
       }
-      issue_grads(g - 1, (n_q_blocks - 1) == i0);
+      issue_grads(g - 1, cnt - 1 == 0);
       ++dkv_uses;
       if (ptx::elect_one()) {
         ptx::mma_commit(dkv_full);
@@ -503,23 +509,25 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
         int bh, nb;
         decode(t, bh, nb);
-        const int i0 = q_begin(nb);
+        const int i0 = q_begin(nb), nqt = n_q_blocks - i0;
+        const int bq0 = (bh / p.Hkv) * p.H + (bh % p.Hkv) * p.group;
         if (it > 0) ptx::mbar_wait(kv_empty, (it - 1) & 1);
         ptx::mbar_arrive_expect_tx(kv_full, 2 * L::KV_TILE);
         for (int s = 0; s < NSUB; ++s) {
           ptx::tma_load_3d_hint(sK + s * 128 * 128, &tm_k, kv_full, s * 64, nb * 128, bh, pol_kv);
           ptx::tma_load_3d_hint(sV + s * 128 * 128, &tm_v, kv_full, s * 64, nb * 128, bh, pol_kv);
         }
-        for (int i = i0; i < n_q_blocks; ++i, ++g) {
+        for (int x = 0; x < nqt * p.group; ++x, ++g) {
+          const int i = i0 + x % nqt, bhq = bq0 + x / nqt;
           const int slot = g % STAGES;
           if (g >= STAGES) ptx::mbar_wait(&q_empty[slot], ((g / STAGES) - 1) & 1);
           ptx::mbar_arrive_expect_tx(&q_full[slot], 2 * L::Q_TILE + 2 * BM * 4);
           for (int s = 0; s < NSUB; ++s) {
-            ptx::tma_load_3d_hint(sQ + slot * L::Q_TILE + s * L::Q_SUB, &tm_q, &q_full[slot], s * 64, i * BM, bh, pol_q);
-            ptx::tma_load_3d_hint(sDO + slot * L::Q_TILE + s * L::Q_SUB, &tm_do, &q_full[slot], s * 64, i * BM, bh, pol_q);
+            ptx::tma_load_3d_hint(sQ + slot * L::Q_TILE + s * L::Q_SUB, &tm_q, &q_full[slot], s * 64, i * BM, bhq, pol_q);
+            ptx::tma_load_3d_hint(sDO + slot * L::Q_TILE + s * L::Q_SUB, &tm_do, &q_full[slot], s * 64, i * BM, bhq, pol_q);
           }
           float* vdst = sVec + slot * 2 * BM;
-          const size_t voff = static_cast<size_t>(bh) * p.npad + static_cast<size_t>(i) * BM;
+          const size_t voff = static_cast<size_t>(bhq) * p.npad + static_cast<size_t>(i) * BM;
           ptx::bulk_load_1d(vdst, gL2 + voff, BM * 4, &q_full[slot]);
           ptx::bulk_load_1d(vdst + BM, gD + voff, BM * 4, &q_full[slot]);
         }

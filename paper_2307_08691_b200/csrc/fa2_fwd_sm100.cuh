@@ -45,7 +45,8 @@ constexpr int kFwdEmuPairs = FA2_FWD_EMU_PAIRS;
 struct FwdParams {
   void* o;             // [BH, N, D] dtype
   float* lse;          // [BH, N]
-  int BH, N;
+  int BH, N;          // BH = B * H (query heads)
+  int H, Hkv, group;   // query heads, key/value heads, H / Hkv (GQA; group == 1 for MHA)
   int num_m_blocks;    // ceil(N / 256)
   int num_tiles;       // BH * num_m_blocks
   float scale_log2;    // softmax_scale * log2(e)
@@ -384,6 +385,8 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         int bh, mb;
         decode(t, bh, mb);
         const int nkv = max(n_blocks(mb, 0), n_blocks(mb, 1));
+        // key/value head of this query head: implicit index manipulation
+        const int kvh = (bh / p.H) * p.Hkv + (bh % p.H) / p.group;
         for (int i = 0; i < 2; ++i) {
           if (it > 0) ptx::mbar_wait(&q_empty[i], (it - 1) & 1);
           ptx::mbar_arrive_expect_tx(&q_full[i], L::TILE);
@@ -394,12 +397,12 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           ptx::mbar_wait(&k_empty[kslot], kphase ^ 1);
           ptx::mbar_arrive_expect_tx(&k_full[kslot], L::TILE);
           for (int s = 0; s < NSUB; ++s)
-            ptx::tma_load_3d_hint(sK + kslot * L::TILE + s * L::SUB, &tm_k, &k_full[kslot], s * 64, j * 128, bh, pol_kv);
+            ptx::tma_load_3d_hint(sK + kslot * L::TILE + s * L::SUB, &tm_k, &k_full[kslot], s * 64, j * 128, kvh, pol_kv);
           if (++kslot == STAGES) { kslot = 0; kphase ^= 1; }
           ptx::mbar_wait(&v_empty[vslot], vphase ^ 1);
           ptx::mbar_arrive_expect_tx(&v_full[vslot], L::TILE);
           for (int s = 0; s < NSUB; ++s)
-            ptx::tma_load_3d_hint(sV + vslot * L::TILE + s * L::SUB, &tm_v, &v_full[vslot], s * 64, j * 128, bh, pol_kv);
+            ptx::tma_load_3d_hint(sV + vslot * L::TILE + s * L::SUB, &tm_v, &v_full[vslot], s * 64, j * 128, kvh, pol_kv);
           if (++vslot == STAGES) { vslot = 0; vphase ^= 1; }
         }
       }

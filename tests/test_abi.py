@@ -125,3 +125,15 @@ def test_kv_block_range_errors(L):
         fa2.kv_block_range(100, 128, 128, 1, False)
     with pytest.raises(fa2.FA2Error):
         fa2.kv_block_range(0, 128, 128, 0, False)
+
+
+def test_gqa_validation(L):
+    p = FAKE
+    # H must be a positive multiple of H_kv
+    assert L.fa2_forward_gqa(p[0], p[1], p[2], p[3], p[4], 1, 6, 4, 128, 64, 0, 0.125, 0, None) == 1
+    assert L.fa2_forward_gqa(p[0], p[1], p[2], p[3], p[4], 1, 6, 0, 128, 64, 0, 0.125, 0, None) == 1
+    assert L.fa2_forward_gqa(p[0], p[1], p[2], p[3], p[4], 1, 6, 3, 128, 96, 0, 0.125, 0, None) == 2
+    ws = ctypes.c_void_p(1 << 20)
+    assert L.fa2_backward_gqa(*p[:9], ws, 1 << 30, 1, 8, 3, 128, 64, 0, 0.125, 0, None) == 1
+    # valid GQA arguments reach CUDA (no device here)
+    assert L.fa2_forward_gqa(p[0], p[1], p[2], p[3], p[4], 1, 8, 2, 128, 64, 1, 0.125, 0, None) in (2, 4)

@@ -154,3 +154,29 @@ def test_launch_count_and_errors():
     assert fa2.lib().fa2_last_launch_count() == 1
     with pytest.raises(fa2.FA2Error):
         fa2.forward(qc.float(), k.cuda().float(), v.cuda().float())
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("shape", [(2, 8, 2, 300, 128), (1, 4, 1, 257, 64), (1, 6, 3, 130, 128), (2, 4, 2, 1000, 64)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_gqa_parity(shape, causal, dtype):
+    """MQA/GQA: H query heads share H_kv key/value heads."""
+    B, H, Hkv, N, d = shape
+    q = W.randn((B, H, N, d), 70, dtype)
+    k = W.randn((B, Hkv, N, d), 71, dtype)
+    v = W.randn((B, Hkv, N, d), 72, dtype)
+    do = W.randn((B, H, N, d), 73, dtype)
+    sc = scale_for(d)
+    qc, kc, vc, doc = q.cuda(), k.cuda(), v.cuda(), do.cuda()
+    o, lse = fa2.forward(qc, kc, vc, causal=causal, softmax_scale=sc)
+    dq, dk, dv = fa2.backward(qc, kc, vc, o, lse, doc, causal=causal, softmax_scale=sc)
+    torch.cuda.synchronize()
+    o_ref, l_ref = R.forward_gqa(to_np(q), to_np(k), to_np(v), sc, causal)
+    assert o_excess(o.cpu(), o_ref, dtype) <= TOL[dtype]["O"]
+    assert max_abs(lse.cpu(), l_ref) <= TOL[dtype]["L"]
+    gq, gk, gv = R.backward_gqa(to_np(q), to_np(k), to_np(v), to_np(do), sc, causal)
+    fl = grad_floor(gq, gk, gv)
+    for name, g, ref in (("dq", dq, gq), ("dk", dk, gk), ("dv", dv, gv)):
+        ok, err, lim = grad_ok(g, ref, dtype, fl)
+        assert ok, f"{name}: err {err} > {lim}"
