@@ -72,7 +72,7 @@ struct FwdSmem {
   static constexpr int OFF_V = OFF_K + STAGES * TILE;
   static constexpr int OFF_BAR = OFF_V + STAGES * TILE;
   // barriers: q_full[2] q_empty[2] k_full[S] k_empty[S] v_full[S] v_empty[S] s_full[2] p_full[2] o_done[2] o_empty[2]
-  static constexpr int NBAR = 2 + 2 + 4 * STAGES + 2 + 2 + 2 + 2;
+  static constexpr int NBAR = 2 + 2 + 4 * STAGES + 2 + 2 + 2 + 2 + 2;   // + s_consumed[2]
   static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
   static constexpr int BYTES = OFF_TMEM + 16;
   static constexpr int ALLOC = BYTES + 1024;   // slack for 1024-B alignment
@@ -85,6 +85,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   using L = FwdSmem<D>;
   constexpr int STAGES = L::STAGES;
   constexpr int NSUB = D / 64;
+  constexpr bool SEP_P = (D == 64);   // P~ in its own TMEM columns (fits only at d = 64)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
 
@@ -102,6 +103,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   uint64_t* p_full = s_full + 2;
   uint64_t* o_done = p_full + 2;
   uint64_t* o_empty = o_done + 2;
+  uint64_t* s_consumed = o_empty + 2;   // [2] d=64 only: softmax has read S_i (4 warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
 
   const int warp = threadIdx.x / 32;
@@ -115,6 +117,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       ptx::mbar_init(&p_full[i], 4);
       ptx::mbar_init(&o_done[i], 1);
       ptx::mbar_init(&o_empty[i], 4);
+      ptx::mbar_init(&s_consumed[i], 4);
     }
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&k_full[s], 1);
@@ -162,6 +165,9 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     const int row = threadIdx.x % 128;       // TMEM lane == row within sub-tile
     const uint32_t lane_base = static_cast<uint32_t>((warp % 4) * 32) << 16;
     const uint32_t tS = tmem + lane_base + wg * 128;
+    // P~_i: over the first 64 columns of S_i (d = 128), or its own 64 columns
+    // after O0, O1 (d = 64: frees S_i for S_{j+1} as soon as it has been read)
+    const uint32_t tP = SEP_P ? (tmem + lane_base + 256 + 2 * D + wg * 64) : tS;
     const uint32_t tO = tmem + lane_base + 256 + wg * D;
     uint32_t s_count = 0;   // completed waits on s_full[wg]
     uint32_t pv_count = 0;  // PV MMAs issued so far for this sub-tile (all tiles)
@@ -186,6 +192,12 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         ptx::tmem_ld_x32(tS + 64, su + 64);
         ptx::tmem_ld_x32(tS + 96, su + 96);
         ptx::tmem_wait_ld();
+        if constexpr (SEP_P) {
+          // S_i has been read: the MMA warp may compute S_i of the next block into it
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&s_consumed[wg]);
+        }
         float s[128];
 #pragma unroll
         for (int c = 0; c < 128; ++c) s[c] = __uint_as_float(su[c]);
@@ -213,6 +225,11 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         float2 rs2 = make_float2(0.f, 0.f);
         // exponent x = s * scale * log2(e) - m (FFMA2), P~ = 2^x.  On unmasked blocks
         // EMU of every 16 column pairs use the FMA-pipe polynomial, the rest MUFU.EX2.
+        if constexpr (SEP_P) {
+          // the P buffer is free once the previous P~V MMA of this sub-tile completed
+          if (pv_count > 0) ptx::mbar_wait(&o_done[wg], (pv_count - 1) & 1);
+          ptx::tc_fence_after();
+        }
         auto exp_block = [&](auto emu_tag) {
           constexpr int EMU = decltype(emu_tag)::value;
 #pragma unroll
@@ -231,7 +248,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
               rs2 = ptx::fadd2(rs2, pr);
               pk[e] = ptx::pack2<BF16>(pr.x, pr.y);
             }
-            ptx::tmem_st_x16(tS + ch * 16, pk);
+            ptx::tmem_st_x16(tP + ch * 16, pk);
           }
         };
         if (need_mask) exp_block(std::integral_constant<int, 0>{});
@@ -310,8 +327,17 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       auto mma_pv = [&](int i, int slot, bool acc) {
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-          ptx::mma_ts(tmem + 256 + i * D, tmem + i * 128 + k * 8, dV + ((slot * L::TILE + k * 2048) >> 4), IDESC_O,
-                      (acc || k > 0) ? 1u : 0u);
+          ptx::mma_ts(tmem + 256 + i * D, tmem + (SEP_P ? 256 + 2 * D + i * 64 : i * 128) + k * 8,
+                      dV + ((slot * L::TILE + k * 2048) >> 4), IDESC_O, (acc || k > 0) ? 1u : 0u);
+      };
+      uint32_t s_iss0 = 0, s_iss1 = 0;   // d = 64: S MMAs issued per sub-tile (s_consumed phases)
+      // d = 64: S_i into its buffer once softmax i has read the previous S_i
+      auto issue_s_sep = [&](int i, uint32_t& s_iss) {
+        if (s_iss > 0) ptx::mbar_wait(&s_consumed[i], (s_iss - 1) & 1);
+        ptx::tc_fence_after();
+        if (ptx::elect_one()) { mma_s(i, kslot); ptx::mma_commit(&s_full[i]); }
+        __syncwarp();
+        ++s_iss;
       };
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
         int bh, mb;
@@ -320,6 +346,45 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         const int nkv = max(nb0, nb1);
         ptx::mbar_wait(&q_full[0], it & 1);
         ptx::mbar_wait(&q_full[1], it & 1);
+        if constexpr (SEP_P) {
+          // S_{j+1} is issued as soon as S_j has been read (P~ has its own buffer),
+          // so the next block's scores are ready when the softmax finishes block j.
+          for (int j = -1; j < nkv; ++j) {
+            if (j + 1 < nkv) {
+              ptx::mbar_wait(&k_full[kslot], kphase);
+              if (j + 1 < nb0) issue_s_sep(0, s_iss0);
+              if (j + 1 < nb1) issue_s_sep(1, s_iss1);
+              if (ptx::elect_one()) ptx::mma_commit(&k_empty[kslot]);
+              __syncwarp();
+              if (++kslot == STAGES) { kslot = 0; kphase ^= 1; }
+            }
+            if (j < 0) continue;
+            ptx::mbar_wait(&v_full[vslot], vphase);
+            auto pv = [&](int i, int nbi, uint32_t& p_count, uint32_t& o_uses) {
+              if (j >= nbi) return;
+              if (j == 0) {
+                if (o_uses > 0) ptx::mbar_wait(&o_empty[i], (o_uses - 1) & 1);
+                ++o_uses;
+              }
+              ptx::mbar_wait(&p_full[i], p_count & 1);
+              ++p_count;
+              ptx::tc_fence_after();
+              if (ptx::elect_one()) { mma_pv(i, vslot, j > 0); ptx::mma_commit(&o_done[i]); }
+              __syncwarp();
+            };
+            pv(0, nb0, p_count0, o_uses0);
+            pv(1, nb1, p_count1, o_uses1);
+            if (ptx::elect_one()) ptx::mma_commit(&v_empty[vslot]);
+            __syncwarp();
+            if (++vslot == STAGES) { vslot = 0; vphase ^= 1; }
+          }
+          if (ptx::elect_one()) {
+            ptx::mma_commit(&q_empty[0]);
+            ptx::mma_commit(&q_empty[1]);
+          }
+          __syncwarp();
+          continue;
+        }
         if (nkv > 0) {
           ptx::mbar_wait(&k_full[kslot], kphase);
           ptx::tc_fence_after();
