@@ -238,12 +238,13 @@ fa2_status_t backward_impl(const void* q, const void* k, const void* v, const vo
   if (s != FA2_OK) return s;
   fa2::BwdMaps maps;
   const CUtensorMapDataType dt = tma_dtype(dtype);
-  const int bm = fa2::bwd_bm(d);
+  const int bm = d == 128 ? fa2::Bwd128Smem::BM : fa2::bwd_bm(d);   // query rows per backward tile
   if ((s = make_map_3d(&maps.q, q, dt, 2, d, N, BH, 64, bm, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
   if ((s = make_map_3d(&maps.dout, dout, dt, 2, d, N, BH, 64, bm, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
   if ((s = make_map_3d(&maps.k, k, dt, 2, d, N, B * Hkv, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
   if ((s = make_map_3d(&maps.v, v, dt, 2, d, N, B * Hkv, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
-  // fp32 dQ accumulator [BH, npad, d]; reduce-add boxes of 32 columns x BM rows (128-B swizzle rows)
+  // fp32 dQ accumulator [BH, npad, d]; reduce-add boxes of 32 columns x BM rows (128-B swizzle rows;
+  // the d=128 kernel uses contiguous 1D bulk reductions instead)
   if ((s = make_map_3d(&maps.dq_acc, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, d, static_cast<int>(npad), BH, 32,
                        bm, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK)
     return s;
