@@ -67,7 +67,8 @@ FA2_API fa2_status_t fa2_forward(const void* q, const void* k, const void* v, vo
 
 /* Bytes of device scratch fa2_backward needs: the fp32 dQ accumulator
  * [B,H,N_pad,d], D [B,H,N_pad] and L*log2(e) [B,H,N_pad] (fp32), where N_pad is
- * N rounded up to a multiple of 128. */
+ * N rounded up to a multiple of 128, plus [B,H,N_pad/128] int32 dQ-tile
+ * counters (used by fa2_backward_deterministic), rounded up to 16 bytes. */
 FA2_API size_t fa2_backward_workspace_size(int B, int H, int N, int d);
 
 /* Backward pass, Alg. 2: writes dq, dk, dv ([B,H,N,d], dtype).
@@ -94,6 +95,22 @@ FA2_API fa2_status_t fa2_backward_gqa(const void* q, const void* k, const void* 
                                       void* workspace, size_t workspace_bytes,
                                       int B, int H, int H_kv, int N, int d, int causal, float softmax_scale,
                                       fa2_dtype_t dtype, void* stream);
+
+/* Deterministic backward.  Same arguments, layouts, workspace and
+ * errors as fa2_backward_gqa (H_kv == H for plain multi-head attention); the
+ * result is bitwise reproducible from run to run on the same device and
+ * arguments.  Alg. 2 accumulates dQ_i += dS_ij K_j into HBM from every key block
+ * j with atomic adds, so the fp32 summation order -- and
+ * the last bits of dQ -- follow arrival order.  Here every dQ tile (query head,
+ * 128-row query tile) takes its key blocks' contributions in one fixed order,
+ * serialised by a counter per tile in the workspace; the arithmetic is otherwise
+ * identical (dK, dV are accumulated on chip in a fixed order in both modes).
+ * Slower than fa2_backward_gqa by the waits on those counters. */
+FA2_API fa2_status_t fa2_backward_deterministic(const void* q, const void* k, const void* v, const void* o,
+                                                const float* lse, const void* dout, void* dq, void* dk, void* dv,
+                                                void* workspace, size_t workspace_bytes,
+                                                int B, int H, int H_kv, int N, int d, int causal,
+                                                float softmax_scale, fa2_dtype_t dtype, void* stream);
 
 /* D = rowsum(dO o O) alone, into d_out [B,H,N] fp32 (device).  Exposed
  * so the preprocessing step can be checked on its own; fa2_backward runs it

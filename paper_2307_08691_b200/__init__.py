@@ -45,6 +45,8 @@ def lib() -> ctypes.CDLL:
         L.fa2_forward_gqa.restype = i
         L.fa2_backward_gqa.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, i, i, i, i, i, i, f, i, vp]
         L.fa2_backward_gqa.restype = i
+        L.fa2_backward_deterministic.argtypes = L.fa2_backward_gqa.argtypes
+        L.fa2_backward_deterministic.restype = i
         L.fa2_backward.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, i, i, i, i, i, f, i, vp]
         L.fa2_backward.restype = i
         L.fa2_backward_preprocess.argtypes = [vp, vp, vp, i, i, i, i, i, vp]
@@ -137,9 +139,11 @@ def backward_workspace_size(B: int, H: int, N: int, d: int) -> int:
 
 
 def backward(q, k, v, o, lse, do, causal: bool = False, softmax_scale: float | None = None,
-             dq=None, dk=None, dv=None, workspace=None, stream=None):
+             dq=None, dk=None, dv=None, workspace=None, stream=None, deterministic: bool = False):
     """dQ, dK, dV (Alg. 2).  With H_kv < H key/value heads, dK/dV are
-    summed over each group of query heads.  Returns (dq, dk, dv)."""
+    summed over each group of query heads.  deterministic=True calls
+    fa2_backward_deterministic (fixed dQ summation order, bitwise reproducible).
+    Returns (dq, dk, dv)."""
     import torch
     B, H, N, d = _shape(q)
     Hkv = _kv_heads(q, k)
@@ -154,10 +158,10 @@ def backward(q, k, v, o, lse, do, causal: bool = False, softmax_scale: float | N
     wsz = backward_workspace_size(B, H, N, d)
     if workspace is None:
         workspace = torch.empty(wsz, dtype=torch.uint8, device=q.device)
-    _check(lib().fa2_backward_gqa(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk),
-                                  _ptr(dv), _ptr(workspace), workspace.numel() * workspace.element_size(),
-                                  B, H, Hkv, N, d, int(bool(causal)), scale, _dtype_code(q),
-                                  ctypes.c_void_p(_stream(stream))))
+    fn = lib().fa2_backward_deterministic if deterministic else lib().fa2_backward_gqa
+    _check(fn(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk),
+              _ptr(dv), _ptr(workspace), workspace.numel() * workspace.element_size(),
+              B, H, Hkv, N, d, int(bool(causal)), scale, _dtype_code(q), ctypes.c_void_p(_stream(stream))))
     return dq, dk, dv
 
 

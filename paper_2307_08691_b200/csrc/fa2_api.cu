@@ -186,37 +186,49 @@ size_t pad128(int N) { return static_cast<size_t>((N + 127) / 128) * 128; }
 size_t ws_dq_bytes(int B, int H, int N, int d) { return static_cast<size_t>(B) * H * pad128(N) * d * 4; }
 // D and L*log2(e), each [B,H,N_pad] fp32
 size_t ws_d_bytes(int B, int H, int N) { return 2 * static_cast<size_t>(B) * H * pad128(N) * 4; }
+// deterministic-mode dQ tile counters, [B,H,N_pad/128] int32 (16-byte rounded)
+size_t ws_sem_bytes(int B, int H, int N) { return (static_cast<size_t>(B) * H * (pad128(N) / 128) * 4 + 15) / 16 * 16; }
 
 fa2_status_t preprocess_impl(const void* o, const void* dout, const float* lse, float* dvec, float* lse2,
-                             float* dq_acc, int BH, int N, int npad, int d, fa2_dtype_t dtype, cudaStream_t st) {
+                             float* dq_acc, int BH, int N, int npad, int d, fa2_dtype_t dtype, cudaStream_t st,
+                             int* dq_sem = nullptr) {
   // one warp per row of the padded [BH, npad] grid; 8 rows per 256-thread block
   const long long rows = static_cast<long long>(BH) * npad;
   const int grid = static_cast<int>((rows + 7) / 8);
   const bool bf16 = dtype == FA2_BF16;
   if (d == 64) {
-    if (bf16) fa2::fa2_bwd_preprocess<64, true><<<grid, 256, 0, st>>>(o, dout, dvec, dq_acc, BH, N, npad, lse, lse2);
-    else fa2::fa2_bwd_preprocess<64, false><<<grid, 256, 0, st>>>(o, dout, dvec, dq_acc, BH, N, npad, lse, lse2);
+    if (bf16) fa2::fa2_bwd_preprocess<64, true><<<grid, 256, 0, st>>>(o, dout, dvec, dq_acc, BH, N, npad, lse, lse2, dq_sem);
+    else fa2::fa2_bwd_preprocess<64, false><<<grid, 256, 0, st>>>(o, dout, dvec, dq_acc, BH, N, npad, lse, lse2, dq_sem);
   } else {
-    if (bf16) fa2::fa2_bwd_preprocess<128, true><<<grid, 256, 0, st>>>(o, dout, dvec, dq_acc, BH, N, npad, lse, lse2);
-    else fa2::fa2_bwd_preprocess<128, false><<<grid, 256, 0, st>>>(o, dout, dvec, dq_acc, BH, N, npad, lse, lse2);
+    if (bf16) fa2::fa2_bwd_preprocess<128, true><<<grid, 256, 0, st>>>(o, dout, dvec, dq_acc, BH, N, npad, lse, lse2, dq_sem);
+    else fa2::fa2_bwd_preprocess<128, false><<<grid, 256, 0, st>>>(o, dout, dvec, dq_acc, BH, N, npad, lse, lse2, dq_sem);
   }
+  FA2_CUDA(cudaGetLastError());
+  return FA2_OK;
+}
+
+template <typename Kern>
+fa2_status_t launch_bwd_kernel(Kern kern, int smem, const fa2::BwdMaps& maps, const fa2::BwdParams& p, int sms,
+                               cudaStream_t st) {
+  fa2_status_t s = set_smem(kern, smem);
+  if (s != FA2_OK) return s;
+  int grid = p.num_tiles < sms ? p.num_tiles : sms;
+  // deterministic cyclic schedule: whole heads per wave (see bwd_q_tile in fa2_bwd_sm100.cuh)
+  if (p.dq_sem != nullptr && p.det_cyclic) grid = (grid / p.num_n_blocks) * p.num_n_blocks;
+  mark(3, st);
+  kern<<<grid, fa2::kBwdThreads, smem, st>>>(maps.q, maps.k, maps.v, maps.dout, maps.dq_acc, p);
+  mark(4, st);
   FA2_CUDA(cudaGetLastError());
   return FA2_OK;
 }
 
 template <int D, bool BF16, bool CAUSAL>
 fa2_status_t launch_bwd(const fa2::BwdMaps& maps, const fa2::BwdParams& p, int sms, cudaStream_t st) {
-  // d = 128: double-region TMEM pipeline (fa2_bwd128_sm100.cuh); d = 64: fa2_bwd_kernel
-  auto kern = D == 128 ? fa2::fa2_bwd128_kernel<BF16, CAUSAL> : fa2::fa2_bwd_kernel<D, BF16, CAUSAL>;
-  constexpr int smem = D == 128 ? fa2::Bwd128Smem::ALLOC : fa2::BwdSmem<D>::ALLOC;
-  fa2_status_t s = set_smem(kern, smem);
-  if (s != FA2_OK) return s;
-  const int grid = p.num_tiles < sms ? p.num_tiles : sms;
-  mark(3, st);
-  kern<<<grid, fa2::kBwdThreads, smem, st>>>(maps.q, maps.k, maps.v, maps.dout, maps.dq_acc, p);
-  mark(4, st);
-  FA2_CUDA(cudaGetLastError());
-  return FA2_OK;
+  // d = 128: fa2_bwd128_sm100.cuh; d = 64: fa2_bwd_kernel
+  if constexpr (D == 128)
+    return launch_bwd_kernel(fa2::fa2_bwd128_kernel<BF16, CAUSAL>, fa2::Bwd128Smem::ALLOC, maps, p, sms, st);
+  else
+    return launch_bwd_kernel(fa2::fa2_bwd_kernel<D, BF16, CAUSAL>, fa2::BwdSmem<D>::ALLOC, maps, p, sms, st);
 }
 
 template <int D, bool BF16>
@@ -227,18 +239,20 @@ fa2_status_t dispatch_bwd_causal(bool causal, const fa2::BwdMaps& maps, const fa
 
 fa2_status_t backward_impl(const void* q, const void* k, const void* v, const void* o, const float* lse,
                            const void* dout, void* dq, void* dk, void* dv, void* ws, int B, int H, int Hkv, int N,
-                           int d, int causal, float scale, fa2_dtype_t dtype, cudaStream_t st, int sms) {
+                           int d, int causal, float scale, fa2_dtype_t dtype, cudaStream_t st, int sms,
+                           bool deterministic = false) {
   const int BH = B * H;
   const size_t npad = pad128(N);
   float* dq_acc = reinterpret_cast<float*>(ws);
   float* dvec = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + ws_dq_bytes(B, H, N, d));
   float* lse2 = dvec + static_cast<size_t>(BH) * npad;
+  int* dq_sem = deterministic ? reinterpret_cast<int*>(lse2 + static_cast<size_t>(BH) * npad) : nullptr;
   mark(2, st);
-  fa2_status_t s = preprocess_impl(o, dout, lse, dvec, lse2, dq_acc, BH, N, static_cast<int>(npad), d, dtype, st);
+  fa2_status_t s = preprocess_impl(o, dout, lse, dvec, lse2, dq_acc, BH, N, static_cast<int>(npad), d, dtype, st, dq_sem);
   if (s != FA2_OK) return s;
   fa2::BwdMaps maps;
   const CUtensorMapDataType dt = tma_dtype(dtype);
-  const int bm = d == 128 ? fa2::Bwd128Smem::BM : fa2::bwd_bm(d);   // query rows per backward tile
+  const int bm = 128;   // query rows per backward tile (both kernels)
   if ((s = make_map_3d(&maps.q, q, dt, 2, d, N, BH, 64, bm, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
   if ((s = make_map_3d(&maps.dout, dout, dt, 2, d, N, BH, 64, bm, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
   if ((s = make_map_3d(&maps.k, k, dt, 2, d, N, B * Hkv, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
@@ -265,6 +279,8 @@ fa2_status_t backward_impl(const void* q, const void* k, const void* v, const vo
   p.scale = scale;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.trace = g_trace;
+  p.dq_sem = dq_sem;
+  p.det_cyclic = p.num_n_blocks <= sms ? 1 : 0;
   const bool bf16 = dtype == FA2_BF16;
   if (d == 64)
     s = bf16 ? dispatch_bwd_causal<64, true>(causal, maps, p, sms, st) : dispatch_bwd_causal<64, false>(causal, maps, p, sms, st);
@@ -283,6 +299,11 @@ fa2_status_t backward_impl(const void* q, const void* k, const void* v, const vo
   }
   return FA2_OK;
 }
+
+fa2_status_t backward_entry(const void* q, const void* k, const void* v, const void* o, const float* lse,
+                            const void* dout, void* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes,
+                            int B, int H, int H_kv, int N, int d, int causal, float softmax_scale, fa2_dtype_t dtype,
+                            void* stream, bool deterministic);
 
 }  // namespace
 
@@ -347,7 +368,7 @@ fa2_status_t fa2_forward(const void* q, const void* k, const void* v, void* o, f
 
 size_t fa2_backward_workspace_size(int B, int H, int N, int d) {
   if (B < 1 || H < 1 || N < 1 || (d != 64 && d != 128)) return 0;
-  return ws_dq_bytes(B, H, N, d) + ws_d_bytes(B, H, N);
+  return ws_dq_bytes(B, H, N, d) + ws_d_bytes(B, H, N) + ws_sem_bytes(B, H, N);
 }
 
 fa2_status_t fa2_backward(const void* q, const void* k, const void* v, const void* o, const float* lse,
@@ -362,6 +383,25 @@ fa2_status_t fa2_backward_gqa(const void* q, const void* k, const void* v, const
                               const void* dout, void* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes,
                               int B, int H, int H_kv, int N, int d, int causal, float softmax_scale, fa2_dtype_t dtype,
                               void* stream) {
+  return backward_entry(q, k, v, o, lse, dout, dq, dk, dv, workspace, workspace_bytes, B, H, H_kv, N, d, causal,
+                        softmax_scale, dtype, stream, false);
+}
+
+fa2_status_t fa2_backward_deterministic(const void* q, const void* k, const void* v, const void* o, const float* lse,
+                                        const void* dout, void* dq, void* dk, void* dv, void* workspace,
+                                        size_t workspace_bytes, int B, int H, int H_kv, int N, int d, int causal,
+                                        float softmax_scale, fa2_dtype_t dtype, void* stream) {
+  return backward_entry(q, k, v, o, lse, dout, dq, dk, dv, workspace, workspace_bytes, B, H, H_kv, N, d, causal,
+                        softmax_scale, dtype, stream, true);
+}
+
+}  // extern "C"
+
+namespace {
+fa2_status_t backward_entry(const void* q, const void* k, const void* v, const void* o, const float* lse,
+                            const void* dout, void* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes,
+                            int B, int H, int H_kv, int N, int d, int causal, float softmax_scale, fa2_dtype_t dtype,
+                            void* stream, bool deterministic) {
   g_detail.clear();
   fa2_status_t s = check_common(B, H, N, d, softmax_scale, dtype, true);
   if (s != FA2_OK) return s;
@@ -375,10 +415,13 @@ fa2_status_t fa2_backward_gqa(const void* q, const void* k, const void* v, const
   DeviceInfo di;
   if ((s = device_info(di)) != FA2_OK) return s;
   s = backward_impl(q, k, v, o, lse, dout, dq, dk, dv, workspace, B, H, H_kv, N, d, causal, softmax_scale, dtype,
-                    static_cast<cudaStream_t>(stream), di.sms);
+                    static_cast<cudaStream_t>(stream), di.sms, deterministic);
   if (s == FA2_OK) g_launches = 3;
   return s;
 }
+}  // namespace
+
+extern "C" {
 
 fa2_status_t fa2_backward_preprocess(const void* o, const void* dout, float* d_out, int B, int H, int N, int d,
                                      fa2_dtype_t dtype, void* stream) {

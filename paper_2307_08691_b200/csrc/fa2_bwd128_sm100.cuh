@@ -123,7 +123,7 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
   const int n_q_blocks = (N + BM - 1) / BM;
   const float* gD = p.dvec;
   const float* gL2 = p.dvec + static_cast<size_t>(p.BH) * p.npad;
-  auto decode = [&](int t, int& bh, int& nb) { bh = t / p.num_n_blocks; nb = t % p.num_n_blocks; };
+  auto decode = [&](int t, int& bh, int& nb) { bwd_decode(p, CAUSAL, t, bh, nb); };
   auto q_begin = [&](int nb) -> int { return CAUSAL ? nb : 0; };   // B_r == B_c == 128
 
   if (warp < 8) {
@@ -142,7 +142,7 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
       const int kv_row = nb * 128 + r;
       const int i0 = q_begin(nb), nqt = n_q_blocks - i0;
       for (int x = 0; x < nqt * p.group; ++x, ++g) {
-        const int i = i0 + x % nqt;
+        const int i = bwd_q_tile(p, CAUSAL, nb, x % nqt, n_q_blocks);
         const uint32_t slot = g & 1;
         const uint32_t vL2 = sVec_a + slot * 2 * BM * 4, vD = vL2 + BM * 4;
         const bool need_mask = (CAUSAL && i == nb) || (nb * 128 + 128 > N);
@@ -258,7 +258,7 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
       const int i0 = q_begin(nb), nqt = n_q_blocks - i0;
       const int bq0 = (bh / p.Hkv) * p.H + (bh % p.Hkv) * p.group;   // first query head of this kv head
       for (int x = 0; x < nqt * p.group; ++x, ++g) {
-        const int i = i0 + x % nqt, bhq = bq0 + x / nqt;
+        const int i = bwd_q_tile(p, CAUSAL, nb, x % nqt, n_q_blocks), bhq = bq0 + x / nqt;
         ptx::mbar_wait(dq_full, g & 1);
         if (leader) FA2_BTRACE(9, g);
         ptx::tc_fence_after();
@@ -277,7 +277,11 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
 #pragma unroll
         for (int rd = 0; rd < BM / L::DQ_ROWS; ++rd) {
           const int buf = rd % L::DQ_NBUF;
-          if (leader) ptx::bulk_wait_read<L::DQ_NBUF - 1>();
+          if (leader) {
+            ptx::bulk_wait_read<L::DQ_NBUF - 1>();
+            // deterministic mode: wait for this key block's turn on dQ tile (bhq, i)
+            if (p.dq_sem != nullptr && rd == 0) dq_sem_wait(dq_sem_ptr(p, bhq, i, n_q_blocks), dq_rank(p, nb, x % nqt));
+          }
           ptx::named_bar_sync(1, 128);
 #pragma unroll
           for (int q = 0; q < L::DQ_ROWS; ++q)
@@ -290,6 +294,7 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
             ptx::bulk_commit();
           }
         }
+        if (leader && p.dq_sem != nullptr) dq_sem_release(dq_sem_ptr(p, bhq, i, n_q_blocks), dq_rank(p, nb, x % nqt));
         if (leader) FA2_BTRACE(16, g);
       }
     }
@@ -419,7 +424,7 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
         const int i0 = q_begin(nb), nqt = n_q_blocks - i0;
         const int bq0 = (bh / p.Hkv) * p.H + (bh % p.Hkv) * p.group;
         for (int x = 0; x < nqt * p.group; ++x, ++g) {
-          const int i = i0 + x % nqt, bhq = bq0 + x / nqt;
+          const int i = bwd_q_tile(p, CAUSAL, nb, x % nqt, n_q_blocks), bhq = bq0 + x / nqt;
           const uint32_t slot = g & 1;
           // Q_i, L_i, D_i (2-stage ring; released after dK(i))
           if (g >= 2) ptx::mbar_wait(&q_empty[slot], ((g >> 1) - 1) & 1);

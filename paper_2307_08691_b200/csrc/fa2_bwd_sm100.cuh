@@ -53,7 +53,64 @@ struct BwdParams {
   float scale;
   float scale_log2;
   unsigned long long* trace;  // optional clock64 trace (CTA 0, first work tile), nullptr in production
+  int* dq_sem;          // deterministic mode: [BH, num_n_blocks] dQ tile counters (nullptr: arrival order)
+  int det_cyclic;       // deterministic schedule (see bwd_q_tile): 1 when num_n_blocks <= gridDim.x
 };
+
+// ---------------------------------------------------------------------------
+// Work schedule shared by every warp role of both backward kernels.
+//
+// A work tile t is (head bh, key block nb), t = bh * num_n_blocks + nb; CTA b takes
+// t = b, b + grid, ...  Within a tile the query tiles are visited in steps s = 0 .. nqt-1.
+//
+// Deterministic mode (P:494-496 accumulate dQ_i with atomics, whose
+// order is arbitrary): every dQ tile (query head bhq, query tile i) receives the
+// contributions of its key blocks in a FIXED order, enforced by a counter per tile:
+// the dQ issuer of key block nb waits until dq_sem[bhq, i] == rank(nb, i), issues its
+// fp32 reduce-adds, waits for them to complete, then stores rank + 1.
+//   det_cyclic = 1 (num_n_blocks <= grid, so a CTA holds at most one tile of any head,
+//   and the grid is a multiple of num_n_blocks so a head's tiles run side by side):
+//     non-causal: step s visits i = (nb + s) mod n, causal: i = nb + s; rank = s, i.e.
+//     the predecessor of (nb, step s) is (nb + 1, step s - 1): the CTAs of one head wait
+//     on one another's previous step only, and no skew accumulates.  Causal work tiles
+//     alternate heavy/light key blocks between iterations to balance the CTAs.
+//   det_cyclic = 0 (a head spans more than the grid): rank = nb (ascending key blocks);
+//     every wait points to a lower work tile, so progress is guaranteed.
+// ---------------------------------------------------------------------------
+FA2_DEVICE void bwd_decode(const BwdParams& p, bool causal, int t, int& bh, int& nb) {
+  bh = t / p.num_n_blocks;
+  nb = t % p.num_n_blocks;
+  if (causal && p.dq_sem != nullptr && p.det_cyclic && ((t / static_cast<int>(gridDim.x)) & 1))
+    nb = p.num_n_blocks - 1 - nb;
+}
+FA2_DEVICE int bwd_q_tile(const BwdParams& p, bool causal, int nb, int s, int n_q_blocks) {
+  if (causal) return nb + s;                       // B_r == B_c: key block nb starts at query tile nb
+  if (p.dq_sem != nullptr && p.det_cyclic) return nb + s < n_q_blocks ? nb + s : nb + s - n_q_blocks;
+  return s;
+}
+// One counter per dQ tile: dq_sem[bhq * n_q_blocks + i] = number of key blocks whose
+// contribution has landed.  The dQ issuer of key block nb spins (acquire) until the
+// counter equals its rank, issues the tile's reduce-adds, waits for them to COMPLETE,
+// then stores rank + 1 (release).  A blocked issuer holds no pending release, and the
+// waits point to (key block + 1, step - 1) in the cyclic schedule or to a lower work
+// tile in the ascending one, so the wait graph is acyclic and every CTA progresses.
+// (Finer-grained counters per part of a tile, with deferred releases, were measured
+// slower: tools/bench_det.py.)
+FA2_DEVICE int* dq_sem_ptr(const BwdParams& p, int bhq, int i, int n_q_blocks) {
+  return p.dq_sem + static_cast<size_t>(bhq) * n_q_blocks + i;
+}
+FA2_DEVICE int dq_rank(const BwdParams& p, int nb, int s) { return p.det_cyclic ? s : nb; }
+FA2_DEVICE void dq_sem_wait(const int* sem, int rank) {
+  while (ptx::ld_acquire_gpu(sem) != rank) {
+  }
+  ptx::fence_proxy_async_global();
+}
+// after the tile's reduce-adds were committed (one or more bulk groups)
+FA2_DEVICE void dq_sem_release(int* sem, int rank) {
+  ptx::bulk_wait<0>();
+  ptx::fence_proxy_async_global();
+  ptx::st_release_gpu(sem, rank + 1);
+}
 
 // Debug timeline: trace[ev * 64 + h] = clock64() for CTA 0's first 64 query tiles.
 #define FA2_BTRACE(ev, h)                                                                       \
@@ -66,6 +123,7 @@ struct BwdParams {
 //   dvec[r] = sum_c dO[r,c] * O[r,c]         (r < N)      else 0
 //   lse2[r] = L[r] * log2(e)                 (r < N)      else +inf
 //   dq_acc[r, :] = 0
+//   dq_sem[bh, r / 128] = 0                  (deterministic mode, first row of a tile)
 // When dq_acc == nullptr (fa2_backward_preprocess) only dvec is written and
 // npad == N, lse == nullptr.
 // ---------------------------------------------------------------------------
@@ -73,7 +131,7 @@ template <int D, bool BF16>
 __global__ void __launch_bounds__(256)
 fa2_bwd_preprocess(const void* __restrict__ o, const void* __restrict__ dout, float* __restrict__ dvec,
                    float* __restrict__ dq_acc, int BH, int N, int npad, const float* __restrict__ lse = nullptr,
-                   float* __restrict__ lse2 = nullptr) {
+                   float* __restrict__ lse2 = nullptr, int* __restrict__ dq_sem = nullptr) {
   const long long row = static_cast<long long>(blockIdx.x) * 8 + threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   if (row >= static_cast<long long>(BH) * npad) return;
@@ -102,6 +160,7 @@ fa2_bwd_preprocess(const void* __restrict__ o, const void* __restrict__ dout, fl
     dvec[row] = acc;
     if (lse2 != nullptr) lse2[row] = (r < N) ? lse[static_cast<size_t>(bh) * N + r] * 1.4426950408889634f : INFINITY;
   }
+  if (dq_sem != nullptr && r % 128 == 0 && lane == 0) dq_sem[static_cast<size_t>(bh) * (npad / 128) + r / 128] = 0;
   if (dq_acc != nullptr) {
     float4* z = reinterpret_cast<float4*>(dq_acc + row * D);
     for (int c = lane; c < D / 4; c += 32) z[c] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -228,7 +287,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   const float* gL2 = p.dvec + static_cast<size_t>(p.BH) * p.npad;
 
   // tile t -> (bh, n_block); for causal, low n_block (more query blocks) first
-  auto decode = [&](int t, int& bh, int& nb) { bh = t / p.num_n_blocks; nb = t % p.num_n_blocks; };
+  auto decode = [&](int t, int& bh, int& nb) { bwd_decode(p, CAUSAL, t, bh, nb); };
   auto q_begin = [&](int nb) -> int { return CAUSAL ? (nb * 128) / BM : 0; };
 
   if (warp < 8) {
@@ -246,7 +305,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       const int i0 = q_begin(nb), nqt = n_q_blocks - i0;
       const int bq0 = (bh / p.Hkv) * p.H + (bh % p.Hkv) * p.group;   // first query head of this kv head
       for (int x = 0; x < nqt * p.group; ++x, ++g) {
-        const int i = i0 + x % nqt, bhq = bq0 + x / nqt;            // query tile, query head
+        const int i = bwd_q_tile(p, CAUSAL, nb, x % nqt, n_q_blocks), bhq = bq0 + x / nqt;  // query tile, query head
         const int slot = g % STAGES;
         ptx::mbar_wait(&q_full[slot], (g / STAGES) & 1);
         ptx::mbar_wait(s_full, g & 1);
@@ -354,7 +413,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       const int i0 = q_begin(nb), nqt = n_q_blocks - i0;
       const int bq0 = (bh / p.Hkv) * p.H + (bh % p.Hkv) * p.group;   // first query head of this kv head
       for (int x = 0; x < nqt * p.group; ++x, ++g) {
-        const int i = i0 + x % nqt, bhq = bq0 + x / nqt;            // query tile, query head
+        const int i = bwd_q_tile(p, CAUSAL, nb, x % nqt, n_q_blocks), bhq = bq0 + x / nqt;  // query tile, query head
         ptx::mbar_wait(dq_full, g & 1);
         if (leader) FA2_BTRACE(7, g);
         ptx::tc_fence_after();
@@ -366,7 +425,8 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(dq_empty);
-        // staging buffer free? (the previous reduce-add has finished reading it)
+        // staging buffer free? (the previous reduce-add has finished reading it); in
+        // deterministic mode also wait for this key block's turn on dQ tile (bhq, i)
         if (leader) ptx::bulk_wait_read<0>();
         ptx::named_bar_sync(1, 128);
         if constexpr (DQT) {
@@ -393,8 +453,12 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         ptx::named_bar_sync(1, 128);
         if (leader) {
 #pragma unroll
+          // deterministic mode: wait for this key block's turn on dQ tile (bhq, i)
+          if (p.dq_sem != nullptr) dq_sem_wait(dq_sem_ptr(p, bhq, i, n_q_blocks), dq_rank(p, nb, x % nqt));
+#pragma unroll
           for (int b = 0; b < D / 32; ++b) ptx::tma_reduce_add_3d(&tm_dq, sDQ + b * (BM * 128), b * 32, i * BM, bhq);
           ptx::bulk_commit();
+          if (p.dq_sem != nullptr) dq_sem_release(dq_sem_ptr(p, bhq, i, n_q_blocks), dq_rank(p, nb, x % nqt));
           FA2_BTRACE(8, g);
         }
       }
@@ -518,7 +582,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           ptx::tma_load_3d_hint(sV + s * 128 * 128, &tm_v, kv_full, s * 64, nb * 128, bh, pol_kv);
         }
         for (int x = 0; x < nqt * p.group; ++x, ++g) {
-          const int i = i0 + x % nqt, bhq = bq0 + x / nqt;
+          const int i = bwd_q_tile(p, CAUSAL, nb, x % nqt, n_q_blocks), bhq = bq0 + x / nqt;
           const int slot = g % STAGES;
           if (g >= STAGES) ptx::mbar_wait(&q_empty[slot], ((g / STAGES) - 1) & 1);
           ptx::mbar_arrive_expect_tx(&q_full[slot], 2 * L::Q_TILE + 2 * BM * 4);

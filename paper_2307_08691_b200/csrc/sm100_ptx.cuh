@@ -93,6 +93,17 @@ FA2_DEVICE void sts_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32
 FA2_DEVICE void fence_proxy_async_smem() {  // generic-proxy smem writes -> visible to TMA / UMMA
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+FA2_DEVICE void fence_proxy_async_global() {  // order async-proxy (bulk) global accesses vs generic ones
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+FA2_DEVICE int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+FA2_DEVICE void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
 FA2_DEVICE void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(nthreads) : "memory");
 }

@@ -73,7 +73,8 @@ def test_forward_validation(L):
 def test_backward_validation(L):
     ws = L.fa2_backward_workspace_size(2, 3, 100, 64)
     npad = 128
-    assert ws == 2 * 3 * npad * 64 * 4 + 2 * 2 * 3 * npad * 4
+    sem = (2 * 3 * (npad // 128) * 4 + 15) // 16 * 16
+    assert ws == 2 * 3 * npad * 64 * 4 + 2 * 2 * 3 * npad * 4 + sem
     assert L.fa2_backward_workspace_size(1, 1, 1, 96) == 0
     args = FAKE[:9]
     r = L.fa2_backward(*args, ctypes.c_void_p(1 << 20), ws - 1, 2, 3, 100, 64, 0, 0.125, 0, None)
@@ -135,5 +136,10 @@ def test_gqa_validation(L):
     assert L.fa2_forward_gqa(p[0], p[1], p[2], p[3], p[4], 1, 6, 3, 128, 96, 0, 0.125, 0, None) == 2
     ws = ctypes.c_void_p(1 << 20)
     assert L.fa2_backward_gqa(*p[:9], ws, 1 << 30, 1, 8, 3, 128, 64, 0, 0.125, 0, None) == 1
+    # the deterministic entry point validates exactly like fa2_backward_gqa
+    assert L.fa2_backward_deterministic(*p[:9], ws, 1 << 30, 1, 8, 3, 128, 64, 0, 0.125, 0, None) == 1
+    assert L.fa2_backward_deterministic(*p[:9], ws, 16, 1, 8, 2, 128, 64, 0, 0.125, 0, None) == 3
+    assert L.fa2_backward_deterministic(*p[:9], ws, 1 << 30, 1, 8, 2, 128, 96, 0, 0.125, 0, None) == 2
+    assert L.fa2_backward_deterministic(*p[:9], ws, 1 << 30, 1, 8, 2, 128, 64, 1, 0.125, 0, None) in (2, 4)
     # valid GQA arguments reach CUDA (no device here)
     assert L.fa2_forward_gqa(p[0], p[1], p[2], p[3], p[4], 1, 8, 2, 128, 64, 1, 0.125, 0, None) in (2, 4)
