@@ -19,7 +19,9 @@ Conventions (R1, R2, R8, R10):
   * ``scale`` multiplies QK^T before the softmax (P:160-162 footnote; read as
     1/sqrt(d) by default, R1).  The caller passes the exact value the kernel
     receives (a float32), and it is used as float64(float32(scale)).
-  * causal: S_ij = -inf for j > i, top-left aligned, N_q = N_k.
+  * causal: S_ij = -inf for j > i, top-left aligned, N_q = N_k (P:375-377);
+    the *_general / *_varlen functions extend it bottom-right aligned to
+    N_q != N_k (R22) with empty rows O = 0, L = -inf (R23).
   * L is the natural-log logsumexp of the *scaled* logits.
 
 Pins: every function here is checked by ``tests/test_oracle.py`` against
@@ -44,6 +46,15 @@ __all__ = [
     "rowsum_dO_O",
     "forward_rows",
     "backward_sampled_head",
+    "naive_softmax_no_max",
+    "forward_gqa",
+    "backward_gqa",
+    "scores_general",
+    "softmax_rows_general",
+    "forward_head_general",
+    "backward_head_general",
+    "forward_varlen",
+    "backward_varlen",
 ]
 
 
@@ -306,4 +317,128 @@ def backward_gqa(q, k, v, do, scale: float, causal: bool):
             dq[bi, hi], dkh, dvh, _ = backward_head(q[bi, hi], k[bi, g], v[bi, g], do[bi, hi], scale, causal)
             dk[bi, g] += dkh
             dv[bi, g] += dvh
+    return dq, dk, dv
+
+
+# ---------------------------------------------------------------------------
+# N_q != N_k and variable-length batches.  The paper defines
+# causal masking only for N_q == N_k; readings:
+#   R22  causal with N_q != N_k is aligned to the BOTTOM-RIGHT corner: query
+#        row i (0-based) sees key j iff j <= i + (N_k - N_q).  For N_q == N_k
+#        this is exactly the mask of ``scores``.
+#   R23  a query row that sees no key (possible when N_q > N_k, causal, or
+#        N_k == 0) has O_i = 0 and L_i = -inf (the log of an empty sum); it
+#        contributes nothing to any gradient.
+# Variable-length batches use the packed layout: q [T_q, H, d], k and v
+# [T_k, H_kv, d], sequence b = rows cu_q[b]:cu_q[b+1] of q and cu_k[b]:cu_k[b+1]
+# of k/v; L is [H, T_q].  Every sequence is an independent attention problem
+# (the per-(b,h) independence of P:162-165).
+# ---------------------------------------------------------------------------
+
+def scores_general(q, k, scale: float, causal: bool) -> np.ndarray:
+    """S = scale * Q K^T [N_q, N_k]; causal mask bottom-right aligned (R22)."""
+    q = np.asarray(q, dtype=np.float64)
+    k = np.asarray(k, dtype=np.float64)
+    s = as_f64_scale(scale) * (q @ k.T)
+    if causal:
+        n_q, n_k = s.shape
+        rows = np.arange(n_q)[:, None]
+        cols = np.arange(n_k)[None, :]
+        s = np.where(cols > rows + (n_k - n_q), -np.inf, s)
+    return s
+
+
+def softmax_rows_general(s: np.ndarray):
+    """``softmax_rows`` extended to rows with no finite entry (R23):
+    for those m = -inf, l = 0 and the row of P is 0.  Returns (P, m, l)."""
+    n_q = s.shape[0]
+    m = np.max(s, axis=1) if s.shape[1] > 0 else np.full(n_q, -np.inf)
+    finite = np.isfinite(m)
+    e = np.exp(s - np.where(finite, m, 0.0)[:, None])       # exp(-inf) = 0 on empty rows
+    ell = np.sum(e, axis=1)
+    p = np.where(ell[:, None] > 0, e / np.where(ell > 0, ell, 1.0)[:, None], 0.0)
+    return p, m, ell
+
+
+def forward_head_general(q, k, v, scale: float, causal: bool):
+    """One head, N_q x N_k (R22, R23): O = P V, L = m + log l (-inf on empty rows)."""
+    v = np.asarray(v, dtype=np.float64)
+    s = scores_general(q, k, scale, causal)
+    p, m, ell = softmax_rows_general(s)
+    o = p @ v if v.shape[0] > 0 else np.zeros((s.shape[0], v.shape[1]))
+    with np.errstate(divide="ignore"):
+        lse = np.where(ell > 0, m + np.log(np.where(ell > 0, ell, 1.0)), -np.inf)
+    return o, lse
+
+
+def backward_head_general(q, k, v, do, scale: float, causal: bool):
+    """The backward of ``backward_head`` for N_q x N_k (R22, R23).
+    Returns (dQ [N_q,d], dK [N_k,d], dV [N_k,d], D [N_q])."""
+    q = np.asarray(q, dtype=np.float64)
+    k = np.asarray(k, dtype=np.float64)
+    v = np.asarray(v, dtype=np.float64)
+    do = np.asarray(do, dtype=np.float64)
+    s = scores_general(q, k, scale, causal)
+    p, _, _ = softmax_rows_general(s)
+    dv = p.T @ do
+    dp = do @ v.T
+    dd = np.sum(p * dp, axis=1)
+    ds = p * (dp - dd[:, None])
+    sc = as_f64_scale(scale)
+    return sc * (ds @ k), sc * (ds.T @ q), dv, dd
+
+
+def _check_cu(cu, total, name):
+    cu = np.asarray(cu, dtype=np.int64)
+    if cu.ndim != 1 or len(cu) < 2 or cu[0] != 0 or cu[-1] != total or np.any(np.diff(cu) < 0):
+        raise ValueError(f"{name} must be non-decreasing, start at 0 and end at {total}")
+    return cu
+
+
+def forward_varlen(q, k, v, cu_q, cu_k, scale: float, causal: bool):
+    """Packed variable-length batch: q [T_q,H,d], k/v [T_k,H_kv,d] ->
+    (O [T_q,H,d], L [H,T_q]).  Query head h uses key/value head h // (H/H_kv)
+    (P:444-452)."""
+    q = np.asarray(q, dtype=np.float64)
+    k = np.asarray(k, dtype=np.float64)
+    v = np.asarray(v, dtype=np.float64)
+    t_q, h, d = q.shape
+    h_kv = k.shape[1]
+    group = h // h_kv
+    cu_q = _check_cu(cu_q, t_q, "cu_q")
+    cu_k = _check_cu(cu_k, k.shape[0], "cu_k")
+    o = np.zeros((t_q, h, v.shape[2]))
+    lse = np.full((h, t_q), -np.inf)
+    for b in range(len(cu_q) - 1):
+        qs, qe, ks, ke = cu_q[b], cu_q[b + 1], cu_k[b], cu_k[b + 1]
+        for hi in range(h):
+            o[qs:qe, hi], lse[hi, qs:qe] = forward_head_general(
+                q[qs:qe, hi], k[ks:ke, hi // group], v[ks:ke, hi // group], scale, causal)
+    return o, lse
+
+
+def backward_varlen(q, k, v, do, cu_q, cu_k, scale: float, causal: bool):
+    """Packed variable-length backward: returns (dQ [T_q,H,d], dK [T_k,H_kv,d],
+    dV [T_k,H_kv,d]); dK/dV of a key/value head sum over its query heads."""
+    q = np.asarray(q, dtype=np.float64)
+    k = np.asarray(k, dtype=np.float64)
+    v = np.asarray(v, dtype=np.float64)
+    do = np.asarray(do, dtype=np.float64)
+    t_q, h, d = q.shape
+    h_kv = k.shape[1]
+    group = h // h_kv
+    cu_q = _check_cu(cu_q, t_q, "cu_q")
+    cu_k = _check_cu(cu_k, k.shape[0], "cu_k")
+    dq = np.zeros_like(q)
+    dk = np.zeros_like(k)
+    dv = np.zeros_like(v)
+    for b in range(len(cu_q) - 1):
+        qs, qe, ks, ke = cu_q[b], cu_q[b + 1], cu_k[b], cu_k[b + 1]
+        for hi in range(h):
+            g = hi // group
+            gq, gk, gv, _ = backward_head_general(q[qs:qe, hi], k[ks:ke, g], v[ks:ke, g], do[qs:qe, hi],
+                                                  scale, causal)
+            dq[qs:qe, hi] = gq
+            dk[ks:ke, g] += gk
+            dv[ks:ke, g] += gv
     return dq, dk, dv

@@ -462,3 +462,181 @@ def test_gqa_finite_differences():
         args[which][idx] -= 2 * eps
         fm = f(*args)
         assert abs((fp - fm) / (2 * eps) - grad[idx]) < 1e-7
+
+
+# --------------------------------------------------------------------------
+# N_q != N_k (bottom-right causal, R22), empty rows (R23), packed varlen
+# --------------------------------------------------------------------------
+
+def _brute_general(q, k, v, do, scale, causal):
+    """Pure-Python loops: forward O, L and backward dQ, dK, dV for an N_q x N_k
+    head with the bottom-right causal mask (j visible iff j <= i + N_k - N_q);
+    rows with no visible key give O = 0, L = -inf and no gradient."""
+    nq, nk, d = len(q), len(k), len(q[0])
+    off = nk - nq
+    o = [[0.0] * len(v[0]) if nk else [0.0] * d for _ in range(nq)]
+    lse = [-math.inf] * nq
+    p = [[0.0] * nk for _ in range(nq)]
+    for i in range(nq):
+        vis = [j for j in range(nk) if not (causal and j > i + off)]
+        if not vis:
+            continue
+        s = {j: scale * math.fsum(q[i][t] * k[j][t] for t in range(d)) for j in vis}
+        mx = max(s.values())
+        den = math.fsum(math.exp(x - mx) for x in s.values())
+        for j in vis:
+            p[i][j] = math.exp(s[j] - mx) / den
+        o[i] = [math.fsum(p[i][j] * v[j][c] for j in vis) for c in range(len(v[0]))]
+        lse[i] = mx + math.log(den)
+    dq = [[0.0] * d for _ in range(nq)]
+    dk = [[0.0] * d for _ in range(nk)]
+    dv = [[0.0] * len(v[0]) for _ in range(nk)]
+    for i in range(nq):
+        dp = [math.fsum(do[i][t] * v[j][t] for t in range(len(v[0]))) for j in range(nk)]
+        for j in range(nk):
+            ds = math.fsum(p[i][j] * ((1.0 if a == j else 0.0) - p[i][a]) * dp[a] for a in range(nk))
+            for t in range(d):
+                dq[i][t] += scale * ds * k[j][t]
+                dk[j][t] += scale * ds * q[i][t]
+            for t in range(len(v[0])):
+                dv[j][t] += p[i][j] * do[i][t]
+    return [np.array(x, dtype=np.float64) for x in (o, lse, dq, dk, dv)]
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("nq,nk", [(3, 7), (7, 3), (5, 5), (1, 4), (4, 1), (6, 0)])
+def test_general_matches_brute_force(nq, nk, causal):
+    r = rng(100 + 10 * nq + nk)
+    d = 3
+    q, do = r.normal(size=(2, nq, d))
+    k, v = r.normal(size=(2, nk, d))
+    scale = float(np.float32(0.8))
+    o, lse = R.forward_head_general(q, k, v, scale, causal)
+    dq, dk, dv, _ = R.backward_head_general(q, k, v, do, scale, causal)
+    bo, bl, bq, bk, bv = _brute_general(q.tolist(), k.tolist(), v.tolist(), do.tolist(), scale, causal)
+    assert np.max(np.abs(o - bo), initial=0) < 1e-13
+    assert np.array_equal(np.isinf(lse), np.isinf(bl))
+    fin = np.isfinite(bl)
+    assert np.max(np.abs(lse[fin] - bl[fin]), initial=0) < 1e-13
+    for a, b in ((dq, bq), (dk, bk), (dv, bv)):
+        assert np.max(np.abs(a - np.reshape(b, a.shape)), initial=0) < 1e-12
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_general_reduces_to_square(causal):
+    """N_q == N_k: the bottom-right mask is the paper's mask."""
+    r = rng(120)
+    q, k, v, do = r.normal(size=(4, 9, 4))
+    o, lse = R.forward_head_general(q, k, v, 0.5, causal)
+    o2, l2 = R.forward_head(q, k, v, 0.5, causal)
+    assert np.max(np.abs(o - o2)) < 1e-15 and np.max(np.abs(lse - l2)) < 1e-15
+    g = R.backward_head_general(q, k, v, do, 0.5, causal)
+    g2 = R.backward_head(q, k, v, do, 0.5, causal)
+    for a, b in zip(g, g2):
+        assert np.max(np.abs(a - b)) < 1e-15
+
+
+def test_general_closed_forms():
+    r = rng(121)
+    d = 4
+    # N_q > N_k causal: the first N_q - N_k rows see nothing, row N_q - N_k sees key 0 only
+    nq, nk = 9, 4
+    q = r.normal(size=(nq, d)); k = r.normal(size=(nk, d)); v = r.normal(size=(nk, d))
+    sc = float(np.float32(0.5))
+    o, lse = R.forward_head_general(q, k, v, sc, True)
+    assert np.all(o[:nq - nk] == 0) and np.all(lse[:nq - nk] == -np.inf)
+    assert np.max(np.abs(o[nq - nk] - v[0])) < 1e-15
+    assert abs(lse[nq - nk] - sc * float(q[nq - nk] @ k[0])) < 1e-14
+    # N_q < N_k causal: row i is plain attention over the first i + N_k - N_q + 1 keys
+    nq, nk = 4, 11
+    q = r.normal(size=(nq, d)); k = r.normal(size=(nk, d)); v = r.normal(size=(nk, d))
+    o, lse = R.forward_head_general(q, k, v, sc, True)
+    for i in range(nq):
+        m = i + nk - nq + 1
+        oi, li = R.forward_head(q[i:i + 1], k[:m], v[:m], sc, False)
+        assert np.max(np.abs(o[i] - oi[0])) < 1e-14 and abs(lse[i] - li[0]) < 1e-14
+    # empty rows carry no gradient
+    dq, dk, dv, dd = R.backward_head_general(q[:1].repeat(3, 0), k[:1], v[:1], r.normal(size=(3, d)), sc, True)
+    assert np.all(dq[:2] == 0) and np.all(dd[:2] == 0)
+
+
+@pytest.mark.parametrize("nq,nk", [(5, 8), (8, 5)])
+def test_general_finite_differences(nq, nk):
+    r = rng(122 + nq)
+    d = 3
+    q, g = r.normal(size=(2, nq, d))
+    k, v = r.normal(size=(2, nk, d))
+    sc = float(np.float32(0.6))
+    dq, dk, dv, _ = R.backward_head_general(q, k, v, g, sc, True)
+
+    def f(qq, kk, vv):
+        return float(np.sum(R.forward_head_general(qq, kk, vv, sc, True)[0] * g))
+
+    h = 1e-6
+    for which, grad, idx in ((0, dq, (nq - 1, 1)), (0, dq, (nq // 2, 0)), (1, dk, (0, 2)), (1, dk, (nk - 1, 0)),
+                             (2, dv, (1, 1)), (2, dv, (nk - 1, 2))):
+        args = [q.copy(), k.copy(), v.copy()]
+        args[which][idx] += h
+        fp = f(*args)
+        args[which][idx] -= 2 * h
+        fm = f(*args)
+        assert abs((fp - fm) / (2 * h) - grad[idx]) < 1e-7, (which, idx)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_varlen_matches_brute_force(causal):
+    """Packed batch with an empty query sequence, N_q > N_k and N_q < N_k
+    sequences, and GQA (H = 4 query heads on H_kv = 2)."""
+    r = rng(130)
+    cu_q = [0, 3, 3, 8, 10]
+    cu_k = [0, 5, 7, 9, 9 + 6]
+    h, h_kv, d = 4, 2, 3
+    q = r.normal(size=(cu_q[-1], h, d)); do = r.normal(size=(cu_q[-1], h, d))
+    k = r.normal(size=(cu_k[-1], h_kv, d)); v = r.normal(size=(cu_k[-1], h_kv, d))
+    sc = float(np.float32(0.7))
+    o, lse = R.forward_varlen(q, k, v, cu_q, cu_k, sc, causal)
+    dq, dk, dv = R.backward_varlen(q, k, v, do, cu_q, cu_k, sc, causal)
+    dk_b = np.zeros_like(k); dv_b = np.zeros_like(v)
+    for b in range(len(cu_q) - 1):
+        qs, qe, ks, ke = cu_q[b], cu_q[b + 1], cu_k[b], cu_k[b + 1]
+        if qe == qs:   # an empty query sequence: nothing to compute, no gradient for its keys
+            assert np.all(dk[ks:ke] == 0) and np.all(dv[ks:ke] == 0)
+            continue
+        for hi in range(h):
+            g = hi // (h // h_kv)
+            bo, bl, bq, bk, bv = _brute_general(q[qs:qe, hi].tolist(), k[ks:ke, g].tolist(), v[ks:ke, g].tolist(),
+                                                do[qs:qe, hi].tolist(), sc, causal)
+            if qe > qs:
+                assert np.max(np.abs(o[qs:qe, hi] - bo)) < 1e-13
+                fin = np.isfinite(bl)
+                assert np.array_equal(np.isinf(lse[hi, qs:qe]), ~fin)
+                assert np.max(np.abs(lse[hi, qs:qe][fin] - bl[fin]), initial=0) < 1e-13
+                assert np.max(np.abs(dq[qs:qe, hi] - bq)) < 1e-12
+            if ke > ks:
+                dk_b[ks:ke, g] += bk
+                dv_b[ks:ke, g] += bv
+    assert np.max(np.abs(dk - dk_b)) < 1e-12 and np.max(np.abs(dv - dv_b)) < 1e-12
+
+
+def test_varlen_finite_differences():
+    r = rng(131)
+    cu_q, cu_k = [0, 4, 9], [0, 6, 9]
+    q = r.normal(size=(9, 2, 3)); g = r.normal(size=(9, 2, 3))
+    k = r.normal(size=(9, 1, 3)); v = r.normal(size=(9, 1, 3))
+    dq, dk, dv = R.backward_varlen(q, k, v, g, cu_q, cu_k, 0.9, True)
+    f = lambda qq, kk, vv: float(np.sum(R.forward_varlen(qq, kk, vv, cu_q, cu_k, 0.9, True)[0] * g))
+    h = 1e-6
+    for which, grad, idx in ((0, dq, (8, 1, 2)), (1, dk, (7, 0, 1)), (2, dv, (2, 0, 0)), (1, dk, (0, 0, 2))):
+        args = [q.copy(), k.copy(), v.copy()]
+        args[which][idx] += h
+        fp = f(*args)
+        args[which][idx] -= 2 * h
+        fm = f(*args)
+        assert abs((fp - fm) / (2 * h) - grad[idx]) < 1e-7, (which, idx)
+
+
+def test_varlen_rejects_bad_offsets():
+    z = np.zeros((4, 1, 2))
+    for cu in ([0, 5], [1, 4], [0, 3, 2, 4], [0]):
+        with pytest.raises(ValueError):
+            R.forward_varlen(z, z, z, cu, [0, 4], 1.0, False)
