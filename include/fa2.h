@@ -96,6 +96,35 @@ FA2_API fa2_status_t fa2_backward_gqa(const void* q, const void* k, const void* 
                                       int B, int H, int H_kv, int N, int d, int causal, float softmax_scale,
                                       fa2_dtype_t dtype, void* stream);
 
+/* General fixed-length attention: q, o [B,H,N_q,d]; k, v
+ * [B,H_kv,N_k,d]; lse [B,H,N_q].  N_q may differ from N_k.  The paper defines the
+ * causal mask only for N_q == N_k; here it is aligned to the
+ * bottom-right corner: query row i sees key j iff j <= i + (N_k - N_q)
+ * (R22), which is the paper's mask when N_q == N_k.  A row that sees no
+ * key (causal with N_q > N_k) gets O = 0 and lse = -inf (R23).  fa2_forward and
+ * fa2_forward_gqa are the special cases N_q == N_k.  Errors as fa2_forward_gqa,
+ * plus FA2_ERR_INVALID_ARG for N_k < 1. */
+FA2_API fa2_status_t fa2_forward_ex(const void* q, const void* k, const void* v, void* o, float* lse,
+                                    int B, int H, int H_kv, int N_q, int N_k, int d, int causal,
+                                    float softmax_scale, fa2_dtype_t dtype, void* stream);
+
+/* Variable-length batch in the packed layout: sequence b is rows
+ * [cu_seqlens_q[b], cu_seqlens_q[b+1]) of q, o ([total_q, H, d], contiguous) and
+ * rows [cu_seqlens_k[b], cu_seqlens_k[b+1]) of k, v ([total_k, H_kv, d]); lse is
+ * [H, total_q] fp32.  cu_seqlens_q / cu_seqlens_k are DEVICE int32 arrays of
+ * B+1 entries, non-decreasing, starting at 0 and ending at total_q / total_k
+ * (not validated on the host: that would need a device sync; a violation gives
+ * undefined results).  max_seqlen_q / _k must be >= every sequence's length
+ * (they size the tile grid; rows past max_seqlen_q are not computed).  Empty
+ * sequences are allowed.  Masking per sequence as fa2_forward_ex (R22, R23).
+ * Errors: FA2_ERR_INVALID_ARG for NULL / misaligned pointers, B, H < 1, H not
+ * a multiple of H_kv, total_q or total_k < 1, max_seqlen outside [1, total];
+ * FA2_ERR_UNSUPPORTED as fa2_forward. */
+FA2_API fa2_status_t fa2_forward_varlen(const void* q, const void* k, const void* v, void* o, float* lse,
+                                        const int* cu_seqlens_q, const int* cu_seqlens_k, int B, int H, int H_kv,
+                                        int total_q, int total_k, int max_seqlen_q, int max_seqlen_k, int d,
+                                        int causal, float softmax_scale, fa2_dtype_t dtype, void* stream);
+
 /* Deterministic backward.  Same arguments, layouts, workspace and
  * errors as fa2_backward_gqa (H_kv == H for plain multi-head attention); the
  * result is bitwise reproducible from run to run on the same device and
@@ -111,6 +140,38 @@ FA2_API fa2_status_t fa2_backward_deterministic(const void* q, const void* k, co
                                                 void* workspace, size_t workspace_bytes,
                                                 int B, int H, int H_kv, int N, int d, int causal,
                                                 float softmax_scale, fa2_dtype_t dtype, void* stream);
+
+/* Backward of fa2_forward_ex (N_q may differ from N_k; causal bottom-right
+ * aligned, R22; rows that saw no key contribute nothing, R23): q, o, dout, dq
+ * [B,H,N_q,d]; k, v, dk, dv [B,H_kv,N_k,d]; lse [B,H,N_q] as fa2_forward_ex wrote
+ * it.  Workspace: fa2_backward_workspace_size(B, H, N_q, d) bytes.
+ * deterministic != 0 gives the fixed dQ summation order of
+ * fa2_backward_deterministic.  Errors as fa2_backward_gqa, plus
+ * FA2_ERR_INVALID_ARG for N_k < 1. */
+FA2_API fa2_status_t fa2_backward_ex(const void* q, const void* k, const void* v, const void* o,
+                                     const float* lse, const void* dout, void* dq, void* dk, void* dv,
+                                     void* workspace, size_t workspace_bytes,
+                                     int B, int H, int H_kv, int N_q, int N_k, int d, int causal,
+                                     float softmax_scale, int deterministic, fa2_dtype_t dtype, void* stream);
+
+/* Bytes of device scratch fa2_backward_varlen needs for B sequences with total_q
+ * query rows: the same buffers as fa2_backward_workspace_size over padded query
+ * rows (every sequence padded to a multiple of 128 rows; at most
+ * H * (total_q + 127 B) rounded up to 128), plus [B+1] int32 tile offsets. */
+FA2_API size_t fa2_backward_varlen_workspace_size(int B, int H, int total_q, int d);
+
+/* Backward of fa2_forward_varlen (packed layout, same arguments and layouts;
+ * dq [total_q, H, d], dk, dv [total_k, H_kv, d]).  Key rows of a sequence with
+ * no query row get dK = dV = 0.  deterministic != 0: fixed dQ summation order.
+ * Workspace: fa2_backward_varlen_workspace_size(B, H, total_q, d).  Errors as
+ * fa2_forward_varlen plus FA2_ERR_WORKSPACE. */
+FA2_API fa2_status_t fa2_backward_varlen(const void* q, const void* k, const void* v, const void* o,
+                                         const float* lse, const void* dout, void* dq, void* dk, void* dv,
+                                         const int* cu_seqlens_q, const int* cu_seqlens_k,
+                                         void* workspace, size_t workspace_bytes, int B, int H, int H_kv,
+                                         int total_q, int total_k, int max_seqlen_q, int max_seqlen_k, int d,
+                                         int causal, float softmax_scale, int deterministic, fa2_dtype_t dtype,
+                                         void* stream);
 
 /* D = rowsum(dO o O) alone, into d_out [B,H,N] fp32 (device).  Exposed
  * so the preprocessing step can be checked on its own; fa2_backward runs it

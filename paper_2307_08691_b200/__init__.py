@@ -11,7 +11,8 @@ import ctypes
 import math
 import os
 
-__all__ = ["lib", "forward", "backward", "backward_preprocess", "backward_workspace_size",
+__all__ = ["lib", "forward", "backward", "forward_varlen", "backward_varlen", "backward_varlen_workspace_size",
+           "backward_preprocess", "backward_workspace_size",
            "attention_step_host", "step_arena_size", "kv_block_range", "set_timing_events", "FA2Error", "LIB_PATH"]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -47,6 +48,16 @@ def lib() -> ctypes.CDLL:
         L.fa2_backward_gqa.restype = i
         L.fa2_backward_deterministic.argtypes = L.fa2_backward_gqa.argtypes
         L.fa2_backward_deterministic.restype = i
+        L.fa2_forward_ex.argtypes = [vp, vp, vp, vp, vp, i, i, i, i, i, i, i, f, i, vp]
+        L.fa2_forward_ex.restype = i
+        L.fa2_forward_varlen.argtypes = [vp, vp, vp, vp, vp, vp, vp, i, i, i, i, i, i, i, i, i, f, i, vp]
+        L.fa2_forward_varlen.restype = i
+        L.fa2_backward_ex.argtypes = [vp] * 10 + [sz, i, i, i, i, i, i, i, f, i, i, vp]
+        L.fa2_backward_ex.restype = i
+        L.fa2_backward_varlen.argtypes = [vp] * 11 + [vp, sz, i, i, i, i, i, i, i, i, i, f, i, i, vp]
+        L.fa2_backward_varlen.restype = i
+        L.fa2_backward_varlen_workspace_size.argtypes = [i, i, i, i]
+        L.fa2_backward_varlen_workspace_size.restype = sz
         L.fa2_backward.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, i, i, i, i, i, f, i, vp]
         L.fa2_backward.restype = i
         L.fa2_backward_preprocess.argtypes = [vp, vp, vp, i, i, i, i, i, vp]
@@ -104,7 +115,7 @@ def _ptr(t):
 
 
 def _need(t, like, name, heads=None):
-    shape = tuple(like.shape) if heads is None else (like.shape[0], heads, like.shape[2], like.shape[3])
+    shape = tuple(like.shape) if heads is None else (like.shape[0], heads) + tuple(like.shape[2:])
     if tuple(t.shape) != shape or t.dtype != like.dtype or not t.is_contiguous() or t.device != like.device:
         raise FA2Error(1, f"{name} must be a contiguous {shape} {like.dtype} tensor on {like.device}")
 
@@ -116,21 +127,35 @@ def _kv_heads(q, k):
     return hkv
 
 
+def _kv_check(q, k, v):
+    """k, v: [B, H_kv, N_k, d] with H_kv | H; returns (H_kv, N_k)."""
+    Hkv = _kv_heads(q, k)
+    if k.dim() != 4 or k.shape[0] != q.shape[0] or k.shape[3] != q.shape[3]:
+        raise FA2Error(1, f"k must be [B, H_kv, N_k, d] matching q {tuple(q.shape)}")
+    _need(k, k, "k")
+    _need(v, k, "v")
+    return Hkv, k.shape[2]
+
+
 def forward(q, k, v, causal: bool = False, softmax_scale: float | None = None, out=None, lse=None, stream=None):
-    """O, L for [B,H,N,d] bf16/fp16 CUDA tensors (Alg. 1).  k, v may have
-    H_kv < H heads (MQA/GQA).  Returns (o, lse[B,H,N] fp32)."""
+    """O, L for [B,H,N_q,d] bf16/fp16 CUDA tensors (Alg. 1).  k, v are
+    [B,H_kv,N_k,d]: H_kv < H heads is MQA/GQA; N_k != N_q uses the
+    bottom-right causal alignment (fa2_forward_ex, R22).
+    Returns (o, lse[B,H,N_q] fp32)."""
     import torch
     B, H, N, d = _shape(q)
-    Hkv = _kv_heads(q, k)
-    for t, n in ((k, "k"), (v, "v")):
-        _need(t, q, n, Hkv)
+    Hkv, Nk = _kv_check(q, k, v)
     if not q.is_contiguous():
         raise FA2Error(1, "q must be contiguous")
     scale = 1.0 / math.sqrt(d) if softmax_scale is None else float(softmax_scale)
     o = torch.empty_like(q) if out is None else out
     L = torch.empty((B, H, N), dtype=torch.float32, device=q.device) if lse is None else lse
-    _check(lib().fa2_forward_gqa(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(L), B, H, Hkv, N, d, int(bool(causal)),
-                                 scale, _dtype_code(q), ctypes.c_void_p(_stream(stream))))
+    if Nk == N:
+        _check(lib().fa2_forward_gqa(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(L), B, H, Hkv, N, d, int(bool(causal)),
+                                     scale, _dtype_code(q), ctypes.c_void_p(_stream(stream))))
+    else:
+        _check(lib().fa2_forward_ex(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(L), B, H, Hkv, N, Nk, d,
+                                    int(bool(causal)), scale, _dtype_code(q), ctypes.c_void_p(_stream(stream))))
     return o, L
 
 
@@ -146,9 +171,7 @@ def backward(q, k, v, o, lse, do, causal: bool = False, softmax_scale: float | N
     Returns (dq, dk, dv)."""
     import torch
     B, H, N, d = _shape(q)
-    Hkv = _kv_heads(q, k)
-    for t, n in ((k, "k"), (v, "v")):
-        _need(t, q, n, Hkv)
+    Hkv, Nk = _kv_check(q, k, v)
     for t, n in ((o, "o"), (do, "do")):
         _need(t, q, n)
     scale = 1.0 / math.sqrt(d) if softmax_scale is None else float(softmax_scale)
@@ -158,10 +181,78 @@ def backward(q, k, v, o, lse, do, causal: bool = False, softmax_scale: float | N
     wsz = backward_workspace_size(B, H, N, d)
     if workspace is None:
         workspace = torch.empty(wsz, dtype=torch.uint8, device=q.device)
-    fn = lib().fa2_backward_deterministic if deterministic else lib().fa2_backward_gqa
-    _check(fn(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk),
-              _ptr(dv), _ptr(workspace), workspace.numel() * workspace.element_size(),
-              B, H, Hkv, N, d, int(bool(causal)), scale, _dtype_code(q), ctypes.c_void_p(_stream(stream))))
+    args = (_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(workspace),
+            workspace.numel() * workspace.element_size())
+    st = ctypes.c_void_p(_stream(stream))
+    if Nk == N:
+        fn = lib().fa2_backward_deterministic if deterministic else lib().fa2_backward_gqa
+        _check(fn(*args, B, H, Hkv, N, d, int(bool(causal)), scale, _dtype_code(q), st))
+    else:
+        _check(lib().fa2_backward_ex(*args, B, H, Hkv, N, Nk, d, int(bool(causal)), scale, int(bool(deterministic)),
+                                     _dtype_code(q), st))
+    return dq, dk, dv
+
+
+def _varlen_check(q, k, v, cu_q, cu_k):
+    import torch
+    if q.dim() != 3 or k.dim() != 3 or k.shape[2] != q.shape[2]:
+        raise FA2Error(1, "varlen tensors are packed [total, heads, d]")
+    Hkv = k.shape[1]
+    if Hkv < 1 or q.shape[1] % Hkv:
+        raise FA2Error(1, f"key/value heads ({Hkv}) must divide query heads ({q.shape[1]})")
+    _need(q, q, "q")
+    _need(k, k, "k")
+    _need(v, k, "v")
+    for c, n in ((cu_q, "cu_seqlens_q"), (cu_k, "cu_seqlens_k")):
+        if c.dtype != torch.int32 or c.dim() != 1 or not c.is_contiguous() or c.device != q.device:
+            raise FA2Error(1, f"{n} must be a contiguous int32 tensor on {q.device}")
+    if cu_q.numel() != cu_k.numel() or cu_q.numel() < 2:
+        raise FA2Error(1, "cu_seqlens_q and cu_seqlens_k must both have B+1 >= 2 entries")
+    return cu_q.numel() - 1, Hkv
+
+
+def forward_varlen(q, k, v, cu_seqlens_q, cu_seqlens_k, max_seqlen_q: int, max_seqlen_k: int, causal: bool = False,
+                   softmax_scale: float | None = None, out=None, lse=None, stream=None):
+    """Packed variable-length batch (fa2_forward_varlen): q [T_q,H,d], k/v
+    [T_k,H_kv,d], cu_seqlens_* int32 [B+1] on the device.  Returns (o [T_q,H,d],
+    lse [H,T_q] fp32)."""
+    import torch
+    B, Hkv = _varlen_check(q, k, v, cu_seqlens_q, cu_seqlens_k)
+    Tq, H, d = q.shape
+    scale = 1.0 / math.sqrt(d) if softmax_scale is None else float(softmax_scale)
+    o = torch.empty_like(q) if out is None else out
+    L = torch.empty((H, Tq), dtype=torch.float32, device=q.device) if lse is None else lse
+    _check(lib().fa2_forward_varlen(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(L), _ptr(cu_seqlens_q),
+                                    _ptr(cu_seqlens_k), B, H, Hkv, Tq, k.shape[0], int(max_seqlen_q),
+                                    int(max_seqlen_k), d, int(bool(causal)), scale, _dtype_code(q),
+                                    ctypes.c_void_p(_stream(stream))))
+    return o, L
+
+
+def backward_varlen_workspace_size(B: int, H: int, total_q: int, d: int) -> int:
+    return int(lib().fa2_backward_varlen_workspace_size(B, H, total_q, d))
+
+
+def backward_varlen(q, k, v, o, lse, do, cu_seqlens_q, cu_seqlens_k, max_seqlen_q: int, max_seqlen_k: int,
+                    causal: bool = False, softmax_scale: float | None = None, dq=None, dk=None, dv=None,
+                    workspace=None, stream=None, deterministic: bool = False):
+    """Backward of forward_varlen (fa2_backward_varlen).  Returns (dq, dk, dv)."""
+    import torch
+    B, Hkv = _varlen_check(q, k, v, cu_seqlens_q, cu_seqlens_k)
+    Tq, H, d = q.shape
+    for t, n in ((o, "o"), (do, "do")):
+        _need(t, q, n)
+    scale = 1.0 / math.sqrt(d) if softmax_scale is None else float(softmax_scale)
+    dq = torch.empty_like(q) if dq is None else dq
+    dk = torch.empty_like(k) if dk is None else dk
+    dv = torch.empty_like(v) if dv is None else dv
+    if workspace is None:
+        workspace = torch.empty(backward_varlen_workspace_size(B, H, Tq, d), dtype=torch.uint8, device=q.device)
+    _check(lib().fa2_backward_varlen(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk),
+                                     _ptr(dv), _ptr(cu_seqlens_q), _ptr(cu_seqlens_k), _ptr(workspace),
+                                     workspace.numel() * workspace.element_size(), B, H, Hkv, Tq, k.shape[0],
+                                     int(max_seqlen_q), int(max_seqlen_k), d, int(bool(causal)), scale,
+                                     int(bool(deterministic)), _dtype_code(q), ctypes.c_void_p(_stream(stream))))
     return dq, dk, dv
 
 

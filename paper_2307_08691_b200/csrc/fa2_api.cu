@@ -8,6 +8,7 @@
 #include <cstring>
 #include <string>
 #include <mutex>
+#include <algorithm>
 
 #include "../../include/fa2.h"
 #include "fa2_fwd_sm100.cuh"
@@ -113,6 +114,76 @@ fa2_status_t make_map_3d(CUtensorMap* m, const void* base, CUtensorMapDataType d
   return FA2_OK;
 }
 
+// Geometry of one call: fixed lengths ([B,H,N_q,d] / [B,H_kv,N_k,d]) or packed
+// variable-length ([T_q,H,d] / [T_k,H_kv,d] with device cu_seqlens).
+struct Geom {
+  int B = 0, H = 0, Hkv = 0, d = 0;
+  int Nq = 0, Nk = 0;                          // fixed lengths, or the packed maxima
+  bool packed = false;
+  const int* cu_q = nullptr;
+  const int* cu_k = nullptr;
+  int Tq = 0, Tk = 0;                          // packed totals
+};
+
+Geom fixed_geom(int B, int H, int Hkv, int Nq, int Nk, int d) {
+  Geom g;
+  g.B = B; g.H = H; g.Hkv = Hkv; g.d = d; g.Nq = Nq; g.Nk = Nk;
+  return g;
+}
+
+// 3-D row-tile map in memory order (fa2_seq.cuh): fixed {d, N, B*heads}, packed
+// {d, heads, T}; box = 64 columns x 128 rows of one head.
+fa2_status_t make_rows_map(CUtensorMap* m, const void* base, CUtensorMapDataType dt, const Geom& g, int heads,
+                           bool is_q) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(FA2_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  const cuuint64_t d = static_cast<cuuint64_t>(g.d), eb = 2;
+  cuuint64_t dims[3], strides[2];
+  cuuint32_t box[3];
+  if (!g.packed) {
+    const cuuint64_t n = static_cast<cuuint64_t>(is_q ? g.Nq : g.Nk);
+    dims[0] = d; dims[1] = n; dims[2] = static_cast<cuuint64_t>(heads) * static_cast<cuuint64_t>(g.B);
+    strides[0] = d * eb; strides[1] = n * d * eb;
+    box[0] = 64; box[1] = 128; box[2] = 1;
+  } else {
+    const cuuint64_t t = static_cast<cuuint64_t>(std::max(1, is_q ? g.Tq : g.Tk));
+    dims[0] = d; dims[1] = static_cast<cuuint64_t>(heads); dims[2] = t;
+    strides[0] = d * eb; strides[1] = static_cast<cuuint64_t>(heads) * d * eb;
+    box[0] = 64; box[1] = 1; box[2] = 128;
+  }
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(FA2_ERR_CUDA, "cuTensorMapEncodeTiled (rows) failed (%d)", static_cast<int>(r));
+  return FA2_OK;
+}
+
+// Validation shared by the packed variable-length entry points.
+fa2_status_t varlen_geom(const int* cu_q, const int* cu_k, int B, int H, int Hkv, int total_q, int total_k, int max_q,
+                         int max_k, int d, float scale, fa2_dtype_t dtype, Geom& g) {
+  fa2_status_t s = check_common(B, H, 1, d, scale, dtype, true);
+  if (s != FA2_OK) return s;
+  if (Hkv < 1 || H % Hkv != 0) return fail(FA2_ERR_INVALID_ARG, "H=%d must be a positive multiple of H_kv=%d", H, Hkv);
+  if (total_q < 1 || total_k < 1) return fail(FA2_ERR_INVALID_ARG, "total_q, total_k must be >= 1 (got %d, %d)", total_q, total_k);
+  if (max_q < 1 || max_k < 1 || max_q > total_q || max_k > total_k)
+    return fail(FA2_ERR_INVALID_ARG, "max_seqlen_q/k must be in [1, total] (got %d, %d)", max_q, max_k);
+  if (cu_q == nullptr || cu_k == nullptr || (reinterpret_cast<uintptr_t>(cu_q) & 3u) || (reinterpret_cast<uintptr_t>(cu_k) & 3u))
+    return fail(FA2_ERR_INVALID_ARG, "cu_seqlens_q / cu_seqlens_k must be non-NULL, 4-byte aligned int32 arrays");
+  g.B = B; g.H = H; g.Hkv = Hkv; g.d = d;
+  g.Nq = max_q; g.Nk = max_k;
+  g.packed = true; g.cu_q = cu_q; g.cu_k = cu_k; g.Tq = total_q; g.Tk = total_k;
+  return FA2_OK;
+}
+
+fa2::SeqGeom seq_geom(const Geom& g) {
+  fa2::SeqGeom s;
+  s.cu_q = g.packed ? g.cu_q : nullptr;
+  s.cu_k = g.packed ? g.cu_k : nullptr;
+  s.Nq = g.Nq;
+  s.Nk = g.Nk;
+  return s;
+}
+
 CUtensorMapDataType tma_dtype(fa2_dtype_t dt) {
   return dt == FA2_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
 }
@@ -126,10 +197,10 @@ fa2_status_t set_smem(K kernel, int bytes) {
 // ----------------------------------------------------------------------------
 // Forward
 // ----------------------------------------------------------------------------
-template <int D, bool BF16, bool CAUSAL>
+template <int D, bool BF16, bool CAUSAL, bool GEN>
 fa2_status_t launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const fa2::FwdParams& p,
                         int sms, cudaStream_t st) {
-  auto kern = fa2::fa2_fwd_kernel<D, BF16, CAUSAL>;
+  auto kern = fa2::fa2_fwd_kernel<D, BF16, CAUSAL, GEN>;
   constexpr int smem = fa2::FwdSmem<D>::ALLOC;
   fa2_status_t s = set_smem(kern, smem);
   if (s != FA2_OK) return s;
@@ -144,32 +215,44 @@ fa2_status_t launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUte
 template <int D, bool BF16>
 fa2_status_t dispatch_fwd_causal(bool causal, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                                  const fa2::FwdParams& p, int sms, cudaStream_t st) {
-  return causal ? launch_fwd<D, BF16, true>(mq, mk, mv, p, sms, st) : launch_fwd<D, BF16, false>(mq, mk, mv, p, sms, st);
+  // general geometry (packed varlen or N_q != N_k) vs the square fixed-length path
+  if (p.geom.cu_q != nullptr || p.geom.Nq != p.geom.Nk)
+    return causal ? launch_fwd<D, BF16, true, true>(mq, mk, mv, p, sms, st)
+                  : launch_fwd<D, BF16, false, true>(mq, mk, mv, p, sms, st);
+  return causal ? launch_fwd<D, BF16, true, false>(mq, mk, mv, p, sms, st)
+                : launch_fwd<D, BF16, false, false>(mq, mk, mv, p, sms, st);
 }
 
-fa2_status_t forward_impl(const void* q, const void* k, const void* v, void* o, float* lse, int B, int H, int Hkv,
-                          int N, int d, int causal, float scale, fa2_dtype_t dtype, cudaStream_t st, int sms) {
-  const int BH = B * H;
+fa2_status_t forward_impl(const void* q, const void* k, const void* v, void* o, float* lse, const Geom& g,
+                          int causal, float scale, fa2_dtype_t dtype, cudaStream_t st, int sms) {
   CUtensorMap mq, mk, mv;
   const CUtensorMapDataType dt = tma_dtype(dtype);
   fa2_status_t s;
-  if ((s = make_map_3d(&mq, q, dt, 2, d, N, BH, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
-  if ((s = make_map_3d(&mk, k, dt, 2, d, N, B * Hkv, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
-  if ((s = make_map_3d(&mv, v, dt, 2, d, N, B * Hkv, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
+  if ((s = make_rows_map(&mq, q, dt, g, g.H, true)) != FA2_OK) return s;
+  if ((s = make_rows_map(&mk, k, dt, g, g.Hkv, false)) != FA2_OK) return s;
+  if ((s = make_rows_map(&mv, v, dt, g, g.Hkv, false)) != FA2_OK) return s;
   fa2::FwdParams p;
   p.o = o;
   p.lse = lse;
-  p.BH = BH;
-  p.H = H;
-  p.Hkv = Hkv;
-  p.group = H / Hkv;
-  p.N = N;
-  p.num_m_blocks = (N + 255) / 256;
-  p.num_tiles = BH * p.num_m_blocks;
+  p.BH = g.B * g.H;
+  p.H = g.H;
+  p.Hkv = g.Hkv;
+  p.group = g.H / g.Hkv;
+  p.geom = seq_geom(g);
+  const long long d = g.d;
+  if (!g.packed) {
+    p.o_rs = d; p.o_hs = static_cast<long long>(g.Nq) * d; p.o_bs = p.o_hs * g.H;
+    p.l_hs = g.Nq; p.l_bs = static_cast<long long>(g.Nq) * g.H;
+  } else {
+    p.o_rs = d * g.H; p.o_hs = d; p.o_bs = 0;
+    p.l_hs = g.Tq; p.l_bs = 0;
+  }
+  p.num_m_blocks = (g.Nq + 255) / 256;
+  p.num_tiles = p.BH * p.num_m_blocks;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.trace = g_trace;
   const bool bf16 = dtype == FA2_BF16;
-  if (d == 64)
+  if (g.d == 64)
     s = bf16 ? dispatch_fwd_causal<64, true>(causal, mq, mk, mv, p, sms, st)
              : dispatch_fwd_causal<64, false>(causal, mq, mk, mv, p, sms, st);
   else
@@ -181,29 +264,94 @@ fa2_status_t forward_impl(const void* q, const void* k, const void* v, void* o, 
 // ----------------------------------------------------------------------------
 // Backward
 // ----------------------------------------------------------------------------
-size_t pad128(int N) { return static_cast<size_t>((N + 127) / 128) * 128; }
+size_t pad128(long long N) { return static_cast<size_t>((N + 127) / 128) * 128; }
+size_t round16(size_t b) { return (b + 15) / 16 * 16; }
 
-size_t ws_dq_bytes(int B, int H, int N, int d) { return static_cast<size_t>(B) * H * pad128(N) * d * 4; }
-// D and L*log2(e), each [B,H,N_pad] fp32
-size_t ws_d_bytes(int B, int H, int N) { return 2 * static_cast<size_t>(B) * H * pad128(N) * 4; }
-// deterministic-mode dQ tile counters, [B,H,N_pad/128] int32 (16-byte rounded)
-size_t ws_sem_bytes(int B, int H, int N) { return (static_cast<size_t>(B) * H * (pad128(N) / 128) * 4 + 15) / 16 * 16; }
+// Backward workspace (both layouts), in this order:
+//   dq_acc [rows, d] fp32 | D [rows] fp32 | L*log2e [rows] fp32 | counters [rows/128] int32 |
+//   tile_off [B+1] int32 (packed only)
+// rows = padded query rows: fixed B*H*N_pad; packed H * pad128(T_q + 127 B) (every sequence is
+// padded to whole 128-row tiles, fa2_bwd_sm100.cuh RowParams).
+struct WsLayout {
+  long long rows = 0, rows_per_head = 0;
+  size_t dq = 0, dvec = 0, lse2 = 0, sem = 0, tile = 0, total = 0;
+};
+WsLayout ws_layout(const Geom& g) {
+  WsLayout w;
+  if (!g.packed) {
+    w.rows_per_head = static_cast<long long>(pad128(g.Nq));
+    w.rows = static_cast<long long>(g.B) * g.H * w.rows_per_head;
+  } else {
+    w.rows_per_head = static_cast<long long>(pad128(static_cast<long long>(g.Tq) + 127LL * g.B));
+    w.rows = static_cast<long long>(g.H) * w.rows_per_head;
+  }
+  w.dq = 0;
+  w.dvec = w.dq + static_cast<size_t>(w.rows) * g.d * 4;
+  w.lse2 = w.dvec + static_cast<size_t>(w.rows) * 4;
+  w.sem = w.lse2 + static_cast<size_t>(w.rows) * 4;
+  w.tile = w.sem + round16(static_cast<size_t>(w.rows / 128) * 4);
+  w.total = w.tile + (g.packed ? round16(static_cast<size_t>(g.B + 1) * 4) : 0);
+  return w;
+}
 
-fa2_status_t preprocess_impl(const void* o, const void* dout, const float* lse, float* dvec, float* lse2,
-                             float* dq_acc, int BH, int N, int npad, int d, fa2_dtype_t dtype, cudaStream_t st,
-                             int* dq_sem = nullptr) {
-  // one warp per row of the padded [BH, npad] grid; 8 rows per 256-thread block
-  const long long rows = static_cast<long long>(BH) * npad;
-  const int grid = static_cast<int>((rows + 7) / 8);
+fa2::RowParams row_params(const Geom& g, const WsLayout& w, const void* o, const void* dout, void* dq,
+                          const float* lse, void* ws) {
+  fa2::RowParams r;
+  uint8_t* base = reinterpret_cast<uint8_t*>(ws);
+  r.o = o;
+  r.dout = dout;
+  r.dq = dq;
+  r.lse = lse;
+  r.dq_acc = reinterpret_cast<float*>(base + w.dq);
+  r.dvec = reinterpret_cast<float*>(base + w.dvec);
+  r.lse2 = reinterpret_cast<float*>(base + w.lse2);
+  r.dq_sem = nullptr;
+  r.B = g.B;
+  r.H = g.H;
+  r.Nq = g.Nq;
+  r.cu_q = g.packed ? g.cu_q : nullptr;
+  r.tile_off = g.packed ? reinterpret_cast<const int*>(base + w.tile) : nullptr;
+  r.acc_hs = w.rows_per_head;
+  r.acc_rows = w.rows;
+  const long long d = g.d;
+  if (!g.packed) {
+    r.o_rs = d; r.o_hs = static_cast<long long>(g.Nq) * d; r.o_bs = r.o_hs * g.H;
+    r.l_hs = g.Nq; r.l_bs = static_cast<long long>(g.Nq) * g.H;
+  } else {
+    r.o_rs = d * g.H; r.o_hs = d; r.o_bs = 0;
+    r.l_hs = g.Tq; r.l_bs = 0;
+  }
+  return r;
+}
+
+fa2_status_t preprocess_impl(const fa2::RowParams& rp, int d, fa2_dtype_t dtype, cudaStream_t st) {
+  // one warp per padded workspace row; 8 rows per 256-thread block (32-bit row arithmetic in the kernels)
+  if (rp.acc_rows >= (1LL << 31)) return fail(FA2_ERR_INVALID_ARG, "problem too large: %lld padded query rows", rp.acc_rows);
+  const long long grid = (rp.acc_rows + 7) / 8;
   const bool bf16 = dtype == FA2_BF16;
   if (d == 64) {
-    if (bf16) fa2::fa2_bwd_preprocess<64, true><<<grid, 256, 0, st>>>(o, dout, dvec, dq_acc, BH, N, npad, lse, lse2, dq_sem);
-    else fa2::fa2_bwd_preprocess<64, false><<<grid, 256, 0, st>>>(o, dout, dvec, dq_acc, BH, N, npad, lse, lse2, dq_sem);
+    if (bf16) fa2::fa2_bwd_preprocess<64, true><<<static_cast<int>(grid), 256, 0, st>>>(rp);
+    else fa2::fa2_bwd_preprocess<64, false><<<static_cast<int>(grid), 256, 0, st>>>(rp);
   } else {
-    if (bf16) fa2::fa2_bwd_preprocess<128, true><<<grid, 256, 0, st>>>(o, dout, dvec, dq_acc, BH, N, npad, lse, lse2, dq_sem);
-    else fa2::fa2_bwd_preprocess<128, false><<<grid, 256, 0, st>>>(o, dout, dvec, dq_acc, BH, N, npad, lse, lse2, dq_sem);
+    if (bf16) fa2::fa2_bwd_preprocess<128, true><<<static_cast<int>(grid), 256, 0, st>>>(rp);
+    else fa2::fa2_bwd_preprocess<128, false><<<static_cast<int>(grid), 256, 0, st>>>(rp);
   }
   FA2_CUDA(cudaGetLastError());
+  return FA2_OK;
+}
+
+// 2-D fp32 view {d, rows} of dq_acc with box {32, 128} (d = 64 kernel's tensor reduce-adds).
+fa2_status_t make_acc_map(CUtensorMap* m, float* dq_acc, int d, long long rows) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(FA2_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(d) * 4};
+  cuuint32_t box[2] = {32, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dq_acc, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(FA2_ERR_CUDA, "cuTensorMapEncodeTiled (dq_acc) failed (%d)", static_cast<int>(r));
   return FA2_OK;
 }
 
@@ -222,78 +370,92 @@ fa2_status_t launch_bwd_kernel(Kern kern, int smem, const fa2::BwdMaps& maps, co
   return FA2_OK;
 }
 
-template <int D, bool BF16, bool CAUSAL>
+template <int D, bool BF16, bool CAUSAL, bool GEN>
 fa2_status_t launch_bwd(const fa2::BwdMaps& maps, const fa2::BwdParams& p, int sms, cudaStream_t st) {
   // d = 128: fa2_bwd128_sm100.cuh; d = 64: fa2_bwd_kernel
   if constexpr (D == 128)
-    return launch_bwd_kernel(fa2::fa2_bwd128_kernel<BF16, CAUSAL>, fa2::Bwd128Smem::ALLOC, maps, p, sms, st);
+    return launch_bwd_kernel(fa2::fa2_bwd128_kernel<BF16, CAUSAL, GEN>, fa2::Bwd128Smem::ALLOC, maps, p, sms, st);
   else
-    return launch_bwd_kernel(fa2::fa2_bwd_kernel<D, BF16, CAUSAL>, fa2::BwdSmem<D>::ALLOC, maps, p, sms, st);
+    return launch_bwd_kernel(fa2::fa2_bwd_kernel<D, BF16, CAUSAL, GEN>, fa2::BwdSmem<D>::ALLOC, maps, p, sms, st);
 }
 
 template <int D, bool BF16>
 fa2_status_t dispatch_bwd_causal(bool causal, const fa2::BwdMaps& maps, const fa2::BwdParams& p, int sms,
                                  cudaStream_t st) {
-  return causal ? launch_bwd<D, BF16, true>(maps, p, sms, st) : launch_bwd<D, BF16, false>(maps, p, sms, st);
+  if (p.geom.cu_q != nullptr || p.geom.Nq != p.geom.Nk)   // general geometry
+    return causal ? launch_bwd<D, BF16, true, true>(maps, p, sms, st) : launch_bwd<D, BF16, false, true>(maps, p, sms, st);
+  return causal ? launch_bwd<D, BF16, true, false>(maps, p, sms, st) : launch_bwd<D, BF16, false, false>(maps, p, sms, st);
 }
 
 fa2_status_t backward_impl(const void* q, const void* k, const void* v, const void* o, const float* lse,
-                           const void* dout, void* dq, void* dk, void* dv, void* ws, int B, int H, int Hkv, int N,
-                           int d, int causal, float scale, fa2_dtype_t dtype, cudaStream_t st, int sms,
-                           bool deterministic = false) {
-  const int BH = B * H;
-  const size_t npad = pad128(N);
-  float* dq_acc = reinterpret_cast<float*>(ws);
-  float* dvec = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + ws_dq_bytes(B, H, N, d));
-  float* lse2 = dvec + static_cast<size_t>(BH) * npad;
-  int* dq_sem = deterministic ? reinterpret_cast<int*>(lse2 + static_cast<size_t>(BH) * npad) : nullptr;
+                           const void* dout, void* dq, void* dk, void* dv, void* ws, const Geom& g, int causal,
+                           float scale, fa2_dtype_t dtype, cudaStream_t st, int sms, bool deterministic) {
+  const WsLayout wl = ws_layout(g);
+  fa2::RowParams rp = row_params(g, wl, o, dout, dq, lse, ws);
+  int* dq_sem = deterministic ? reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + wl.sem) : nullptr;
+  rp.dq_sem = dq_sem;
   mark(2, st);
-  fa2_status_t s = preprocess_impl(o, dout, lse, dvec, lse2, dq_acc, BH, N, static_cast<int>(npad), d, dtype, st, dq_sem);
+  if (g.packed) {
+    fa2::fa2_tile_prefix<<<1, 1024, 0, st>>>(g.cu_q, g.B, const_cast<int*>(rp.tile_off));
+    FA2_CUDA(cudaGetLastError());
+  }
+  fa2_status_t s = preprocess_impl(rp, g.d, dtype, st);
   if (s != FA2_OK) return s;
   fa2::BwdMaps maps;
   const CUtensorMapDataType dt = tma_dtype(dtype);
-  const int bm = 128;   // query rows per backward tile (both kernels)
-  if ((s = make_map_3d(&maps.q, q, dt, 2, d, N, BH, 64, bm, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
-  if ((s = make_map_3d(&maps.dout, dout, dt, 2, d, N, BH, 64, bm, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
-  if ((s = make_map_3d(&maps.k, k, dt, 2, d, N, B * Hkv, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
-  if ((s = make_map_3d(&maps.v, v, dt, 2, d, N, B * Hkv, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK) return s;
-  // fp32 dQ accumulator [BH, npad, d]; reduce-add boxes of 32 columns x BM rows (128-B swizzle rows;
-  // the d=128 kernel uses contiguous 1D bulk reductions instead)
-  if ((s = make_map_3d(&maps.dq_acc, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, d, static_cast<int>(npad), BH, 32,
-                       bm, CU_TENSOR_MAP_SWIZZLE_128B)) != FA2_OK)
-    return s;
+  if ((s = make_rows_map(&maps.q, q, dt, g, g.H, true)) != FA2_OK) return s;
+  if ((s = make_rows_map(&maps.dout, dout, dt, g, g.H, true)) != FA2_OK) return s;
+  if ((s = make_rows_map(&maps.k, k, dt, g, g.Hkv, false)) != FA2_OK) return s;
+  if ((s = make_rows_map(&maps.v, v, dt, g, g.Hkv, false)) != FA2_OK) return s;
+  if ((s = make_acc_map(&maps.dq_acc, rp.dq_acc, g.d, wl.rows)) != FA2_OK) return s;
   fa2::BwdParams p;
   p.lse = lse;
-  p.dvec = dvec;
+  p.dvec = rp.dvec;
   p.dk = dk;
   p.dv = dv;
-  p.dq_acc = dq_acc;
-  p.BH = BH;
-  p.H = H;
-  p.Hkv = Hkv;
-  p.group = H / Hkv;
-  p.N = N;
-  p.npad = static_cast<int>(npad);
-  p.num_n_blocks = (N + 127) / 128;
-  p.num_tiles = B * Hkv * p.num_n_blocks;   // one work tile per (key/value head, key block)
+  p.dq_acc = rp.dq_acc;
+  p.BH = g.B * g.H;
+  p.H = g.H;
+  p.Hkv = g.Hkv;
+  p.group = g.H / g.Hkv;
+  p.num_n_blocks = (g.Nk + 127) / 128;
+  p.num_tiles = g.B * g.Hkv * p.num_n_blocks;   // one work tile per (sequence, key/value head, key block)
   p.scale = scale;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.trace = g_trace;
   p.dq_sem = dq_sem;
-  p.det_cyclic = p.num_n_blocks <= sms ? 1 : 0;
+  // the cyclic deterministic schedule needs one square query/key tile grid per head
+  p.det_cyclic = (!g.packed && g.Nq == g.Nk && p.num_n_blocks <= sms) ? 1 : 0;
+  p.geom = seq_geom(g);
+  const long long d = g.d;
+  if (!g.packed) {
+    p.k_rs = d; p.k_hs = static_cast<long long>(g.Nk) * d; p.k_bs = p.k_hs * g.Hkv;
+    p.acc_hs = wl.rows_per_head; p.acc_bs = wl.rows_per_head * g.H;
+  } else {
+    p.k_rs = d * g.Hkv; p.k_hs = d; p.k_bs = 0;
+    p.acc_hs = wl.rows_per_head; p.acc_bs = 0;
+  }
+  p.acc_rows = wl.rows;
+  p.tile_off = rp.tile_off;
   const bool bf16 = dtype == FA2_BF16;
-  if (d == 64)
+  if (g.d == 64)
     s = bf16 ? dispatch_bwd_causal<64, true>(causal, maps, p, sms, st) : dispatch_bwd_causal<64, false>(causal, maps, p, sms, st);
   else
     s = bf16 ? dispatch_bwd_causal<128, true>(causal, maps, p, sms, st)
              : dispatch_bwd_causal<128, false>(causal, maps, p, sms, st);
   if (s != FA2_OK) return s;
-  // dQ = cast(dq_acc) (the softmax scale is already applied to dS), rows < N only
+  // dQ = cast(dq_acc) (the softmax scale is already applied to dS), real rows only
   {
-    const long long elems = static_cast<long long>(BH) * N * d;
-    const int grid = static_cast<int>((elems / 8 + 255) / 256);
-    if (bf16) fa2::fa2_dq_convert<true><<<grid, 256, 0, st>>>(dq_acc, dq, BH, N, static_cast<int>(npad), d);
-    else fa2::fa2_dq_convert<false><<<grid, 256, 0, st>>>(dq_acc, dq, BH, N, static_cast<int>(npad), d);
+    const long long rows_out = g.packed ? static_cast<long long>(g.Tq) * g.H : static_cast<long long>(g.B) * g.H * g.Nq;
+    if (rows_out >= (1LL << 31)) return fail(FA2_ERR_INVALID_ARG, "problem too large: %lld query rows", rows_out);
+    const long long grid = (rows_out * (g.d / 8) + 255) / 256;
+    if (g.d == 64) {
+      if (bf16) fa2::fa2_dq_convert<64, true><<<static_cast<int>(grid), 256, 0, st>>>(rp, rows_out);
+      else fa2::fa2_dq_convert<64, false><<<static_cast<int>(grid), 256, 0, st>>>(rp, rows_out);
+    } else {
+      if (bf16) fa2::fa2_dq_convert<128, true><<<static_cast<int>(grid), 256, 0, st>>>(rp, rows_out);
+      else fa2::fa2_dq_convert<128, false><<<static_cast<int>(grid), 256, 0, st>>>(rp, rows_out);
+    }
     FA2_CUDA(cudaGetLastError());
     mark(5, st);
   }
@@ -302,8 +464,8 @@ fa2_status_t backward_impl(const void* q, const void* k, const void* v, const vo
 
 fa2_status_t backward_entry(const void* q, const void* k, const void* v, const void* o, const float* lse,
                             const void* dout, void* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes,
-                            int B, int H, int H_kv, int N, int d, int causal, float softmax_scale, fa2_dtype_t dtype,
-                            void* stream, bool deterministic);
+                            const Geom& g, float softmax_scale, fa2_dtype_t dtype, void* stream, int causal,
+                            bool deterministic);
 
 }  // namespace
 
@@ -355,8 +517,42 @@ fa2_status_t fa2_forward_gqa(const void* q, const void* k, const void* v, void* 
   if ((s = check_ptrs({q, k, v, o, lse})) != FA2_OK) return s;
   DeviceInfo di;
   if ((s = device_info(di)) != FA2_OK) return s;
-  s = forward_impl(q, k, v, o, lse, B, H, H_kv, N, d, causal, softmax_scale, dtype, static_cast<cudaStream_t>(stream),
-                   di.sms);
+  s = forward_impl(q, k, v, o, lse, fixed_geom(B, H, H_kv, N, N, d), causal, softmax_scale, dtype,
+                   static_cast<cudaStream_t>(stream), di.sms);
+  if (s == FA2_OK) g_launches = 1;
+  return s;
+}
+
+fa2_status_t fa2_forward_ex(const void* q, const void* k, const void* v, void* o, float* lse, int B, int H, int H_kv,
+                            int N_q, int N_k, int d, int causal, float softmax_scale, fa2_dtype_t dtype, void* stream) {
+  g_detail.clear();
+  fa2_status_t s = check_common(B, H, N_q, d, softmax_scale, dtype, true);
+  if (s != FA2_OK) return s;
+  if (N_k < 1) return fail(FA2_ERR_INVALID_ARG, "N_k must be >= 1 (got %d)", N_k);
+  if (H_kv < 1 || H % H_kv != 0) return fail(FA2_ERR_INVALID_ARG, "H=%d must be a positive multiple of H_kv=%d", H, H_kv);
+  if ((s = check_ptrs({q, k, v, o, lse})) != FA2_OK) return s;
+  DeviceInfo di;
+  if ((s = device_info(di)) != FA2_OK) return s;
+  s = forward_impl(q, k, v, o, lse, fixed_geom(B, H, H_kv, N_q, N_k, d), causal, softmax_scale, dtype,
+                   static_cast<cudaStream_t>(stream), di.sms);
+  if (s == FA2_OK) g_launches = 1;
+  return s;
+}
+
+fa2_status_t fa2_forward_varlen(const void* q, const void* k, const void* v, void* o, float* lse,
+                                const int* cu_seqlens_q, const int* cu_seqlens_k, int B, int H, int H_kv,
+                                int total_q, int total_k, int max_seqlen_q, int max_seqlen_k, int d, int causal,
+                                float softmax_scale, fa2_dtype_t dtype, void* stream) {
+  g_detail.clear();
+  fa2_status_t s;
+  Geom g;
+  if ((s = varlen_geom(cu_seqlens_q, cu_seqlens_k, B, H, H_kv, total_q, total_k, max_seqlen_q, max_seqlen_k, d,
+                       softmax_scale, dtype, g)) != FA2_OK)
+    return s;
+  if ((s = check_ptrs({q, k, v, o, lse})) != FA2_OK) return s;
+  DeviceInfo di;
+  if ((s = device_info(di)) != FA2_OK) return s;
+  s = forward_impl(q, k, v, o, lse, g, causal, softmax_scale, dtype, static_cast<cudaStream_t>(stream), di.sms);
   if (s == FA2_OK) g_launches = 1;
   return s;
 }
@@ -368,7 +564,7 @@ fa2_status_t fa2_forward(const void* q, const void* k, const void* v, void* o, f
 
 size_t fa2_backward_workspace_size(int B, int H, int N, int d) {
   if (B < 1 || H < 1 || N < 1 || (d != 64 && d != 128)) return 0;
-  return ws_dq_bytes(B, H, N, d) + ws_d_bytes(B, H, N) + ws_sem_bytes(B, H, N);
+  return ws_layout(fixed_geom(B, H, H, N, N, d)).total;
 }
 
 fa2_status_t fa2_backward(const void* q, const void* k, const void* v, const void* o, const float* lse,
@@ -383,16 +579,49 @@ fa2_status_t fa2_backward_gqa(const void* q, const void* k, const void* v, const
                               const void* dout, void* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes,
                               int B, int H, int H_kv, int N, int d, int causal, float softmax_scale, fa2_dtype_t dtype,
                               void* stream) {
-  return backward_entry(q, k, v, o, lse, dout, dq, dk, dv, workspace, workspace_bytes, B, H, H_kv, N, d, causal,
-                        softmax_scale, dtype, stream, false);
+  return backward_entry(q, k, v, o, lse, dout, dq, dk, dv, workspace, workspace_bytes, fixed_geom(B, H, H_kv, N, N, d),
+                        softmax_scale, dtype, stream, causal, false);
 }
 
 fa2_status_t fa2_backward_deterministic(const void* q, const void* k, const void* v, const void* o, const float* lse,
                                         const void* dout, void* dq, void* dk, void* dv, void* workspace,
                                         size_t workspace_bytes, int B, int H, int H_kv, int N, int d, int causal,
                                         float softmax_scale, fa2_dtype_t dtype, void* stream) {
-  return backward_entry(q, k, v, o, lse, dout, dq, dk, dv, workspace, workspace_bytes, B, H, H_kv, N, d, causal,
-                        softmax_scale, dtype, stream, true);
+  return backward_entry(q, k, v, o, lse, dout, dq, dk, dv, workspace, workspace_bytes, fixed_geom(B, H, H_kv, N, N, d),
+                        softmax_scale, dtype, stream, causal, true);
+}
+
+fa2_status_t fa2_backward_ex(const void* q, const void* k, const void* v, const void* o, const float* lse,
+                             const void* dout, void* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes,
+                             int B, int H, int H_kv, int N_q, int N_k, int d, int causal, float softmax_scale,
+                             int deterministic, fa2_dtype_t dtype, void* stream) {
+  if (N_k < 1) {
+    g_detail.clear();
+    return fail(FA2_ERR_INVALID_ARG, "N_k must be >= 1 (got %d)", N_k);
+  }
+  return backward_entry(q, k, v, o, lse, dout, dq, dk, dv, workspace, workspace_bytes,
+                        fixed_geom(B, H, H_kv, N_q, N_k, d), softmax_scale, dtype, stream, causal, deterministic != 0);
+}
+
+size_t fa2_backward_varlen_workspace_size(int B, int H, int total_q, int d) {
+  if (B < 1 || H < 1 || total_q < 1 || (d != 64 && d != 128)) return 0;
+  Geom g;
+  g.B = B; g.H = H; g.Hkv = H; g.d = d; g.packed = true; g.Tq = total_q;
+  return ws_layout(g).total;
+}
+
+fa2_status_t fa2_backward_varlen(const void* q, const void* k, const void* v, const void* o, const float* lse,
+                                 const void* dout, void* dq, void* dk, void* dv, const int* cu_seqlens_q,
+                                 const int* cu_seqlens_k, void* workspace, size_t workspace_bytes, int B, int H,
+                                 int H_kv, int total_q, int total_k, int max_seqlen_q, int max_seqlen_k, int d,
+                                 int causal, float softmax_scale, int deterministic, fa2_dtype_t dtype, void* stream) {
+  g_detail.clear();
+  Geom g;
+  fa2_status_t s = varlen_geom(cu_seqlens_q, cu_seqlens_k, B, H, H_kv, total_q, total_k, max_seqlen_q, max_seqlen_k,
+                               d, softmax_scale, dtype, g);
+  if (s != FA2_OK) return s;
+  return backward_entry(q, k, v, o, lse, dout, dq, dk, dv, workspace, workspace_bytes, g, softmax_scale, dtype, stream,
+                        causal, deterministic != 0);
 }
 
 }  // extern "C"
@@ -400,23 +629,23 @@ fa2_status_t fa2_backward_deterministic(const void* q, const void* k, const void
 namespace {
 fa2_status_t backward_entry(const void* q, const void* k, const void* v, const void* o, const float* lse,
                             const void* dout, void* dq, void* dk, void* dv, void* workspace, size_t workspace_bytes,
-                            int B, int H, int H_kv, int N, int d, int causal, float softmax_scale, fa2_dtype_t dtype,
-                            void* stream, bool deterministic) {
+                            const Geom& g, float softmax_scale, fa2_dtype_t dtype, void* stream, int causal,
+                            bool deterministic) {
   g_detail.clear();
-  fa2_status_t s = check_common(B, H, N, d, softmax_scale, dtype, true);
+  fa2_status_t s = check_common(g.B, g.H, g.packed ? 1 : g.Nq, g.d, softmax_scale, dtype, true);
   if (s != FA2_OK) return s;
-  if (H_kv < 1 || H % H_kv != 0) return fail(FA2_ERR_INVALID_ARG, "H=%d must be a positive multiple of H_kv=%d", H, H_kv);
+  if (g.Hkv < 1 || g.H % g.Hkv != 0)
+    return fail(FA2_ERR_INVALID_ARG, "H=%d must be a positive multiple of H_kv=%d", g.H, g.Hkv);
   if ((s = check_ptrs({q, k, v, o, lse, dout, dq, dk, dv})) != FA2_OK) return s;
   if (workspace == nullptr || !aligned16(workspace))
     return fail(FA2_ERR_WORKSPACE, "workspace is NULL or not 16-byte aligned");
-  if (workspace_bytes < fa2_backward_workspace_size(B, H, N, d))
-    return fail(FA2_ERR_WORKSPACE, "workspace too small: %zu < %zu", workspace_bytes,
-                fa2_backward_workspace_size(B, H, N, d));
+  const size_t need = ws_layout(g).total;
+  if (workspace_bytes < need) return fail(FA2_ERR_WORKSPACE, "workspace too small: %zu < %zu", workspace_bytes, need);
   DeviceInfo di;
   if ((s = device_info(di)) != FA2_OK) return s;
-  s = backward_impl(q, k, v, o, lse, dout, dq, dk, dv, workspace, B, H, H_kv, N, d, causal, softmax_scale, dtype,
+  s = backward_impl(q, k, v, o, lse, dout, dq, dk, dv, workspace, g, causal, softmax_scale, dtype,
                     static_cast<cudaStream_t>(stream), di.sms, deterministic);
-  if (s == FA2_OK) g_launches = 3;
+  if (s == FA2_OK) g_launches = g.packed ? 4 : 3;
   return s;
 }
 }  // namespace
@@ -431,19 +660,20 @@ fa2_status_t fa2_backward_preprocess(const void* o, const void* dout, float* d_o
   if ((s = check_ptrs({o, dout, d_out})) != FA2_OK) return s;
   DeviceInfo di;
   if ((s = device_info(di)) != FA2_OK) return s;
-  // d_out has N entries per head (no padding); write D via a padded-stride-free variant: npad == N here.
-  const int BH = B * H;
-  const long long rows = static_cast<long long>(BH) * N;
-  const int grid = static_cast<int>((rows + 7) / 8);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const bool bf16 = dtype == FA2_BF16;
-  if (d == 64) {
-    if (bf16) fa2::fa2_bwd_preprocess<64, true><<<grid, 256, 0, st>>>(o, dout, d_out, nullptr, BH, N, N);
-    else fa2::fa2_bwd_preprocess<64, false><<<grid, 256, 0, st>>>(o, dout, d_out, nullptr, BH, N, N);
-  } else {
-    if (bf16) fa2::fa2_bwd_preprocess<128, true><<<grid, 256, 0, st>>>(o, dout, d_out, nullptr, BH, N, N);
-    else fa2::fa2_bwd_preprocess<128, false><<<grid, 256, 0, st>>>(o, dout, d_out, nullptr, BH, N, N);
-  }
+  // d_out has N entries per head (no padding): the fixed row geometry with N_pad = N
+  fa2::RowParams rp{};
+  rp.o = o;
+  rp.dout = dout;
+  rp.dvec = d_out;
+  rp.B = B;
+  rp.H = H;
+  rp.Nq = N;
+  rp.acc_hs = N;
+  rp.acc_rows = static_cast<long long>(B) * H * N;
+  rp.o_rs = d;
+  rp.o_hs = static_cast<long long>(N) * d;
+  rp.o_bs = rp.o_hs * H;
+  if ((s = preprocess_impl(rp, d, dtype, static_cast<cudaStream_t>(stream))) != FA2_OK) return s;
   FA2_CUDA(cudaGetLastError());
   g_launches = 1;
   return FA2_OK;
@@ -484,9 +714,11 @@ fa2_status_t fa2_attention_step_host(const void* q_h, const void* k_h, const voi
   FA2_CUDA(cudaMemcpyAsync(k, k_h, t, cudaMemcpyHostToDevice, st));
   FA2_CUDA(cudaMemcpyAsync(v, v_h, t, cudaMemcpyHostToDevice, st));
   FA2_CUDA(cudaMemcpyAsync(dout, dout_h, t, cudaMemcpyHostToDevice, st));
-  if ((s = forward_impl(q, k, v, o, lse, B, H, H, N, d, causal, softmax_scale, dtype, st, di.sms)) != FA2_OK) return s;
-  if ((s = backward_impl(q, k, v, o, lse, dout, dq, dk, dv, ws, B, H, H, N, d, causal, softmax_scale, dtype, st,
-                         di.sms)) != FA2_OK)
+  if ((s = forward_impl(q, k, v, o, lse, fixed_geom(B, H, H, N, N, d), causal, softmax_scale, dtype, st, di.sms)) !=
+      FA2_OK)
+    return s;
+  if ((s = backward_impl(q, k, v, o, lse, dout, dq, dk, dv, ws, fixed_geom(B, H, H, N, N, d), causal, softmax_scale,
+                         dtype, st, di.sms, false)) != FA2_OK)
     return s;
   if (o_h) FA2_CUDA(cudaMemcpyAsync(o_h, o, t, cudaMemcpyDeviceToHost, st));
   if (lse_h) FA2_CUDA(cudaMemcpyAsync(lse_h, lse, lbytes, cudaMemcpyDeviceToHost, st));

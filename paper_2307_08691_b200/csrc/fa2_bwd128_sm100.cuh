@@ -57,7 +57,7 @@ struct Bwd128Smem {
   static_assert(ALLOC <= 232448, "shared memory budget");
 };
 
-template <bool BF16, bool CAUSAL>
+template <bool BF16, bool CAUSAL, bool GEN>
 __global__ void __launch_bounds__(kBwdThreads, 1)
 fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
@@ -119,12 +119,8 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
   const uint32_t tmem = *tmem_slot;
   constexpr uint32_t T_S = 0, T_DP = 128, T_DV = 256, T_DK = 384;
 
-  const int N = p.N;
-  const int n_q_blocks = (N + BM - 1) / BM;
   const float* gD = p.dvec;
-  const float* gL2 = p.dvec + static_cast<size_t>(p.BH) * p.npad;
-  auto decode = [&](int t, int& bh, int& nb) { bwd_decode(p, CAUSAL, t, bh, nb); };
-  auto q_begin = [&](int nb) -> int { return CAUSAL ? nb : 0; };   // B_r == B_c == 128
+  const float* gL2 = p.dvec + p.acc_rows;
 
   if (warp < 8) {
     // ====================== compute warpgroups: P^T, dS^T ======================
@@ -136,16 +132,25 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
     const int c0 = wg * 64;                             // this warpgroup's 64 query columns
     uint32_t g = 0;
     int it = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-      int bh, nb;
-      decode(t, bh, nb);
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      BwdTile w;
+      if (!bwd_tile<GEN>(p, CAUSAL, t, w)) continue;
+      const int nb = w.nb, nqt = w.nqt, nk = w.sq.nk, off = w.sq.off;
       const int kv_row = nb * 128 + r;
-      const int i0 = q_begin(nb), nqt = n_q_blocks - i0;
+      if (nqt == 0) {   // no query row sees this key block (N_q == 0): dV = dK = 0
+        if (kv_row < nk) {
+          uint4* z = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(wg == 0 ? p.dv : p.dk) + bwd_kv_off<GEN>(p, w, kv_row) * 2);
+          for (int e = 0; e < D / 8; ++e) z[e] = make_uint4(0u, 0u, 0u, 0u);
+        }
+        continue;
+      }
       for (int x = 0; x < nqt * p.group; ++x, ++g) {
-        const int i = bwd_q_tile(p, CAUSAL, nb, x % nqt, n_q_blocks);
+        const int i = bwd_q_tile(p, CAUSAL, w, x % nqt);
         const uint32_t slot = g & 1;
         const uint32_t vL2 = sVec_a + slot * 2 * BM * 4, vD = vL2 + BM * 4;
-        const bool need_mask = (CAUSAL && i == nb) || (nb * 128 + 128 > N);
+        // mask: causal tiles crossing the (bottom-right aligned, R22) diagonal and the ragged key tail;
+        // query rows past N_q need none (their L*log2e is +inf in the workspace, so P = 0)
+        const bool need_mask = (CAUSAL && nb * 128 + 127 > i * BM + off) || (nb * 128 + 128 > nk);
         // ---- P^T = exp2(S^T * scale*log2e - L*log2e), masked ----
         ptx::mbar_wait(&q_full[slot], (g >> 1) & 1);
         ptx::mbar_wait(s_full, g & 1);
@@ -163,7 +168,7 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
             float pv = ptx::ex2(fmaf(__uint_as_float(sv[e]), p.scale_log2, -ptx::lds_f32(vL2 + c * 4)));
             if (need_mask) {
               const int q_row = i * BM + c;
-              if ((CAUSAL && kv_row > q_row) || kv_row >= N) pv = 0.f;
+              if ((CAUSAL && kv_row > q_row + off) || kv_row >= nk) pv = 0.f;
             }
             pf[ch * 32 + e] = pv;
           }
@@ -224,7 +229,7 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
       {
         const uint32_t tsrc = tmem + lane_base + (wg == 0 ? T_DV : T_DK);
         const float mul = wg == 0 ? 1.f : p.scale;
-        uint8_t* dst = reinterpret_cast<uint8_t*>(wg == 0 ? p.dv : p.dk) + (static_cast<size_t>(bh) * N + kv_row) * (D * 2);
+        uint8_t* dst = reinterpret_cast<uint8_t*>(wg == 0 ? p.dv : p.dk) + bwd_kv_off<GEN>(p, w, kv_row) * 2;
 #pragma unroll
         for (int ch = 0; ch < D / 32; ++ch) {
           uint32_t v[32];
@@ -233,7 +238,7 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
           uint32_t o16[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) o16[e] = ptx::pack2<BF16>(__uint_as_float(v[2 * e]) * mul, __uint_as_float(v[2 * e + 1]) * mul);
-          if (kv_row < N) {
+          if (kv_row < nk) {
             uint4* o = reinterpret_cast<uint4*>(dst + ch * 64);
 #pragma unroll
             for (int e = 0; e < 4; ++e) o[e] = make_uint4(o16[4 * e], o16[4 * e + 1], o16[4 * e + 2], o16[4 * e + 3]);
@@ -243,6 +248,7 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(dkv_empty);
+      ++it;
     }
   } else if (warp < 12) {
     // ====================== dQ read-out + fp32 reduce-add ======================
@@ -253,12 +259,13 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
     const uint32_t sDQ_a = ptx::smem_u32(sDQ);
     uint32_t g = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-      int bh, nb;
-      decode(t, bh, nb);
-      const int i0 = q_begin(nb), nqt = n_q_blocks - i0;
-      const int bq0 = (bh / p.Hkv) * p.H + (bh % p.Hkv) * p.group;   // first query head of this kv head
+      BwdTile w;
+      if (!bwd_tile<GEN>(p, CAUSAL, t, w) || w.nqt == 0) continue;
+      const int nb = w.nb, nqt = w.nqt;
       for (int x = 0; x < nqt * p.group; ++x, ++g) {
-        const int i = bwd_q_tile(p, CAUSAL, nb, x % nqt, n_q_blocks), bhq = bq0 + x / nqt;
+        const int i = bwd_q_tile(p, CAUSAL, w, x % nqt);
+        const long long acc0 = bwd_acc_row0<GEN>(p, w, w.kvh * p.group + x / nqt);   // query head of the group
+        float* const dq_rows = p.dq_acc + (acc0 + i * BM) * D;                        // this tile's 128 rows
         ptx::mbar_wait(dq_full, g & 1);
         if (leader) FA2_BTRACE(9, g);
         ptx::tc_fence_after();
@@ -280,7 +287,7 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
           if (leader) {
             ptx::bulk_wait_read<L::DQ_NBUF - 1>();
             // deterministic mode: wait for this key block's turn on dQ tile (bhq, i)
-            if (p.dq_sem != nullptr && rd == 0) dq_sem_wait(dq_sem_ptr(p, bhq, i, n_q_blocks), dq_rank(p, nb, x % nqt));
+            if (p.dq_sem != nullptr && rd == 0) dq_sem_wait(dq_sem_ptr(p, acc0, i), dq_rank(p, nb, x % nqt));
           }
           ptx::named_bar_sync(1, 128);
 #pragma unroll
@@ -289,12 +296,12 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
           ptx::fence_proxy_async_smem();
           ptx::named_bar_sync(1, 128);
           if (leader) {
-            ptx::bulk_reduce_add_f32(p.dq_acc + (static_cast<size_t>(bhq) * p.npad + i * BM + rd * L::DQ_ROWS) * D,
+            ptx::bulk_reduce_add_f32(dq_rows + rd * (L::DQ_ROWS * D),
                                      sDQ + buf * L::DQ_BUF, L::DQ_BUF);
             ptx::bulk_commit();
           }
         }
-        if (leader && p.dq_sem != nullptr) dq_sem_release(dq_sem_ptr(p, bhq, i, n_q_blocks), dq_rank(p, nb, x % nqt));
+        if (leader && p.dq_sem != nullptr) dq_sem_release(dq_sem_ptr(p, acc0, i), dq_rank(p, nb, x % nqt));
         if (leader) FA2_BTRACE(16, g);
       }
     }
@@ -330,10 +337,10 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
     uint32_t g = 0;
     int it = 0;
     uint32_t dkv_uses = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-      int bh, nb;
-      decode(t, bh, nb);
-      const uint32_t n = static_cast<uint32_t>((n_q_blocks - q_begin(nb)) * p.group);
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      BwdTile w;
+      if (!bwd_tile<GEN>(p, CAUSAL, t, w) || w.nqt == 0) continue;
+      const uint32_t n = static_cast<uint32_t>(w.nqt * p.group);
       const uint32_t g0 = g;
       ptx::mbar_wait(kv_full, it & 1);
       // prologue: S^T of the first query tile (the S^T columns were last read by dV of the
@@ -403,6 +410,7 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
         ptx::mma_commit(kv_empty);
       }
       __syncwarp();
+      ++it;
     }
   } else if (warp == 13) {
     // ============================ TMA producer ============================
@@ -412,35 +420,36 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
       int it = 0;
       const uint64_t pol_q = ptx::l2_policy_evict_last();
       const uint64_t pol_kv = ptx::l2_policy_evict_first();
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-        int bh, nb;
-        decode(t, bh, nb);
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        BwdTile w;
+        if (!bwd_tile<GEN>(p, CAUSAL, t, w) || w.nqt == 0) continue;
+        const int nb = w.nb, nqt = w.nqt;
         if (it > 0) ptx::mbar_wait(kv_empty, (it - 1) & 1);
         ptx::mbar_arrive_expect_tx(kv_full, 2 * L::TILE);
         for (int s = 0; s < NSUB; ++s) {
-          ptx::tma_load_3d_hint(sK + s * L::SUB, &tm_k, kv_full, s * 64, nb * 128, bh, pol_kv);
-          ptx::tma_load_3d_hint(sV + s * L::SUB, &tm_v, kv_full, s * 64, nb * 128, bh, pol_kv);
+          tma_load_rows<GEN>(sK + s * L::SUB, &tm_k, kv_full, p.geom, s * 64, w.sq.k0 + nb * 128, w.kvh, w.sq.bc, p.Hkv, pol_kv);
+          tma_load_rows<GEN>(sV + s * L::SUB, &tm_v, kv_full, p.geom, s * 64, w.sq.k0 + nb * 128, w.kvh, w.sq.bc, p.Hkv, pol_kv);
         }
-        const int i0 = q_begin(nb), nqt = n_q_blocks - i0;
-        const int bq0 = (bh / p.Hkv) * p.H + (bh % p.Hkv) * p.group;
         for (int x = 0; x < nqt * p.group; ++x, ++g) {
-          const int i = bwd_q_tile(p, CAUSAL, nb, x % nqt, n_q_blocks), bhq = bq0 + x / nqt;
+          const int i = bwd_q_tile(p, CAUSAL, w, x % nqt), hq = w.kvh * p.group + x / nqt;
           const uint32_t slot = g & 1;
           // Q_i, L_i, D_i (2-stage ring; released after dK(i))
           if (g >= 2) ptx::mbar_wait(&q_empty[slot], ((g >> 1) - 1) & 1);
           ptx::mbar_arrive_expect_tx(&q_full[slot], L::TILE + 2 * BM * 4);
           for (int s = 0; s < NSUB; ++s)
-            ptx::tma_load_3d_hint(sQ + slot * L::TILE + s * L::SUB, &tm_q, &q_full[slot], s * 64, i * BM, bhq, pol_q);
+            tma_load_rows<GEN>(sQ + slot * L::TILE + s * L::SUB, &tm_q, &q_full[slot], p.geom, s * 64, w.sq.q0 + i * BM, hq,
+                          w.sq.bc, p.H, pol_q);
           float* vdst = sVec + slot * 2 * BM;
-          const size_t voff = static_cast<size_t>(bhq) * p.npad + static_cast<size_t>(i) * BM;
+          const long long voff = bwd_acc_row0<GEN>(p, w, hq) + static_cast<long long>(i) * BM;
           ptx::bulk_load_1d(vdst, gL2 + voff, BM * 4, &q_full[slot]);
           ptx::bulk_load_1d(vdst + BM, gD + voff, BM * 4, &q_full[slot]);
           // dO_i (single stage; released after dP^T(i))
           if (g >= 1) ptx::mbar_wait(do_empty, (g - 1) & 1);
           ptx::mbar_arrive_expect_tx(do_full, L::TILE);
           for (int s = 0; s < NSUB; ++s)
-            ptx::tma_load_3d_hint(sDO + s * L::SUB, &tm_do, do_full, s * 64, i * BM, bhq, pol_q);
+            tma_load_rows<GEN>(sDO + s * L::SUB, &tm_do, do_full, p.geom, s * 64, w.sq.q0 + i * BM, hq, w.sq.bc, p.H, pol_q);
         }
+        ++it;
       }
     }
   } else {

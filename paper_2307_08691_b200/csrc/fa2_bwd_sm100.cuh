@@ -29,7 +29,7 @@
 #pragma once
 #include <cuda_fp16.h>
 #include <cuda_bf16.h>
-#include "sm100_ptx.cuh"
+#include "fa2_seq.cuh"
 
 namespace fa2 {
 
@@ -42,20 +42,70 @@ struct BwdMaps {
 
 struct BwdParams {
   const float* lse;     // unused by the main kernel (L2 in workspace); kept for reference
-  const float* dvec;    // workspace: [BH, npad] D, followed by [BH, npad] L*log2(e)
+  const float* dvec;    // workspace: [acc_rows] D, followed by [acc_rows] L*log2(e)
   void* dk;
   void* dv;
-  float* dq_acc;        // fp32 dQ accumulator ([BH, npad, D], or [BH, D, npad] when transposed)
-  int BH, N, npad;      // BH = B * H (query heads)
+  float* dq_acc;        // fp32 dQ accumulator [acc_rows, D] (padded query rows, RowParams)
+  int BH;              // B * H (query heads)
   int H, Hkv, group;    // query heads, key/value heads, H / Hkv (GQA; group == 1 for MHA)
   int num_n_blocks;     // ceil(N / 128)
   int num_tiles;        // BH * num_n_blocks
   float scale;
   float scale_log2;
   unsigned long long* trace;  // optional clock64 trace (CTA 0, first work tile), nullptr in production
-  int* dq_sem;          // deterministic mode: [BH, num_n_blocks] dQ tile counters (nullptr: arrival order)
-  int det_cyclic;       // deterministic schedule (see bwd_q_tile): 1 when num_n_blocks <= gridDim.x
+  int* dq_sem;          // deterministic mode: one counter per 128-row tile of the padded workspace
+  int det_cyclic;       // deterministic schedule (see bwd_q_tile): 1 for the square fixed layout when
+                        // num_n_blocks <= gridDim.x
+  SeqGeom geom;                  // sequence geometry (fa2_seq.cuh)
+  long long k_bs, k_hs, k_rs;    // dK / dV strides in elements: batch, key/value head, row
+  long long acc_bs, acc_hs;      // padded workspace rows per batch entry (fixed layout) and per query head
+  long long acc_rows;            // rows of dq_acc (and of D, L*log2e) in total
+  const int* tile_off;           // packed: [B+1] prefix sums of ceil(N_q(b) / 128); nullptr: fixed layout
 };
+
+// A backward work tile: key block nb (128 rows) of key/value head kvh of sequence b,
+// visited with query tiles i0 .. i0+nqt-1 of every query head of the group.
+struct BwdTile {
+  int b, kvh, nb;
+  Seq sq;
+  int nqb;        // query tiles of the sequence, ceil(N_q / 128)
+  int i0, nqt;    // first query tile and number of query tiles (per query head)
+};
+FA2_DEVICE void bwd_decode(const BwdParams& p, bool causal, int t, int& bh, int& nb);
+// Returns false when the key block lies past the sequence's keys (nothing to do).
+// nqt == 0 (no query row sees the block, i.e. N_q == 0): dK = dV = 0 for its rows.
+template <bool GEN>
+FA2_DEVICE bool bwd_tile(const BwdParams& p, bool causal, int t, BwdTile& w) {
+  int bh, nb;
+  bwd_decode(p, causal, t, bh, nb);
+  w.b = bh / p.Hkv;
+  w.kvh = bh % p.Hkv;
+  w.nb = nb;
+  w.sq = seq_of<GEN>(p.geom, w.b);
+  if (nb * 128 >= w.sq.nk) return false;
+  w.nqb = (w.sq.nq + 127) / 128;
+  int i0 = 0;
+  if (causal) {   // first query row that sees key nb*128: row >= nb*128 - (N_k - N_q) (R22)
+    const int first_row = nb * 128 - w.sq.off;
+    i0 = first_row > 0 ? first_row / 128 : 0;
+  }
+  w.i0 = i0;
+  w.nqt = w.nqb > i0 ? w.nqb - i0 : 0;
+  return true;
+}
+// Padded workspace row of query row 0 of (sequence b, query head hq): rows of dq_acc,
+// D and L*log2e; every sequence starts at a multiple of 128.
+template <bool GEN>
+FA2_DEVICE long long bwd_acc_row0(const BwdParams& p, const BwdTile& w, int hq) {
+  if (GEN && p.tile_off != nullptr) return hq * p.acc_hs + 128LL * __ldg(p.tile_off + w.b);
+  return w.sq.bc * p.acc_bs + hq * p.acc_hs;
+}
+// dK / dV row `kv_row` (sequence-relative) of the tile's key/value head, in elements
+template <bool GEN>
+FA2_DEVICE long long bwd_kv_off(const BwdParams& p, const BwdTile& w, int kv_row) {
+  if constexpr (!GEN) return (static_cast<long long>(w.b * p.Hkv + w.kvh) * w.sq.nk + kv_row) * p.k_rs;
+  return w.sq.bc * p.k_bs + w.kvh * p.k_hs + (w.sq.k0 + kv_row) * p.k_rs;
+}
 
 // ---------------------------------------------------------------------------
 // Work schedule shared by every warp role of both backward kernels.
@@ -83,9 +133,9 @@ FA2_DEVICE void bwd_decode(const BwdParams& p, bool causal, int t, int& bh, int&
   if (causal && p.dq_sem != nullptr && p.det_cyclic && ((t / static_cast<int>(gridDim.x)) & 1))
     nb = p.num_n_blocks - 1 - nb;
 }
-FA2_DEVICE int bwd_q_tile(const BwdParams& p, bool causal, int nb, int s, int n_q_blocks) {
-  if (causal) return nb + s;                       // B_r == B_c: key block nb starts at query tile nb
-  if (p.dq_sem != nullptr && p.det_cyclic) return nb + s < n_q_blocks ? nb + s : nb + s - n_q_blocks;
+FA2_DEVICE int bwd_q_tile(const BwdParams& p, bool causal, const BwdTile& w, int s) {
+  if (causal) return w.i0 + s;
+  if (p.dq_sem != nullptr && p.det_cyclic) return w.nb + s < w.nqb ? w.nb + s : w.nb + s - w.nqb;
   return s;
 }
 // One counter per dQ tile: dq_sem[bhq * n_q_blocks + i] = number of key blocks whose
@@ -96,9 +146,7 @@ FA2_DEVICE int bwd_q_tile(const BwdParams& p, bool causal, int nb, int s, int n_
 // tile in the ascending one, so the wait graph is acyclic and every CTA progresses.
 // (Finer-grained counters per part of a tile, with deferred releases, were measured
 // slower: tools/bench_det.py.)
-FA2_DEVICE int* dq_sem_ptr(const BwdParams& p, int bhq, int i, int n_q_blocks) {
-  return p.dq_sem + static_cast<size_t>(bhq) * n_q_blocks + i;
-}
+FA2_DEVICE int* dq_sem_ptr(const BwdParams& p, long long acc_row0, int i) { return p.dq_sem + acc_row0 / 128 + i; }
 FA2_DEVICE int dq_rank(const BwdParams& p, int nb, int s) { return p.det_cyclic ? s : nb; }
 FA2_DEVICE void dq_sem_wait(const int* sem, int rank) {
   while (ptx::ld_acquire_gpu(sem) != rank) {
@@ -119,73 +167,157 @@ FA2_DEVICE void dq_sem_release(int* sem, int rank) {
   } while (0)
 
 // ---------------------------------------------------------------------------
-// Preprocess: one warp per row (rows of the padded [BH, npad] grid).
-//   dvec[r] = sum_c dO[r,c] * O[r,c]         (r < N)      else 0
-//   lse2[r] = L[r] * log2(e)                 (r < N)      else +inf
-//   dq_acc[r, :] = 0
-//   dq_sem[bh, r / 128] = 0                  (deterministic mode, first row of a tile)
-// When dq_acc == nullptr (fa2_backward_preprocess) only dvec is written and
-// npad == N, lse == nullptr.
+// Row geometry of the backward workspace, shared by preprocess and dQ convert.
+// Workspace rows are "padded query rows": fixed layout (b*H + h) * N_pad + r; packed
+// layout h * acc_hs + 128 * tile_off[b] + r (every sequence starts at a multiple of
+// 128 so that whole 128-row query tiles address contiguous, aligned rows).
+// ---------------------------------------------------------------------------
+struct RowParams {
+  const void* o;          // q-layout tensors: O and dO (preprocess), dQ (convert)
+  const void* dout;
+  void* dq;
+  const float* lse;       // fixed [B,H,N_q]; packed [H,T_q]
+  float* dvec;            // [acc_rows] D
+  float* lse2;            // [acc_rows] L * log2(e) (+inf on padding rows and rows that saw no key)
+  float* dq_acc;          // [acc_rows, D] fp32
+  int* dq_sem;            // [acc_rows / 128] deterministic-mode counters (or nullptr)
+  int B, H, Nq;           // Nq: fixed query length
+  const int* cu_q;        // packed: [B+1]; nullptr for the fixed layout
+  const int* tile_off;    // packed: [B+1] prefix sums of ceil(N_q(b) / 128)
+  long long acc_hs;       // fixed: N_pad (rows per (b, h)); packed: rows per query head
+  long long acc_rows;     // total workspace rows
+  long long o_bs, o_hs, o_rs, l_bs, l_hs;   // strides (elements) of the q layout and of L
+};
+
+// Padded workspace row R -> element offsets of that query row in the q layout (O, dO)
+// and in L; false for padding rows.  32-bit index arithmetic: the host guarantees
+// acc_rows < 2^31.  Fixed layout: R = bh * N_pad + r with bh = b*H + h, so the q-layout
+// offset is bh * N_q * d + r * d and the L offset bh * N_q + r.
+FA2_DEVICE bool acc_row_ref(const RowParams& p, long long R, long long& q_off, long long& l_off) {
+  const unsigned hs = static_cast<unsigned>(p.acc_hs), Ru = static_cast<unsigned>(R);
+  const unsigned hd = Ru / hs, pr = Ru - hd * hs;   // fixed: (b*H + h, r); packed: (h, padded row)
+  if (p.cu_q == nullptr) {
+    if (pr >= static_cast<unsigned>(p.Nq)) return false;
+    q_off = static_cast<long long>(hd) * p.o_hs + static_cast<long long>(pr) * p.o_rs;
+    l_off = static_cast<long long>(hd) * p.l_hs + pr;
+    return true;
+  }
+  if (pr >= 128u * static_cast<unsigned>(__ldg(p.tile_off + p.B))) return false;
+  int lo = 0, hi = p.B;   // largest b with 128 * tile_off[b] <= pr (skips empty sequences)
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) / 2;
+    if (128u * static_cast<unsigned>(__ldg(p.tile_off + mid)) <= pr) lo = mid; else hi = mid;
+  }
+  const int q0 = __ldg(p.cu_q + lo);
+  const int r = static_cast<int>(pr - 128u * static_cast<unsigned>(__ldg(p.tile_off + lo)));
+  if (r >= __ldg(p.cu_q + lo + 1) - q0) return false;
+  q_off = static_cast<long long>(hd) * p.o_hs + static_cast<long long>(q0 + r) * p.o_rs;
+  l_off = static_cast<long long>(hd) * p.l_hs + q0 + r;
+  return true;
+}
+
+// packed layout: tile_off[b] = sum_{b' < b} ceil(N_q(b') / 128), one block
+__global__ void __launch_bounds__(1024) fa2_tile_prefix(const int* __restrict__ cu_q, int B, int* __restrict__ tile_off) {
+  __shared__ int part[1024];
+  const int per = (B + 1023) / 1024;
+  const int b0 = threadIdx.x * per, b1 = min(B, b0 + per);
+  int sum = 0;
+  for (int b = b0; b < b1; ++b) sum += (cu_q[b + 1] - cu_q[b] + 127) / 128;
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {   // inclusive Hillis-Steele scan
+    const int v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int run = threadIdx.x == 0 ? 0 : part[threadIdx.x - 1];
+  for (int b = b0; b < b1; ++b) {
+    tile_off[b] = run;
+    run += (cu_q[b + 1] - cu_q[b] + 127) / 128;
+  }
+  if (threadIdx.x == 1023) tile_off[B] = part[1023];
+}
+
+// ---------------------------------------------------------------------------
+// Preprocess: one warp per padded workspace row R.
+//   dvec[R] = sum_c dO[row, c] * O[row, c]     (real rows)       else 0
+//   lse2[R] = L[row] * log2(e)                 (real rows, finite L; +inf otherwise:
+//             padding rows and rows that saw no key, R23, so P = 0 there)
+//   dq_acc[R, :] = 0 ; dq_sem[R / 128] = 0 at the first row of a tile (deterministic mode)
+// fa2_backward_preprocess uses it with lse2 == dq_acc == nullptr and N_pad == N_q.
 // ---------------------------------------------------------------------------
 template <int D, bool BF16>
-__global__ void __launch_bounds__(256)
-fa2_bwd_preprocess(const void* __restrict__ o, const void* __restrict__ dout, float* __restrict__ dvec,
-                   float* __restrict__ dq_acc, int BH, int N, int npad, const float* __restrict__ lse = nullptr,
-                   float* __restrict__ lse2 = nullptr, int* __restrict__ dq_sem = nullptr) {
-  const long long row = static_cast<long long>(blockIdx.x) * 8 + threadIdx.x / 32;
+__global__ void __launch_bounds__(256) fa2_bwd_preprocess(const RowParams p) {
+  const long long R = static_cast<long long>(blockIdx.x) * 8 + threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  if (row >= static_cast<long long>(BH) * npad) return;
-  const int bh = static_cast<int>(row / npad);
-  const int r = static_cast<int>(row % npad);
+  if (R >= p.acc_rows) return;
+  long long q_off = 0, l_off = 0;
+  const bool real = acc_row_ref(p, R, q_off, l_off);
   constexpr int PER = D / 32;  // elements per lane (2 or 4)
   float acc = 0.f;
-  if (r < N) {
-    const size_t base = (static_cast<size_t>(bh) * N + r) * D + lane * PER;
+  if (real) {
+    const long long base = q_off + lane * PER;
     if constexpr (PER == 4) {
-      const uint2 a = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(o) + base);
-      const uint2 b = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(dout) + base);
+      const uint2 a = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(p.o) + base);
+      const uint2 c = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(p.dout) + base);
       const float2 a0 = ptx::unpack2<BF16>(a.x), a1 = ptx::unpack2<BF16>(a.y);
-      const float2 b0 = ptx::unpack2<BF16>(b.x), b1 = ptx::unpack2<BF16>(b.y);
-      acc = a0.x * b0.x + a0.y * b0.y + a1.x * b1.x + a1.y * b1.y;
+      const float2 c0 = ptx::unpack2<BF16>(c.x), c1 = ptx::unpack2<BF16>(c.y);
+      acc = a0.x * c0.x + a0.y * c0.y + a1.x * c1.x + a1.y * c1.y;
     } else {
-      const uint32_t a = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint16_t*>(o) + base);
-      const uint32_t b = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint16_t*>(dout) + base);
-      const float2 a0 = ptx::unpack2<BF16>(a), b0 = ptx::unpack2<BF16>(b);
-      acc = a0.x * b0.x + a0.y * b0.y;
+      const uint32_t a = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint16_t*>(p.o) + base);
+      const uint32_t c = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint16_t*>(p.dout) + base);
+      const float2 a0 = ptx::unpack2<BF16>(a), c0 = ptx::unpack2<BF16>(c);
+      acc = a0.x * c0.x + a0.y * c0.y;
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   }
   if (lane == 0) {
-    dvec[row] = acc;
-    if (lse2 != nullptr) lse2[row] = (r < N) ? lse[static_cast<size_t>(bh) * N + r] * 1.4426950408889634f : INFINITY;
+    p.dvec[R] = acc;
+    if (p.lse2 != nullptr) {
+      const float l = real ? p.lse[l_off] : INFINITY;
+      p.lse2[R] = l == -INFINITY ? INFINITY : l * 1.4426950408889634f;
+    }
+    if (p.dq_sem != nullptr && R % 128 == 0) p.dq_sem[R / 128] = 0;
   }
-  if (dq_sem != nullptr && r % 128 == 0 && lane == 0) dq_sem[static_cast<size_t>(bh) * (npad / 128) + r / 128] = 0;
-  if (dq_acc != nullptr) {
-    float4* z = reinterpret_cast<float4*>(dq_acc + row * D);
+  if (p.dq_acc != nullptr) {
+    float4* z = reinterpret_cast<float4*>(p.dq_acc + R * D);
     for (int c = lane; c < D / 4; c += 32) z[c] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
 }
 
-template <bool BF16>
-__global__ void __launch_bounds__(256)
-fa2_dq_convert(const float* __restrict__ dq_acc, void* __restrict__ dq, int BH, int N, int npad, int D) {
+// dQ = cast(dq_acc) for every real query row: one thread per 8 elements of the q layout
+// (fixed: [B,H,N_q,D] in order; packed: [T_q,H,D] in order).
+template <int D, bool BF16>
+__global__ void __launch_bounds__(256) fa2_dq_convert(const RowParams p, long long rows_out) {
   const long long i8 = static_cast<long long>(blockIdx.x) * 256 + threadIdx.x;  // index of 8-element group
-  const long long total8 = static_cast<long long>(BH) * N * D / 8;
-  if (i8 >= total8) return;
-  const long long e = i8 * 8;
-  const long long row = e / D;
-  const int c = static_cast<int>(e % D);
-  const int bh = static_cast<int>(row / N);
-  const int r = static_cast<int>(row % N);
-  const float4* src = reinterpret_cast<const float4*>(dq_acc + (static_cast<size_t>(bh) * npad + r) * D + c);
+  if (i8 >= rows_out * (D / 8)) return;
+  const long long row = i8 / (D / 8);
+  const int c = static_cast<int>(i8 % (D / 8)) * 8;
+  long long R;
+  if (p.cu_q == nullptr) {            // row = (b*H + h)*N_q + r   (rows_out < 2^31, host-checked)
+    const unsigned ru = static_cast<unsigned>(row), nq = static_cast<unsigned>(p.Nq);
+    const unsigned bh = ru / nq;
+    R = static_cast<long long>(bh) * p.acc_hs + (ru - bh * nq);
+  } else {                            // row = t*H + h
+    const unsigned ru = static_cast<unsigned>(row), hh = static_cast<unsigned>(p.H);
+    const int t = static_cast<int>(ru / hh), h = static_cast<int>(ru - (ru / hh) * hh);
+    int lo = 0, hi = p.B;             // the sequence b with cu_q[b] <= t < cu_q[b+1] (largest such b)
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) / 2;
+      if (__ldg(p.cu_q + mid) <= t) lo = mid; else hi = mid;
+    }
+    R = h * p.acc_hs + 128LL * __ldg(p.tile_off + lo) + (t - __ldg(p.cu_q + lo));
+  }
+  const float4* src = reinterpret_cast<const float4*>(p.dq_acc + R * D + c);
   const float4 a = src[0], b = src[1];
   uint4 out;
   out.x = ptx::pack2<BF16>(a.x, a.y);
   out.y = ptx::pack2<BF16>(a.z, a.w);
   out.z = ptx::pack2<BF16>(b.x, b.y);
   out.w = ptx::pack2<BF16>(b.z, b.w);
-  reinterpret_cast<uint4*>(dq)[i8] = out;
+  reinterpret_cast<uint4*>(p.dq)[i8] = out;
 }
 
 template <int D>
@@ -214,7 +346,7 @@ struct BwdSmem {
   static_assert(ALLOC <= 232448, "shared memory budget");
 };
 
-template <int D, bool BF16, bool CAUSAL>
+template <int D, bool BF16, bool CAUSAL, bool GEN>
 __global__ void __launch_bounds__(kBwdThreads, 1)
 fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
@@ -281,31 +413,33 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   constexpr uint32_t T_PT = T_DQ + 64, T_DST = T_PT + BM / 2;
   static_assert(T_PT + BM / 2 + (DST_TMEM ? BM / 2 : 0) <= 512, "TMEM budget");
 
-  const int N = p.N;
-  const int n_q_blocks = (N + BM - 1) / BM;
+  static_assert(BM == 128, "query tiles of 128 rows (bwd_tile / bwd_q_tile assume B_r == B_c)");
   const float* gD = p.dvec;
-  const float* gL2 = p.dvec + static_cast<size_t>(p.BH) * p.npad;
-
-  // tile t -> (bh, n_block); for causal, low n_block (more query blocks) first
-  auto decode = [&](int t, int& bh, int& nb) { bwd_decode(p, CAUSAL, t, bh, nb); };
-  auto q_begin = [&](int nb) -> int { return CAUSAL ? (nb * 128) / BM : 0; };
+  const float* gL2 = p.dvec + p.acc_rows;
 
   if (warp < 8) {
     // ====================== compute warpgroups: P^T, dS^T ======================
+    ptx::setmaxnreg_inc<144>();   // 144*384 + 80*128 == 128*512 (compute + dQ warpgroups / control warps)
     const int wg = warp / 4;
     const int r = threadIdx.x % 128;                   // key row within the block == TMEM lane
     const uint32_t lane_base = static_cast<uint32_t>((warp % 4) * 32) << 16;
     const uint32_t sVec_a = ptx::smem_u32(sVec), sDST_a = ptx::smem_u32(sDST);
     uint32_t g = 0;          // global query-tile counter
     int it = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-      int bh, nb;
-      decode(t, bh, nb);
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      BwdTile w;
+      if (!bwd_tile<GEN>(p, CAUSAL, t, w)) continue;
+      const int nb = w.nb, nqt = w.nqt, nk = w.sq.nk, off = w.sq.off;
       const int kv_row = nb * 128 + r;
-      const int i0 = q_begin(nb), nqt = n_q_blocks - i0;
-      const int bq0 = (bh / p.Hkv) * p.H + (bh % p.Hkv) * p.group;   // first query head of this kv head
+      if (nqt == 0) {   // no query row sees this key block (N_q == 0): dV = dK = 0
+        if (kv_row < nk) {
+          uint4* z = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(wg == 0 ? p.dv : p.dk) + bwd_kv_off<GEN>(p, w, kv_row) * 2);
+          for (int e = 0; e < D / 8; ++e) z[e] = make_uint4(0u, 0u, 0u, 0u);
+        }
+        continue;
+      }
       for (int x = 0; x < nqt * p.group; ++x, ++g) {
-        const int i = bwd_q_tile(p, CAUSAL, nb, x % nqt, n_q_blocks), bhq = bq0 + x / nqt;  // query tile, query head
+        const int i = bwd_q_tile(p, CAUSAL, w, x % nqt);   // query tile (of query head kvh*group + x/nqt)
         const int slot = g % STAGES;
         ptx::mbar_wait(&q_full[slot], (g / STAGES) & 1);
         ptx::mbar_wait(s_full, g & 1);
@@ -313,7 +447,9 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         ptx::tc_fence_after();
         const uint32_t vL2 = sVec_a + slot * 2 * BM * 4;     // L_i * log2(e) for the BM query rows
         const uint32_t vD = vL2 + BM * 4;                     // D_i
-        const bool need_mask = (CAUSAL && (i * BM < nb * 128 + 128)) || (nb * 128 + 128 > N);
+        // causal tiles crossing the (bottom-right aligned, R22) diagonal and the ragged key tail; query
+        // rows past N_q need no mask (L*log2e = +inf in the workspace -> P = 0)
+        const bool need_mask = (CAUSAL && nb * 128 + 127 > i * BM + off) || (nb * 128 + 128 > nk);
         uint32_t pk[HALF / 2], dk[HALF / 2];
 #pragma unroll
         for (int ch = 0; ch < HALF / 32; ++ch) {
@@ -338,7 +474,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
               float pv = ptx::ex2(fmaf(__uint_as_float(sv[2 * e + h]), p.scale_log2, -ptx::lds_f32(vL2 + c * 4)));
               if (need_mask) {
                 const int q_row = i * BM + c;
-                if ((CAUSAL && kv_row > q_row) || kv_row >= N) pv = 0.f;
+                if ((CAUSAL && kv_row > q_row + off) || kv_row >= nk) pv = 0.f;
               }
               pp[h] = pv;
               dd[h] = pv * (__uint_as_float(dpv[2 * e + h]) - ptx::lds_f32(vD + c * 4));
@@ -380,7 +516,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       {
         const uint32_t tsrc = tmem + lane_base + (wg == 0 ? T_DV : T_DK);
         const float mul = wg == 0 ? 1.f : p.scale;
-        uint8_t* dst = reinterpret_cast<uint8_t*>(wg == 0 ? p.dv : p.dk) + (static_cast<size_t>(bh) * N + kv_row) * (D * 2);
+        uint8_t* dst = reinterpret_cast<uint8_t*>(wg == 0 ? p.dv : p.dk) + bwd_kv_off<GEN>(p, w, kv_row) * 2;
 #pragma unroll
         for (int ch = 0; ch < D / 32; ++ch) {
           uint32_t v[32];
@@ -389,7 +525,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           uint32_t pk[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) pk[e] = ptx::pack2<BF16>(__uint_as_float(v[2 * e]) * mul, __uint_as_float(v[2 * e + 1]) * mul);
-          if (kv_row < N) {
+          if (kv_row < nk) {
             uint4* o = reinterpret_cast<uint4*>(dst + ch * 64);
 #pragma unroll
             for (int e = 0; e < 4; ++e) o[e] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
@@ -399,21 +535,23 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(dkv_empty);
+      ++it;
     }
   } else if (warp < 12) {
     // ====================== dQ readout + fp32 reduce-add ======================
+    ptx::setmaxnreg_inc<144>();
     const int r = threadIdx.x - 256;                    // 0..127 == TMEM lane
     const uint32_t lane_base = static_cast<uint32_t>((warp % 4) * 32) << 16;
     const bool leader = (r == 0);
     const uint32_t sDQ_a = ptx::smem_u32(sDQ);
     uint32_t g = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-      int bh, nb;
-      decode(t, bh, nb);
-      const int i0 = q_begin(nb), nqt = n_q_blocks - i0;
-      const int bq0 = (bh / p.Hkv) * p.H + (bh % p.Hkv) * p.group;   // first query head of this kv head
+      BwdTile w;
+      if (!bwd_tile<GEN>(p, CAUSAL, t, w) || w.nqt == 0) continue;
+      const int nb = w.nb, nqt = w.nqt;
       for (int x = 0; x < nqt * p.group; ++x, ++g) {
-        const int i = bwd_q_tile(p, CAUSAL, nb, x % nqt, n_q_blocks), bhq = bq0 + x / nqt;  // query tile, query head
+        const int i = bwd_q_tile(p, CAUSAL, w, x % nqt);
+        const long long acc0 = bwd_acc_row0<GEN>(p, w, w.kvh * p.group + x / nqt);   // query head of the group
         ptx::mbar_wait(dq_full, g & 1);
         if (leader) FA2_BTRACE(7, g);
         ptx::tc_fence_after();
@@ -454,17 +592,19 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         if (leader) {
 #pragma unroll
           // deterministic mode: wait for this key block's turn on dQ tile (bhq, i)
-          if (p.dq_sem != nullptr) dq_sem_wait(dq_sem_ptr(p, bhq, i, n_q_blocks), dq_rank(p, nb, x % nqt));
+          if (p.dq_sem != nullptr) dq_sem_wait(dq_sem_ptr(p, acc0, i), dq_rank(p, nb, x % nqt));
 #pragma unroll
-          for (int b = 0; b < D / 32; ++b) ptx::tma_reduce_add_3d(&tm_dq, sDQ + b * (BM * 128), b * 32, i * BM, bhq);
+          for (int b = 0; b < D / 32; ++b)
+            ptx::tma_reduce_add_2d(&tm_dq, sDQ + b * (BM * 128), b * 32, static_cast<int>(acc0 + i * BM));
           ptx::bulk_commit();
-          if (p.dq_sem != nullptr) dq_sem_release(dq_sem_ptr(p, bhq, i, n_q_blocks), dq_rank(p, nb, x % nqt));
+          if (p.dq_sem != nullptr) dq_sem_release(dq_sem_ptr(p, acc0, i), dq_rank(p, nb, x % nqt));
           FA2_BTRACE(8, g);
         }
       }
     }
     if (leader) ptx::bulk_wait<0>();
   } else if (warp == 12) {
+    ptx::setmaxnreg_dec<80>();
     // ================== MMA issuer: whole warp, one elected lane issues ==================
     constexpr uint32_t IDESC_S = ptx::idesc_f16(BF16, 128, BM, false, false);   // S^T, dP^T
     constexpr uint32_t IDESC_G = ptx::idesc_f16(BF16, 128, D, false, true);     // dV, dK
@@ -520,13 +660,12 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       __syncwarp();
       FA2_BTRACE(6, h);
     };
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-      int bh, nb;
-      decode(t, bh, nb);
-      const int i0 = q_begin(nb);
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      BwdTile w;
+      if (!bwd_tile<GEN>(p, CAUSAL, t, w) || w.nqt == 0) continue;
       ptx::mbar_wait(kv_full, it & 1);
       bool have_prev = false;
-      const int cnt = (n_q_blocks - i0) * p.group;   // query tiles of every query head of the group
+      const int cnt = w.nqt * p.group;   // query tiles of every query head of the group
       for (int x = 0; x < cnt; ++x, ++g) {
         const uint32_t slot = g % STAGES;
         FA2_BTRACE(10, g);
@@ -562,41 +701,47 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         ptx::mma_commit(kv_empty);
       }
       __syncwarp();
+      ++it;
     }
   } else if (warp == 13) {
+    ptx::setmaxnreg_dec<80>();
     // ============================ TMA producer ============================
     if (lane == 0) {
       uint32_t g = 0;
       int it = 0;
       const uint64_t pol_q = ptx::l2_policy_evict_last();
       const uint64_t pol_kv = ptx::l2_policy_evict_first();
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-        int bh, nb;
-        decode(t, bh, nb);
-        const int i0 = q_begin(nb), nqt = n_q_blocks - i0;
-        const int bq0 = (bh / p.Hkv) * p.H + (bh % p.Hkv) * p.group;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        BwdTile w;
+        if (!bwd_tile<GEN>(p, CAUSAL, t, w) || w.nqt == 0) continue;
+        const int nb = w.nb, nqt = w.nqt;
         if (it > 0) ptx::mbar_wait(kv_empty, (it - 1) & 1);
         ptx::mbar_arrive_expect_tx(kv_full, 2 * L::KV_TILE);
         for (int s = 0; s < NSUB; ++s) {
-          ptx::tma_load_3d_hint(sK + s * 128 * 128, &tm_k, kv_full, s * 64, nb * 128, bh, pol_kv);
-          ptx::tma_load_3d_hint(sV + s * 128 * 128, &tm_v, kv_full, s * 64, nb * 128, bh, pol_kv);
+          tma_load_rows<GEN>(sK + s * 128 * 128, &tm_k, kv_full, p.geom, s * 64, w.sq.k0 + nb * 128, w.kvh, w.sq.bc, p.Hkv, pol_kv);
+          tma_load_rows<GEN>(sV + s * 128 * 128, &tm_v, kv_full, p.geom, s * 64, w.sq.k0 + nb * 128, w.kvh, w.sq.bc, p.Hkv, pol_kv);
         }
         for (int x = 0; x < nqt * p.group; ++x, ++g) {
-          const int i = bwd_q_tile(p, CAUSAL, nb, x % nqt, n_q_blocks), bhq = bq0 + x / nqt;
+          const int i = bwd_q_tile(p, CAUSAL, w, x % nqt), hq = w.kvh * p.group + x / nqt;
           const int slot = g % STAGES;
           if (g >= STAGES) ptx::mbar_wait(&q_empty[slot], ((g / STAGES) - 1) & 1);
           ptx::mbar_arrive_expect_tx(&q_full[slot], 2 * L::Q_TILE + 2 * BM * 4);
           for (int s = 0; s < NSUB; ++s) {
-            ptx::tma_load_3d_hint(sQ + slot * L::Q_TILE + s * L::Q_SUB, &tm_q, &q_full[slot], s * 64, i * BM, bhq, pol_q);
-            ptx::tma_load_3d_hint(sDO + slot * L::Q_TILE + s * L::Q_SUB, &tm_do, &q_full[slot], s * 64, i * BM, bhq, pol_q);
+            tma_load_rows<GEN>(sQ + slot * L::Q_TILE + s * L::Q_SUB, &tm_q, &q_full[slot], p.geom, s * 64, w.sq.q0 + i * BM,
+                          hq, w.sq.bc, p.H, pol_q);
+            tma_load_rows<GEN>(sDO + slot * L::Q_TILE + s * L::Q_SUB, &tm_do, &q_full[slot], p.geom, s * 64,
+                          w.sq.q0 + i * BM, hq, w.sq.bc, p.H, pol_q);
           }
           float* vdst = sVec + slot * 2 * BM;
-          const size_t voff = static_cast<size_t>(bhq) * p.npad + static_cast<size_t>(i) * BM;
+          const long long voff = bwd_acc_row0<GEN>(p, w, hq) + static_cast<long long>(i) * BM;
           ptx::bulk_load_1d(vdst, gL2 + voff, BM * 4, &q_full[slot]);
           ptx::bulk_load_1d(vdst + BM, gD + voff, BM * 4, &q_full[slot]);
         }
+        ++it;
       }
     }
+  } else {
+    ptx::setmaxnreg_dec<80>();   // warps 14-15 idle (complete the control warpgroup)
   }
   __syncwarp();
   ptx::tc_fence_before();

@@ -31,7 +31,7 @@
 #include <cuda_fp16.h>
 #include <cuda_bf16.h>
 #include <type_traits>
-#include "sm100_ptx.cuh"
+#include "fa2_seq.cuh"
 
 namespace fa2 {
 
@@ -43,11 +43,14 @@ namespace fa2 {
 constexpr int kFwdEmuPairs = FA2_FWD_EMU_PAIRS;
 
 struct FwdParams {
-  void* o;             // [BH, N, D] dtype
-  float* lse;          // [BH, N]
-  int BH, N;          // BH = B * H (query heads)
+  void* o;             // fixed: [B, H, N_q, D]; packed: [T_q, H, D] (dtype)
+  float* lse;          // fixed: [B, H, N_q]; packed: [H, T_q]
+  int BH;              // B * H (query heads)
   int H, Hkv, group;   // query heads, key/value heads, H / Hkv (GQA; group == 1 for MHA)
-  int num_m_blocks;    // ceil(N / 256)
+  SeqGeom geom;        // sequence lengths / offsets (fa2_seq.cuh)
+  long long o_bs, o_hs, o_rs;   // O strides in elements: batch, head, row
+  long long l_bs, l_hs;         // L strides: batch, head (row stride 1)
+  int num_m_blocks;    // ceil(N_q (max) / 256)
   int num_tiles;       // BH * num_m_blocks
   float scale_log2;    // softmax_scale * log2(e)
   unsigned long long* trace;  // optional clock64 trace (CTA 0, first tile), nullptr in production
@@ -78,7 +81,7 @@ struct FwdSmem {
   static constexpr int ALLOC = BYTES + 1024;   // slack for 1024-B alignment
 };
 
-template <int D, bool BF16, bool CAUSAL>
+template <int D, bool BF16, bool CAUSAL, bool GEN>
 __global__ void __launch_bounds__(384, 1)
 fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
@@ -138,24 +141,25 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int N = p.N;
-  const int n_kv_total = (N + 127) / 128;
 
   // Work-tile decode, shared by all roles.  Heads are contiguous in the tile
   // order so that the CTAs running concurrently share K/V in L2; for causal the
-  // heavy (late) row blocks of each head come first.
-  auto decode = [&](int t, int& bh, int& mb) {
+  // heavy (late) row blocks of each head come first.  sq: the tile's sequence.
+  auto decode = [&](int t, int& bh, int& mb, Seq& sq) {
     bh = t / p.num_m_blocks;
     int r = t % p.num_m_blocks;
     mb = CAUSAL ? (p.num_m_blocks - 1 - r) : r;
+    sq = seq_of<GEN>(p.geom, bh / p.H);
   };
-  // Number of KV blocks query sub-tile i of row block mb visits.
-  auto n_blocks = [&](int mb, int i) -> int {
+  // Number of KV blocks query sub-tile i of row block mb visits (0 when the sub-tile
+  // is past the sequence end, or when no row of it sees a key: causal, N_q > N_k).
+  auto n_blocks = [&](const Seq& sq, int mb, int i) -> int {
     const int r0 = mb * 256 + i * 128;
-    if (r0 >= N) return 0;
-    if (!CAUSAL) return n_kv_total;
-    const int last_row = min(N - 1, r0 + 127);
-    return min(n_kv_total, last_row / 128 + 1);
+    if (r0 >= sq.nq) return 0;
+    const int nkb = (sq.nk + 127) / 128;
+    if (!CAUSAL) return nkb;
+    const int last_col = min(sq.nq - 1, r0 + 127) + sq.off;   // last key the sub-tile's last row sees
+    return last_col < 0 ? 0 : min(nkb, last_col / 128 + 1);
   };
 
   if (warp < 8) {
@@ -174,11 +178,22 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     const float sl2 = p.scale_log2;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
       int bh, mb;
-      decode(t, bh, mb);
-      const int nb = n_blocks(mb, wg);
-      if (nb == 0) continue;
+      Seq sq;
+      decode(t, bh, mb, sq);
+      const int nb = n_blocks(sq, mb, wg);
       const int row0 = mb * 256 + wg * 128;
       const int grow = row0 + row;
+      if (nb == 0) {
+        // rows that see no key (R23): O = 0, L = -inf; no MMA work was scheduled
+        if (grow < sq.nq) {
+          uint4* dst = reinterpret_cast<uint4*>(
+              reinterpret_cast<uint8_t*>(p.o) + (sq.bc * p.o_bs + (bh % p.H) * p.o_hs + (sq.q0 + grow) * p.o_rs) * 2);
+#pragma unroll
+          for (int e = 0; e < D / 8; ++e) dst[e] = make_uint4(0u, 0u, 0u, 0u);
+          p.lse[sq.bc * p.l_bs + (bh % p.H) * p.l_hs + sq.q0 + grow] = -INFINITY;
+        }
+        continue;
+      }
       float m_used = -INFINITY;   // running max in log2 units (may lag the true max by <= 8)
       float l_sum = 0.f;
       for (int j = 0; j < nb; ++j) {
@@ -202,9 +217,9 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 #pragma unroll
         for (int c = 0; c < 128; ++c) s[c] = __uint_as_float(su[c]);
         const int c0 = j * 128;
-        const bool need_mask = (c0 + 128 > N) || (CAUSAL && (c0 + 127 > row0));
+        const bool need_mask = (c0 + 128 > sq.nk) || (CAUSAL && (c0 + 127 > row0 + sq.off));
         if (need_mask) {
-          const int lim = CAUSAL ? min(N - 1, grow) : (N - 1);
+          const int lim = CAUSAL ? min(sq.nk - 1, grow + sq.off) : (sq.nk - 1);
 #pragma unroll
           for (int c = 0; c < 128; ++c)
             if (c0 + c > lim) s[c] = -INFINITY;
@@ -280,8 +295,10 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       // ---- epilogue: O = O / l, L = m + log l (natural log) ----
       ptx::mbar_wait(&o_done[wg], (pv_count - 1) & 1);
       ptx::tc_fence_after();
-      const float inv_l = 1.f / l_sum;
-      uint8_t* orow = reinterpret_cast<uint8_t*>(p.o) + (static_cast<size_t>(bh) * N + grow) * (D * 2);
+      const float inv_l = l_sum > 0.f ? 1.f / l_sum : 0.f;   // rows that saw no key: O = 0 (R23)
+      uint8_t* orow = reinterpret_cast<uint8_t*>(p.o) +
+                      (GEN ? (sq.bc * p.o_bs + (bh % p.H) * p.o_hs + (sq.q0 + grow) * p.o_rs)
+                           : (static_cast<size_t>(bh) * sq.nq + grow) * D) * 2;
 #pragma unroll
       for (int ch = 0; ch < D / 32; ++ch) {
         uint32_t o[32];
@@ -291,13 +308,14 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 #pragma unroll
         for (int e = 0; e < 16; ++e)
           pk[e] = ptx::pack2<BF16>(__uint_as_float(o[2 * e]) * inv_l, __uint_as_float(o[2 * e + 1]) * inv_l);
-        if (grow < N) {
+        if (grow < sq.nq) {
           uint4* dst = reinterpret_cast<uint4*>(orow + ch * 64);
 #pragma unroll
           for (int e = 0; e < 4; ++e) dst[e] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
         }
       }
-      if (grow < N) p.lse[static_cast<size_t>(bh) * N + grow] = (m_used + ptx::lg2(l_sum)) * 0.69314718055994531f;
+      if (grow < sq.nq)
+        p.lse[GEN ? sq.bc * p.l_bs + (bh % p.H) * p.l_hs + sq.q0 + grow : static_cast<size_t>(bh) * sq.nq + grow] = l_sum > 0.f ? (m_used + ptx::lg2(l_sum)) * 0.69314718055994531f : -INFINITY;
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&o_empty[wg]);
@@ -341,8 +359,9 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       };
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
         int bh, mb;
-        decode(t, bh, mb);
-        const int nb0 = n_blocks(mb, 0), nb1 = n_blocks(mb, 1);
+        Seq sq;
+        decode(t, bh, mb, sq);
+        const int nb0 = n_blocks(sq, mb, 0), nb1 = n_blocks(sq, mb, 1);
         const int nkv = max(nb0, nb1);
         ptx::mbar_wait(&q_full[0], it & 1);
         ptx::mbar_wait(&q_full[1], it & 1);
@@ -448,26 +467,30 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       const uint64_t pol_q = ptx::l2_policy_evict_first();
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
         int bh, mb;
-        decode(t, bh, mb);
-        const int nkv = max(n_blocks(mb, 0), n_blocks(mb, 1));
+        Seq sq;
+        decode(t, bh, mb, sq);
+        const int nkv = max(n_blocks(sq, mb, 0), n_blocks(sq, mb, 1));
         // key/value head of this query head: implicit index manipulation
-        const int kvh = (bh / p.H) * p.Hkv + (bh % p.H) / p.group;
+        const int h = bh % p.H, kvh = h / p.group;
         for (int i = 0; i < 2; ++i) {
           if (it > 0) ptx::mbar_wait(&q_empty[i], (it - 1) & 1);
           ptx::mbar_arrive_expect_tx(&q_full[i], L::TILE);
           for (int s = 0; s < NSUB; ++s)
-            ptx::tma_load_3d_hint(sQ + i * L::TILE + s * L::SUB, &tm_q, &q_full[i], s * 64, mb * 256 + i * 128, bh, pol_q);
+            tma_load_rows<GEN>(sQ + i * L::TILE + s * L::SUB, &tm_q, &q_full[i], p.geom, s * 64, sq.q0 + mb * 256 + i * 128,
+                          h, sq.bc, p.H, pol_q);
         }
         for (int j = 0; j < nkv; ++j) {
           ptx::mbar_wait(&k_empty[kslot], kphase ^ 1);
           ptx::mbar_arrive_expect_tx(&k_full[kslot], L::TILE);
           for (int s = 0; s < NSUB; ++s)
-            ptx::tma_load_3d_hint(sK + kslot * L::TILE + s * L::SUB, &tm_k, &k_full[kslot], s * 64, j * 128, kvh, pol_kv);
+            tma_load_rows<GEN>(sK + kslot * L::TILE + s * L::SUB, &tm_k, &k_full[kslot], p.geom, s * 64, sq.k0 + j * 128,
+                          kvh, sq.bc, p.Hkv, pol_kv);
           if (++kslot == STAGES) { kslot = 0; kphase ^= 1; }
           ptx::mbar_wait(&v_empty[vslot], vphase ^ 1);
           ptx::mbar_arrive_expect_tx(&v_full[vslot], L::TILE);
           for (int s = 0; s < NSUB; ++s)
-            ptx::tma_load_3d_hint(sV + vslot * L::TILE + s * L::SUB, &tm_v, &v_full[vslot], s * 64, j * 128, kvh, pol_kv);
+            tma_load_rows<GEN>(sV + vslot * L::TILE + s * L::SUB, &tm_v, &v_full[vslot], p.geom, s * 64, sq.k0 + j * 128,
+                          kvh, sq.bc, p.Hkv, pol_kv);
           if (++vslot == STAGES) { vslot = 0; vphase ^= 1; }
         }
       }

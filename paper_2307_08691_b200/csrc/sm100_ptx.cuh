@@ -131,9 +131,22 @@ FA2_DEVICE void tma_load_3d_hint(void* smem_dst, const CUtensorMap* d, uint64_t*
       :: "r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(d)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+FA2_DEVICE void tma_load_4d_hint(void* smem_dst, const CUtensorMap* d, uint64_t* bar, int c0, int c1, int c2, int c3,
+                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;"
+      :: "r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(d)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+         "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
 FA2_DEVICE void tma_store_3d(const CUtensorMap* d, const void* smem_src, int c0, int c1, int c2) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];"
                :: "l"(reinterpret_cast<uint64_t>(d)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(smem_src)) : "memory");
+}
+FA2_DEVICE void tma_reduce_add_2d(const CUtensorMap* d, const void* smem_src, int c0, int c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];"
+               :: "l"(reinterpret_cast<uint64_t>(d)), "r"(c0), "r"(c1), "r"(smem_u32(smem_src)) : "memory");
 }
 FA2_DEVICE void tma_reduce_add_3d(const CUtensorMap* d, const void* smem_src, int c0, int c1, int c2) {
   asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];"

@@ -143,3 +143,30 @@ def test_gqa_validation(L):
     assert L.fa2_backward_deterministic(*p[:9], ws, 1 << 30, 1, 8, 2, 128, 64, 1, 0.125, 0, None) in (2, 4)
     # valid GQA arguments reach CUDA (no device here)
     assert L.fa2_forward_gqa(p[0], p[1], p[2], p[3], p[4], 1, 8, 2, 128, 64, 1, 0.125, 0, None) in (2, 4)
+
+
+def test_rectangular_and_varlen_validation(L):
+    p = FAKE
+    cu = ctypes.c_void_p(4096)
+    # N_k < 1
+    assert L.fa2_forward_ex(p[0], p[1], p[2], p[3], p[4], 1, 2, 2, 128, 0, 64, 0, 0.125, 0, None) == 1
+    # valid rectangular arguments reach CUDA
+    assert L.fa2_forward_ex(p[0], p[1], p[2], p[3], p[4], 1, 2, 1, 100, 300, 64, 1, 0.125, 0, None) in (2, 4)
+    vl = lambda *a: L.fa2_forward_varlen(p[0], p[1], p[2], p[3], p[4], *a)
+    assert vl(None, cu, 2, 4, 2, 100, 100, 60, 60, 64, 0, 0.125, 0, None) == 1          # NULL cu_seqlens
+    assert vl(ctypes.c_void_p(4097), cu, 2, 4, 2, 100, 100, 60, 60, 64, 0, 0.125, 0, None) == 1   # misaligned
+    assert vl(cu, cu, 2, 4, 3, 100, 100, 60, 60, 64, 0, 0.125, 0, None) == 1            # H % H_kv
+    assert vl(cu, cu, 2, 4, 2, 0, 100, 60, 60, 64, 0, 0.125, 0, None) == 1              # total_q < 1
+    assert vl(cu, cu, 2, 4, 2, 100, 100, 101, 60, 64, 0, 0.125, 0, None) == 1           # max > total
+    assert vl(cu, cu, 2, 4, 2, 100, 100, 60, 60, 96, 0, 0.125, 0, None) == 2            # d
+    assert vl(cu, cu, 2, 4, 2, 100, 100, 60, 60, 64, 1, 0.125, 0, None) in (2, 4)       # valid
+    # varlen workspace: padded rows H * pad128(T_q + 127 B), dq_acc + D + L2 + counters + tile offsets
+    B, H, T, d = 3, 4, 1000, 64
+    rows = H * (-(-(T + 127 * B) // 128) * 128)
+    r16 = lambda x: (x + 15) // 16 * 16
+    want = rows * d * 4 + 2 * rows * 4 + r16(rows // 128 * 4) + r16((B + 1) * 4)
+    assert L.fa2_backward_varlen_workspace_size(B, H, T, d) == want
+    ws = ctypes.c_void_p(1 << 20)
+    bv = lambda nbytes, *a: L.fa2_backward_varlen(*p[:9], cu, cu, ws, nbytes, *a)
+    assert bv(want - 1, B, H, 2, T, T, 500, 500, d, 0, 0.125, 0, 0, None) == 3
+    assert bv(want, B, H, 2, T, T, 500, 500, d, 0, 0.125, 0, 0, None) in (2, 4)

@@ -5,6 +5,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 CHILD = r'''
 import json, math, sys, torch
 import paper_2307_08691_b200 as fa2
+sys.stderr.write(fa2.__file__ + "\n")
 res = {}
 for (d, H) in ((128, 16), (64, 32)):
     for causal in (False, True):
@@ -38,7 +39,13 @@ if __name__ == "__main__":
     for lib in sys.argv[1:]:
         if lib == "bwd":
             continue
-        env = dict(os.environ, FA2_LIB_PATH=os.path.abspath(lib))
-        r = subprocess.run([sys.executable, "-c", CHILD] + (["bwd"] if "bwd" in sys.argv else []), env=env, capture_output=True, text=True, timeout=600)
+        if os.path.isdir(lib):   # a checkout: use its own binding and library (A/B across API changes)
+            env = dict(os.environ, PYTHONPATH=os.path.abspath(lib))
+            env.pop("FA2_LIB_PATH", None)
+        else:
+            env = dict(os.environ, FA2_LIB_PATH=os.path.abspath(lib))
+        r = subprocess.run([sys.executable, "-c", CHILD] + (["bwd"] if "bwd" in sys.argv else []), env=env,
+                           cwd=os.path.abspath(lib) if os.path.isdir(lib) else None, capture_output=True, text=True,
+                           timeout=600)
         out[os.path.basename(lib)] = json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else r.stderr[-2000:]
         print(os.path.basename(lib), out[os.path.basename(lib)], flush=True)
