@@ -1,6 +1,6 @@
 """Benchmark of the B200 FlashAttention-2 hot path (fwd + bwd step).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--sweep]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--sweep] [--extras]
 
 Under torchrun (N > 1) each rank runs the same per-GPU workload (weak scaling
 over batch x heads, no collective in the data path); the step time is the max
@@ -307,6 +307,8 @@ def run_ours(args, world, rank, local):
         out["cpu_baseline"] = cpu_baseline(cfg, budget_s=args.cpu_budget)
     if args.sweep and rank == 0:
         out["sweep"] = run_sweep(fa2, dev)
+    if args.extras and rank == 0:
+        out["extras"] = run_extras(fa2, dev)
     return out
 
 
@@ -373,6 +375,85 @@ def run_sweep(fa2, dev):
     return res
 
 
+def _tm(fn, reps=10):
+    import torch
+    for _ in range(3):
+        fn()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / reps
+
+
+def run_extras(fa2, dev):
+    """SURVEY §8f rows beyond the square MHA path, timed like the sweep (device events,
+    inputs resident): MQA/GQA, the deterministic backward, N_q != N_k (chunked-prefill
+    shape, bottom-right causal) and a packed variable-length batch.  FLOPs: the paper's
+    count 4*N_q*N_k*d per (b, h) (x2.5 for the backward); causal rectangular shapes count
+    the exact visible entries, causal square sequences /2 as in the paper."""
+    import torch
+    res = []
+    mk = lambda *shape: torch.randn(*shape, device=dev, dtype=torch.bfloat16)
+    # MQA / GQA: Llama-style 32 query heads on 8 (and 1) key/value heads
+    for hkv in (8, 1):
+        for causal in (False, True):
+            B, H, N, d = 2, 32, 8192, 128
+            q, do = mk(B, H, N, d), mk(B, H, N, d)
+            k, v = mk(B, hkv, N, d), mk(B, hkv, N, d)
+            o, lse = fa2.forward(q, k, v, causal=causal)
+            ws = torch.empty(fa2.backward_workspace_size(B, H, N, d), dtype=torch.uint8, device=dev)
+            t_f = _tm(lambda: fa2.forward(q, k, v, causal=causal, out=o, lse=lse))
+            t_b = _tm(lambda: fa2.backward(q, k, v, o, lse, do, causal=causal, workspace=ws))
+            res.append({"case": f"gqa H={H} H_kv={hkv}", "B": B, "N": N, "d": d, "causal": causal,
+                        "fwd_tflops": round(flops(B, H, N, d, causal, "fwd") / t_f / 1e9, 1),
+                        "bwd_tflops": round(flops(B, H, N, d, causal, "bwd") / t_b / 1e9, 1)})
+    # deterministic backward vs arrival-order backward
+    for d, H in ((128, 16), (64, 32)):
+        for causal in (False, True):
+            B, N = 2, 8192
+            q, k, v, do = mk(B, H, N, d), mk(B, H, N, d), mk(B, H, N, d), mk(B, H, N, d)
+            o, lse = fa2.forward(q, k, v, causal=causal)
+            ws = torch.empty(fa2.backward_workspace_size(B, H, N, d), dtype=torch.uint8, device=dev)
+            t_a = _tm(lambda: fa2.backward(q, k, v, o, lse, do, causal=causal, workspace=ws))
+            t_d = _tm(lambda: fa2.backward(q, k, v, o, lse, do, causal=causal, workspace=ws, deterministic=True))
+            res.append({"case": "deterministic bwd", "B": B, "H": H, "N": N, "d": d, "causal": causal,
+                        "bwd_tflops": round(flops(B, H, N, d, causal, "bwd") / t_a / 1e9, 1),
+                        "bwd_deterministic_tflops": round(flops(B, H, N, d, causal, "bwd") / t_d / 1e9, 1)})
+    # N_q != N_k: a 2048-row chunk attending to 8192 keys (bottom-right causal, R22)
+    for causal in (False, True):
+        B, H, Nq, Nk, d = 4, 16, 2048, 8192, 128
+        q, do = mk(B, H, Nq, d), mk(B, H, Nq, d)
+        k, v = mk(B, H, Nk, d), mk(B, H, Nk, d)
+        o, lse = fa2.forward(q, k, v, causal=causal)
+        ws = torch.empty(fa2.backward_workspace_size(B, H, Nq, d), dtype=torch.uint8, device=dev)
+        t_f = _tm(lambda: fa2.forward(q, k, v, causal=causal, out=o, lse=lse))
+        t_b = _tm(lambda: fa2.backward(q, k, v, o, lse, do, causal=causal, workspace=ws))
+        vis = Nq * (Nk - Nq + 1) + Nq * (Nq - 1) / 2 if causal else Nq * Nk
+        fl = 4.0 * d * H * B * vis
+        res.append({"case": "N_q != N_k", "B": B, "H": H, "N_q": Nq, "N_k": Nk, "d": d, "causal": causal,
+                    "fwd_tflops": round(fl / t_f / 1e9, 1), "bwd_tflops": round(2.5 * fl / t_b / 1e9, 1)})
+    # packed variable-length batch: 32 sequences, lengths uniform in [512, 8192] (seeded)
+    g = torch.Generator().manual_seed(11)
+    lens = torch.randint(512, 8193, (32,), generator=g).tolist()
+    cu = torch.tensor([0] + list(__import__("itertools").accumulate(lens)), dtype=torch.int32, device=dev)
+    T, H, d = cu[-1].item(), 16, 128
+    for causal in (False, True):
+        q, k, v, do = mk(T, H, d), mk(T, H, d), mk(T, H, d), mk(T, H, d)
+        o, lse = fa2.forward_varlen(q, k, v, cu, cu, max(lens), max(lens), causal=causal)
+        ws = torch.empty(fa2.backward_varlen_workspace_size(len(lens), H, T, d), dtype=torch.uint8, device=dev)
+        t_f = _tm(lambda: fa2.forward_varlen(q, k, v, cu, cu, max(lens), max(lens), causal=causal, out=o, lse=lse))
+        t_b = _tm(lambda: fa2.backward_varlen(q, k, v, o, lse, do, cu, cu, max(lens), max(lens), causal=causal,
+                                              workspace=ws))
+        fl = sum(4.0 * n * n * d * H / (2 if causal else 1) for n in lens)
+        res.append({"case": "varlen", "sequences": len(lens), "total_tokens": T, "min_len": min(lens),
+                    "max_len": max(lens), "H": H, "d": d, "causal": causal,
+                    "fwd_tflops": round(fl / t_f / 1e9, 1), "bwd_tflops": round(2.5 * fl / t_b / 1e9, 1)})
+    return res
+
+
 # ---------------------------------------------------------------------------
 # reference arm: the CPU fp64 oracle on the host cores
 # ---------------------------------------------------------------------------
@@ -414,6 +495,7 @@ def main():
     ap.add_argument("--head-dim", type=int, default=128)
     ap.add_argument("--causal", type=int, default=0)
     ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--extras", action="store_true", help="also time GQA, deterministic bwd, N_q != N_k, varlen")
     ap.add_argument("--strong", action="store_true", help="split the global B*H over ranks instead of replicating")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
