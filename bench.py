@@ -435,6 +435,14 @@ def run_extras(fa2, dev):
         fl = 4.0 * d * H * B * vis
         res.append({"case": "N_q != N_k", "B": B, "H": H, "N_q": Nq, "N_k": Nk, "d": d, "causal": causal,
                     "fwd_tflops": round(fl / t_f / 1e9, 1), "bwd_tflops": round(2.5 * fl / t_b / 1e9, 1)})
+    # FP8 forward: E4M3 q, k, v (per-tensor descale 1), bf16 O
+    for causal in (False, True):
+        B, H, N, d = 2, 16, 8192, 128
+        q8, k8, v8 = (mk(B, H, N, d).to(torch.float8_e4m3fn) for _ in range(3))
+        o, lse = fa2.forward_fp8(q8, k8, v8, causal=causal)
+        t_f = _tm(lambda: fa2.forward_fp8(q8, k8, v8, causal=causal, out=o, lse=lse))
+        res.append({"case": "fp8 forward (E4M3 in, bf16 out)", "B": B, "H": H, "N": N, "d": d, "causal": causal,
+                    "fwd_tflops": round(flops(B, H, N, d, causal, "fwd") / t_f / 1e9, 1)})
     # packed variable-length batch: 32 sequences, lengths uniform in [512, 8192] (seeded)
     g = torch.Generator().manual_seed(11)
     lens = torch.randint(512, 8193, (32,), generator=g).tolist()

@@ -125,6 +125,21 @@ FA2_API fa2_status_t fa2_forward_varlen(const void* q, const void* k, const void
                                         int total_q, int total_k, int max_seqlen_q, int max_seqlen_k, int d,
                                         int causal, float softmax_scale, fa2_dtype_t dtype, void* stream);
 
+/* FP8 forward (the paper lists FP8 as future work).
+ * q [B,H,N,d], k, v [B,H_kv,N,d] are float8 E4M3 (1 byte per element, the same
+ * contiguous layouts as fa2_forward_gqa); the represented values are
+ * descale_q * q, descale_k * k, descale_v * v (per-tensor fp32 factors, finite
+ * and > 0).  Computes the same O and lse as fa2_forward_gqa on those values:
+ * S = softmax_scale * (descale_q q)(descale_k k)^T is accumulated exactly in fp32
+ * (E4M3 products are exact), the online softmax runs in fp32, and P~ is rounded
+ * to E4M3 for the P~V product (R25: relative error <= 2^-4 per P~
+ * entry); l sums the fp32 P~.  o is written as bf16 [B,H,N,d], lse fp32
+ * [B,H,N].  d = 128 only (FA2_ERR_UNSUPPORTED otherwise).  There is no FP8
+ * backward. */
+FA2_API fa2_status_t fa2_forward_fp8(const void* q, const void* k, const void* v, void* o, float* lse,
+                                     int B, int H, int H_kv, int N, int d, int causal, float softmax_scale,
+                                     float descale_q, float descale_k, float descale_v, void* stream);
+
 /* Deterministic backward.  Same arguments, layouts, workspace and
  * errors as fa2_backward_gqa (H_kv == H for plain multi-head attention); the
  * result is bitwise reproducible from run to run on the same device and

@@ -11,7 +11,7 @@ import ctypes
 import math
 import os
 
-__all__ = ["lib", "forward", "backward", "forward_varlen", "backward_varlen", "backward_varlen_workspace_size",
+__all__ = ["lib", "forward", "backward", "forward_fp8", "forward_varlen", "backward_varlen", "backward_varlen_workspace_size",
            "backward_preprocess", "backward_workspace_size",
            "attention_step_host", "step_arena_size", "kv_block_range", "set_timing_events", "FA2Error", "LIB_PATH"]
 
@@ -52,6 +52,8 @@ def lib() -> ctypes.CDLL:
         L.fa2_forward_ex.restype = i
         L.fa2_forward_varlen.argtypes = [vp, vp, vp, vp, vp, vp, vp, i, i, i, i, i, i, i, i, i, f, i, vp]
         L.fa2_forward_varlen.restype = i
+        L.fa2_forward_fp8.argtypes = [vp, vp, vp, vp, vp, i, i, i, i, i, i, f, f, f, f, vp]
+        L.fa2_forward_fp8.restype = i
         L.fa2_backward_ex.argtypes = [vp] * 10 + [sz, i, i, i, i, i, i, i, f, i, i, vp]
         L.fa2_backward_ex.restype = i
         L.fa2_backward_varlen.argtypes = [vp] * 11 + [vp, sz, i, i, i, i, i, i, i, i, i, f, i, i, vp]
@@ -191,6 +193,26 @@ def backward(q, k, v, o, lse, do, causal: bool = False, softmax_scale: float | N
         _check(lib().fa2_backward_ex(*args, B, H, Hkv, N, Nk, d, int(bool(causal)), scale, int(bool(deterministic)),
                                      _dtype_code(q), st))
     return dq, dk, dv
+
+
+def forward_fp8(q, k, v, descale_q: float = 1.0, descale_k: float = 1.0, descale_v: float = 1.0,
+                causal: bool = False, softmax_scale: float | None = None, out=None, lse=None, stream=None):
+    """FP8 forward (fa2_forward_fp8): q [B,H,N,128], k/v [B,H_kv,N,128] torch.float8_e4m3fn
+    CUDA tensors representing descale_x * x.  Returns (o [B,H,N,128] bf16, lse [B,H,N] fp32)."""
+    import torch
+    B, H, N, d = _shape(q)
+    for t, n in ((q, "q"), (k, "k"), (v, "v")):
+        if t.dtype != torch.float8_e4m3fn:
+            raise FA2Error(1, f"{n} must be torch.float8_e4m3fn")
+    Hkv, Nk = _kv_check(q, k, v)
+    if Nk != N or not q.is_contiguous():
+        raise FA2Error(1, "FP8 forward: contiguous q, and k/v with N_k == N_q")
+    scale = 1.0 / math.sqrt(d) if softmax_scale is None else float(softmax_scale)
+    o = torch.empty((B, H, N, d), dtype=torch.bfloat16, device=q.device) if out is None else out
+    L = torch.empty((B, H, N), dtype=torch.float32, device=q.device) if lse is None else lse
+    _check(lib().fa2_forward_fp8(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(L), B, H, Hkv, N, d, int(bool(causal)), scale,
+                                 float(descale_q), float(descale_k), float(descale_v), ctypes.c_void_p(_stream(stream))))
+    return o, L
 
 
 def _varlen_check(q, k, v, cu_q, cu_k):

@@ -134,22 +134,23 @@ Geom fixed_geom(int B, int H, int Hkv, int Nq, int Nk, int d) {
 // 3-D row-tile map in memory order (fa2_seq.cuh): fixed {d, N, B*heads}, packed
 // {d, heads, T}; box = 64 columns x 128 rows of one head.
 fa2_status_t make_rows_map(CUtensorMap* m, const void* base, CUtensorMapDataType dt, const Geom& g, int heads,
-                           bool is_q) {
+                           bool is_q, int elem_bytes = 2) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return fail(FA2_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
-  const cuuint64_t d = static_cast<cuuint64_t>(g.d), eb = 2;
+  const cuuint64_t d = static_cast<cuuint64_t>(g.d), eb = static_cast<cuuint64_t>(elem_bytes);
+  const cuuint32_t box_cols = static_cast<cuuint32_t>(128 / elem_bytes);   // one 128-B swizzle row
   cuuint64_t dims[3], strides[2];
   cuuint32_t box[3];
   if (!g.packed) {
     const cuuint64_t n = static_cast<cuuint64_t>(is_q ? g.Nq : g.Nk);
     dims[0] = d; dims[1] = n; dims[2] = static_cast<cuuint64_t>(heads) * static_cast<cuuint64_t>(g.B);
     strides[0] = d * eb; strides[1] = n * d * eb;
-    box[0] = 64; box[1] = 128; box[2] = 1;
+    box[0] = box_cols; box[1] = 128; box[2] = 1;
   } else {
     const cuuint64_t t = static_cast<cuuint64_t>(std::max(1, is_q ? g.Tq : g.Tk));
     dims[0] = d; dims[1] = static_cast<cuuint64_t>(heads); dims[2] = t;
     strides[0] = d * eb; strides[1] = static_cast<cuuint64_t>(heads) * d * eb;
-    box[0] = 64; box[1] = 1; box[2] = 128;
+    box[0] = box_cols; box[1] = 1; box[2] = 128;
   }
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -197,11 +198,11 @@ fa2_status_t set_smem(K kernel, int bytes) {
 // ----------------------------------------------------------------------------
 // Forward
 // ----------------------------------------------------------------------------
-template <int D, bool BF16, bool CAUSAL, bool GEN>
+template <int D, bool BF16, bool CAUSAL, bool GEN, bool FP8 = false>
 fa2_status_t launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const fa2::FwdParams& p,
                         int sms, cudaStream_t st) {
-  auto kern = fa2::fa2_fwd_kernel<D, BF16, CAUSAL, GEN>;
-  constexpr int smem = fa2::FwdSmem<D>::ALLOC;
+  auto kern = fa2::fa2_fwd_kernel<D, BF16, CAUSAL, GEN, FP8>;
+  constexpr int smem = fa2::FwdSmem<D, FP8 ? 1 : 2>::ALLOC;
   fa2_status_t s = set_smem(kern, smem);
   if (s != FA2_OK) return s;
   const int grid = p.num_tiles < sms ? p.num_tiles : sms;
@@ -259,6 +260,35 @@ fa2_status_t forward_impl(const void* q, const void* k, const void* v, void* o, 
     s = bf16 ? dispatch_fwd_causal<128, true>(causal, mq, mk, mv, p, sms, st)
              : dispatch_fwd_causal<128, false>(causal, mq, mk, mv, p, sms, st);
   return s;
+}
+
+// FP8 forward: E4M3 q, k, v with per-tensor descales, bf16 O.
+fa2_status_t forward_fp8_impl(const void* q, const void* k, const void* v, void* o, float* lse, const Geom& g,
+                              int causal, float scale, float dq, float dk, float dv, cudaStream_t st, int sms) {
+  CUtensorMap mq, mk, mv;
+  fa2_status_t s;
+  if ((s = make_rows_map(&mq, q, CU_TENSOR_MAP_DATA_TYPE_UINT8, g, g.H, true, 1)) != FA2_OK) return s;
+  if ((s = make_rows_map(&mk, k, CU_TENSOR_MAP_DATA_TYPE_UINT8, g, g.Hkv, false, 1)) != FA2_OK) return s;
+  if ((s = make_rows_map(&mv, v, CU_TENSOR_MAP_DATA_TYPE_UINT8, g, g.Hkv, false, 1)) != FA2_OK) return s;
+  fa2::FwdParams p;
+  p.o = o;
+  p.lse = lse;
+  p.BH = g.B * g.H;
+  p.H = g.H;
+  p.Hkv = g.Hkv;
+  p.group = g.H / g.Hkv;
+  p.geom = seq_geom(g);
+  const long long d = g.d;
+  p.o_rs = d; p.o_hs = static_cast<long long>(g.Nq) * d; p.o_bs = p.o_hs * g.H;
+  p.l_hs = g.Nq; p.l_bs = static_cast<long long>(g.Nq) * g.H;
+  p.num_m_blocks = (g.Nq + 255) / 256;
+  p.num_tiles = p.BH * p.num_m_blocks;
+  // S = scale * (descale_q q8) . (descale_k k8): fold the descales into the exponent scale
+  p.scale_log2 = static_cast<float>(static_cast<double>(scale) * dq * dk * 1.4426950408889634);
+  p.o_descale = dv;
+  p.trace = g_trace;
+  return causal ? launch_fwd<128, true, true, false, true>(mq, mk, mv, p, sms, st)
+                : launch_fwd<128, true, false, false, true>(mq, mk, mv, p, sms, st);
 }
 
 // ----------------------------------------------------------------------------
@@ -553,6 +583,25 @@ fa2_status_t fa2_forward_varlen(const void* q, const void* k, const void* v, voi
   DeviceInfo di;
   if ((s = device_info(di)) != FA2_OK) return s;
   s = forward_impl(q, k, v, o, lse, g, causal, softmax_scale, dtype, static_cast<cudaStream_t>(stream), di.sms);
+  if (s == FA2_OK) g_launches = 1;
+  return s;
+}
+
+fa2_status_t fa2_forward_fp8(const void* q, const void* k, const void* v, void* o, float* lse, int B, int H, int H_kv,
+                             int N, int d, int causal, float softmax_scale, float descale_q, float descale_k,
+                             float descale_v, void* stream) {
+  g_detail.clear();
+  fa2_status_t s = check_common(B, H, N, d, softmax_scale, FA2_BF16, true);
+  if (s != FA2_OK) return s;
+  if (d != 128) return fail(FA2_ERR_UNSUPPORTED, "FP8 forward supports d = 128 (got %d)", d);
+  if (H_kv < 1 || H % H_kv != 0) return fail(FA2_ERR_INVALID_ARG, "H=%d must be a positive multiple of H_kv=%d", H, H_kv);
+  for (float x : {descale_q, descale_k, descale_v})
+    if (!(std::isfinite(x) && x > 0.f)) return fail(FA2_ERR_INVALID_ARG, "descale factors must be finite and > 0");
+  if ((s = check_ptrs({q, k, v, o, lse})) != FA2_OK) return s;
+  DeviceInfo di;
+  if ((s = device_info(di)) != FA2_OK) return s;
+  s = forward_fp8_impl(q, k, v, o, lse, fixed_geom(B, H, H_kv, N, N, d), causal, softmax_scale, descale_q, descale_k,
+                       descale_v, static_cast<cudaStream_t>(stream), di.sms);
   if (s == FA2_OK) g_launches = 1;
   return s;
 }

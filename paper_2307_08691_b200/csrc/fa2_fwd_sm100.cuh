@@ -52,7 +52,8 @@ struct FwdParams {
   long long l_bs, l_hs;         // L strides: batch, head (row stride 1)
   int num_m_blocks;    // ceil(N_q (max) / 256)
   int num_tiles;       // BH * num_m_blocks
-  float scale_log2;    // softmax_scale * log2(e)
+  float scale_log2;    // softmax_scale * log2(e)  (FP8: times descale_q * descale_k)
+  float o_descale;     // FP8: descale_v, applied with 1/l in the epilogue (unused otherwise)
   unsigned long long* trace;  // optional clock64 trace (CTA 0, first tile), nullptr in production
 };
 
@@ -64,12 +65,12 @@ struct FwdParams {
       p.trace[((ev) * 2 + (who)) * 64 + (j)] = clock64();                              \
   } while (0)
 
-template <int D>
+template <int D, int EB = 2>   // EB: bytes per Q/K/V element (2: bf16/fp16, 1: FP8)
 struct FwdSmem {
   static constexpr int BM = 128, BN = 128;
-  static constexpr int STAGES = (D == 64) ? 3 : 2;
-  static constexpr int TILE = 128 * D * 2;       // bytes of one 128 x D tile
-  static constexpr int SUB = 128 * 128;          // one 128-row x 64-col swizzle box (16 KB)
+  static constexpr int STAGES = (D == 64 || EB == 1) ? 3 : 2;
+  static constexpr int TILE = 128 * D * EB;      // bytes of one 128 x D tile
+  static constexpr int SUB = 128 * 128;          // one 128-row x 128-B swizzle box (16 KB)
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + 2 * TILE;
   static constexpr int OFF_V = OFF_K + STAGES * TILE;
@@ -81,13 +82,17 @@ struct FwdSmem {
   static constexpr int ALLOC = BYTES + 1024;   // slack for 1024-B alignment
 };
 
-template <int D, bool BF16, bool CAUSAL, bool GEN>
+// FP8: Q, K, V in E4M3 (kind::f8f6f4 MMAs, K = 32 per instruction),
+// P~ quantized to E4M3 for the P~V MMA (P~ <= 2^8 under the lazy rescale, inside E4M3's
+// 448), O written as bf16 (BF16 == true); d = 128 only (one 128-B swizzle atom per row).
+template <int D, bool BF16, bool CAUSAL, bool GEN, bool FP8 = false>
 __global__ void __launch_bounds__(384, 1)
 fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
-  using L = FwdSmem<D>;
+  static_assert(!FP8 || (D == 128 && BF16), "FP8 forward: d = 128, bf16 output");
+  using L = FwdSmem<D, FP8 ? 1 : 2>;
   constexpr int STAGES = L::STAGES;
-  constexpr int NSUB = D / 64;
+  constexpr int NSUB = D * (FP8 ? 1 : 2) / 128;   // 128-B swizzle boxes per tile row
   constexpr bool SEP_P = (D == 64);   // P~ in its own TMEM columns (fits only at d = 64)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -261,9 +266,15 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
                 pr.y = ptx::ex2(x.y);
               }
               rs2 = ptx::fadd2(rs2, pr);
-              pk[e] = ptx::pack2<BF16>(pr.x, pr.y);
+              if constexpr (FP8) {   // 4 E4M3 values per TMEM column
+                if (e % 2 == 0) pk[e / 2] = __float_as_uint(pr.x), pk[8 + e / 2] = __float_as_uint(pr.y);
+                else pk[e / 2] = ptx::pack4_e4m3(__uint_as_float(pk[e / 2]), __uint_as_float(pk[8 + e / 2]), pr.x, pr.y);
+              } else {
+                pk[e] = ptx::pack2<BF16>(pr.x, pr.y);
+              }
             }
-            ptx::tmem_st_x16(tP + ch * 16, pk);
+            if constexpr (FP8) ptx::tmem_st_x8(tP + ch * 8, pk);
+            else ptx::tmem_st_x16(tP + ch * 16, pk);
           }
         };
         if (need_mask) exp_block(std::integral_constant<int, 0>{});
@@ -295,7 +306,8 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       // ---- epilogue: O = O / l, L = m + log l (natural log) ----
       ptx::mbar_wait(&o_done[wg], (pv_count - 1) & 1);
       ptx::tc_fence_after();
-      const float inv_l = l_sum > 0.f ? 1.f / l_sum : 0.f;   // rows that saw no key: O = 0 (R23)
+      float inv_l = l_sum > 0.f ? 1.f / l_sum : 0.f;   // rows that saw no key: O = 0 (R23)
+      if constexpr (FP8) inv_l *= p.o_descale;
       uint8_t* orow = reinterpret_cast<uint8_t*>(p.o) +
                       (GEN ? (sq.bc * p.o_bs + (bh % p.H) * p.o_hs + (sq.q0 + grow) * p.o_rs)
                            : (static_cast<size_t>(bh) * sq.nq + grow) * D) * 2;
@@ -324,8 +336,9 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     ptx::setmaxnreg_dec<56>();
     if (warp == 8) {
       // ================== MMA issuer: whole warp, one elected lane issues ==================
-      constexpr uint32_t IDESC_S = ptx::idesc_f16(BF16, 128, 128, false, false);
-      constexpr uint32_t IDESC_O = ptx::idesc_f16(BF16, 128, D, false, true);
+      // (E4M3 has format code 0 in the kind::f8f6f4 descriptor, as F16 in kind::f16)
+      constexpr uint32_t IDESC_S = ptx::idesc_f16(FP8 ? false : BF16, 128, 128, false, false);
+      constexpr uint32_t IDESC_O = ptx::idesc_f16(FP8 ? false : BF16, 128, D, false, true);
       // base descriptors; per-MMA descriptors add (byte offset >> 4) to the start-address field
       const uint64_t dQ = ptx::sw128_desc(ptx::smem_u32(sQ), 16, 1024);
       const uint64_t dK = ptx::sw128_desc(ptx::smem_u32(sK), 16, 1024);
@@ -335,18 +348,32 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       uint32_t p_count0 = 0, p_count1 = 0, o_uses0 = 0, o_uses1 = 0;
       int it = 0;
       auto mma_s = [&](int i, int slot) {
+        // K steps of 32 bytes (16 bf16/fp16 or 32 E4M3 elements), 4 per 128-B swizzle box
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
+        for (int k = 0; k < D * (FP8 ? 1 : 2) / 32; ++k) {
           const uint32_t off = (k / 4) * L::SUB + (k % 4) * 32;
-          ptx::mma_ss(tmem + i * 128, dQ + ((i * L::TILE + off) >> 4), dK + ((slot * L::TILE + off) >> 4), IDESC_S,
-                      k > 0 ? 1u : 0u);
+          if constexpr (FP8)
+            ptx::mma_ss_f8(tmem + i * 128, dQ + ((i * L::TILE + off) >> 4), dK + ((slot * L::TILE + off) >> 4),
+                           IDESC_S, k > 0 ? 1u : 0u);
+          else
+            ptx::mma_ss(tmem + i * 128, dQ + ((i * L::TILE + off) >> 4), dK + ((slot * L::TILE + off) >> 4), IDESC_S,
+                        k > 0 ? 1u : 0u);
         }
       };
       auto mma_pv = [&](int i, int slot, bool acc) {
+        // K = 128 keys: 8 steps of 16 (P~ 16-bit: 8 TMEM columns, V rows 16 x 128 B) or
+        // 4 steps of 32 (P~ E4M3: 8 TMEM columns, V rows 32 x 128 B)
+        if constexpr (FP8) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          ptx::mma_ts(tmem + 256 + i * D, tmem + (SEP_P ? 256 + 2 * D + i * 64 : i * 128) + k * 8,
-                      dV + ((slot * L::TILE + k * 2048) >> 4), IDESC_O, (acc || k > 0) ? 1u : 0u);
+          for (int k = 0; k < 4; ++k)
+            ptx::mma_ts_f8(tmem + 256 + i * D, tmem + i * 128 + k * 8, dV + ((slot * L::TILE + k * 4096) >> 4), IDESC_O,
+                           (acc || k > 0) ? 1u : 0u);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            ptx::mma_ts(tmem + 256 + i * D, tmem + (SEP_P ? 256 + 2 * D + i * 64 : i * 128) + k * 8,
+                        dV + ((slot * L::TILE + k * 2048) >> 4), IDESC_O, (acc || k > 0) ? 1u : 0u);
+        }
       };
       uint32_t s_iss0 = 0, s_iss1 = 0;   // d = 64: S MMAs issued per sub-tile (s_consumed phases)
       // d = 64: S_i into its buffer once softmax i has read the previous S_i

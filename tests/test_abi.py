@@ -170,3 +170,12 @@ def test_rectangular_and_varlen_validation(L):
     bv = lambda nbytes, *a: L.fa2_backward_varlen(*p[:9], cu, cu, ws, nbytes, *a)
     assert bv(want - 1, B, H, 2, T, T, 500, 500, d, 0, 0.125, 0, 0, None) == 3
     assert bv(want, B, H, 2, T, T, 500, 500, d, 0, 0.125, 0, 0, None) in (2, 4)
+
+
+def test_fp8_validation(L):
+    p = FAKE
+    assert L.fa2_forward_fp8(p[0], p[1], p[2], p[3], p[4], 1, 2, 2, 128, 64, 0, 0.1, 1.0, 1.0, 1.0, None) == 2   # d
+    assert L.fa2_forward_fp8(p[0], p[1], p[2], p[3], p[4], 1, 2, 2, 128, 128, 0, 0.1, 0.0, 1.0, 1.0, None) == 1  # descale
+    assert L.fa2_forward_fp8(p[0], p[1], p[2], p[3], p[4], 1, 2, 2, 128, 128, 0, 0.1, 1.0, float("inf"), 1.0, None) == 1
+    assert L.fa2_forward_fp8(p[0], p[1], p[2], p[3], p[4], 1, 3, 2, 128, 128, 0, 0.1, 1.0, 1.0, 1.0, None) == 1  # H % H_kv
+    assert L.fa2_forward_fp8(p[0], p[1], p[2], p[3], p[4], 1, 2, 1, 128, 128, 1, 0.1, 1.0, 1.0, 1.0, None) in (2, 4)

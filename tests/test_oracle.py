@@ -640,3 +640,57 @@ def test_varlen_rejects_bad_offsets():
     for cu in ([0, 5], [1, 4], [0, 3, 2, 4], [0]):
         with pytest.raises(ValueError):
             R.forward_varlen(z, z, z, cu, [0, 4], 1.0, False)
+
+
+# --------------------------------------------------------------------------
+# FP8 (R25): the P~V rounding bound
+# --------------------------------------------------------------------------
+
+def _e4m3_round(x):
+    """Independent E4M3 round-to-nearest-even of non-negative values (max 448;
+    normals 2^-6..448 with 3 mantissa bits, subnormals in steps of 2^-9)."""
+    x = np.asarray(x, dtype=np.float64)
+    out = np.zeros_like(x)
+    nz = x > 0
+    e = np.floor(np.log2(np.where(nz, x, 1.0)))
+    e = np.maximum(e, -6)                      # below 2^-6: subnormal spacing 2^-9
+    step = 2.0 ** (e - 3)
+    out[nz] = (np.round(x[nz] / step[nz]) * step[nz])   # np.round: half to even
+    return np.minimum(out, 448.0)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_fp8_bound_matches_brute_force_and_holds(causal):
+    r = rng(140)
+    n, d = 11, 4
+    q, k, v = r.normal(size=(3, n, d))
+    sc = 0.9
+    bound = R.fp8_pv_error_bound(q, k, v, sc, causal)
+    # brute force of the formula
+    for i in range(n):
+        vis = [j for j in range(n) if not (causal and j > i)]
+        s = [float(np.float32(sc)) * float(q[i] @ k[j]) for j in vis]
+        mx = max(s)
+        e = [math.exp(x - mx) for x in s]
+        l = math.fsum(e)
+        for c in range(d):
+            want = 2 ** -4 * math.fsum(e[t] / l * abs(v[j, c]) for t, j in enumerate(vis)) + \
+                2 ** -10 / l * math.fsum(abs(v[j, c]) for j in vis)
+            assert abs(bound[i, c] - want) < 1e-14
+    # the bound holds for P~ rounded to E4M3 relative to any running max within 8 (log2) of the true max
+    o, _ = R.forward_head(q, k, v, sc, causal)
+    s_ = R.scores(q, k, sc, causal)
+    for shift in (0.0, 3.0, 8.0):   # running max below the true max by `shift` (log2 units)
+        m = np.max(s_, axis=1) - shift * math.log(2)
+        pt = np.exp(s_ - m[:, None])
+        o8 = (_e4m3_round(pt) @ v) / np.sum(pt, axis=1)[:, None]
+        assert np.all(np.abs(o8 - o) <= bound + 1e-12)
+
+
+def test_e4m3_rounding_helper():
+    """The test's E4M3 rounding against torch's float8_e4m3fn cast."""
+    import torch
+    x = np.concatenate([np.linspace(0, 2, 1001), np.exp(np.linspace(-12, 6, 500))])
+    x = x[x <= 448]
+    ref = torch.tensor(x, dtype=torch.float32).to(torch.float8_e4m3fn).double().numpy()
+    assert np.array_equal(_e4m3_round(x.astype(np.float32).astype(np.float64)), ref)
