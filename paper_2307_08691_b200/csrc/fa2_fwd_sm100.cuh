@@ -36,11 +36,17 @@
 namespace fa2 {
 
 // Column pairs (out of every 16) whose exponential runs as a polynomial on the
-// FMA pipe instead of MUFU.EX2 (unmasked blocks only).
+// FMA pipe instead of MUFU.EX2 (unmasked blocks only).  Measured best on B200
+// (tools/fwd_ms.py sweep over 2/4/6/8): 4 at d = 128 (bf16 and FP8), 6 at d = 64,
+// where the MMAs are shorter and MUFU.EX2 (16/clk/SM) binds harder.
 #ifndef FA2_FWD_EMU_PAIRS
 #define FA2_FWD_EMU_PAIRS 4
 #endif
+#ifndef FA2_FWD_EMU_PAIRS_D64
+#define FA2_FWD_EMU_PAIRS_D64 6
+#endif
 constexpr int kFwdEmuPairs = FA2_FWD_EMU_PAIRS;
+constexpr int kFwdEmuPairsD64 = FA2_FWD_EMU_PAIRS_D64;
 
 struct FwdParams {
   void* o;             // fixed: [B, H, N_q, D]; packed: [T_q, H, D] (dtype)
@@ -278,7 +284,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           }
         };
         if (need_mask) exp_block(std::integral_constant<int, 0>{});
-        else exp_block(std::integral_constant<int, kFwdEmuPairs>{});
+        else exp_block(std::integral_constant<int, D == 64 ? kFwdEmuPairsD64 : kFwdEmuPairs>{});
         l_sum = l_sum * alpha + (rs2.x + rs2.y);
         if (threadIdx.x % 128 == 0 && t == (int)blockIdx.x) FA2_TRACE(2, wg, j);
         // Rescale the un-normalised O accumulator before P~_j V_j is added
