@@ -68,7 +68,11 @@ FA2_API fa2_status_t fa2_forward(const void* q, const void* k, const void* v, vo
 /* Bytes of device scratch fa2_backward needs: the fp32 dQ accumulator
  * [B,H,N_pad,d], D [B,H,N_pad] and L*log2(e) [B,H,N_pad] (fp32), where N_pad is
  * N rounded up to a multiple of 128, plus [B,H,N_pad/128] int32 dQ-tile
- * counters (used by fa2_backward_deterministic), rounded up to 16 bytes. */
+ * counters (used by fa2_backward_deterministic), rounded up to 16 bytes -- the
+ * minimum -- plus, 256-byte aligned, 2*B*H*N*d fp32 for the GQA load-balance
+ * split (fp32 dK, dV partial sums when the query heads of a key/value group are
+ * spread over several CTAs; used only when H_kv < H, not deterministic, and the
+ * caller's workspace has the room). */
 FA2_API size_t fa2_backward_workspace_size(int B, int H, int N, int d);
 
 /* Backward pass, Alg. 2: writes dq, dk, dv ([B,H,N,d], dtype).

@@ -417,10 +417,39 @@ fa2_status_t dispatch_bwd_causal(bool causal, const fa2::BwdMaps& maps, const fa
   return causal ? launch_bwd<D, BF16, true, false>(maps, p, sms, st) : launch_bwd<D, BF16, false, false>(maps, p, sms, st);
 }
 
+// GQA load balance (BwdParams::hsplit): the query heads of a key/value group are split
+// over `hsplit` work tiles when the unsplit tile count would leave SMs idle (< 2 waves) or,
+// causal, when the heaviest tile exceeds half of an SM's average share.  Needs fp32 dK/dV
+// accumulators (2 * numel(dk) * 4 bytes) after the base workspace; not used in the
+// deterministic mode (the fp32 reduce-adds would make dK/dV order-dependent).
+int choose_hsplit(const Geom& g, bool causal, bool deterministic, int sms, size_t ws_bytes, size_t base,
+                  size_t& acc_off, long long& dk_numel) {
+  const int group = g.H / g.Hkv;
+  dk_numel = (g.packed ? static_cast<long long>(g.Tk) : static_cast<long long>(g.B) * g.Nk) * g.Hkv * g.d;
+  acc_off = (base + 255) / 256 * 256;
+  if (group == 1 || deterministic || ws_bytes < acc_off + static_cast<size_t>(dk_numel) * 8) return 1;
+  const long long nkb = (g.Nk + 127) / 128, nqb = (g.Nq + 127) / 128;
+  const long long tiles1 = static_cast<long long>(g.B) * g.Hkv * nkb;
+  long long need = (2LL * sms + tiles1 - 1) / tiles1;
+  if (causal) {   // heaviest tile (key block 0: nqb query tiles x group/split heads) <= half an SM's share
+    const long long den = (nqb + 1) * g.B * g.Hkv;
+    need = std::max(need, (4LL * sms + den - 1) / den);
+  }
+  for (int sp = 1; sp <= group; ++sp)
+    if (group % sp == 0 && sp >= need) return sp;
+  return group;
+}
+
 fa2_status_t backward_impl(const void* q, const void* k, const void* v, const void* o, const float* lse,
                            const void* dout, void* dq, void* dk, void* dv, void* ws, const Geom& g, int causal,
-                           float scale, fa2_dtype_t dtype, cudaStream_t st, int sms, bool deterministic) {
+                           float scale, fa2_dtype_t dtype, cudaStream_t st, int sms, bool deterministic,
+                           size_t ws_bytes) {
   const WsLayout wl = ws_layout(g);
+  size_t acc_off = 0;
+  long long dk_numel = 0;
+  const int hsplit = choose_hsplit(g, causal != 0, deterministic, sms, ws_bytes, wl.total, acc_off, dk_numel);
+  float* dk_acc = hsplit > 1 ? reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + acc_off) : nullptr;
+  float* dv_acc = hsplit > 1 ? dk_acc + dk_numel : nullptr;
   fa2::RowParams rp = row_params(g, wl, o, dout, dq, lse, ws);
   int* dq_sem = deterministic ? reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + wl.sem) : nullptr;
   rp.dq_sem = dq_sem;
@@ -431,6 +460,7 @@ fa2_status_t backward_impl(const void* q, const void* k, const void* v, const vo
   }
   fa2_status_t s = preprocess_impl(rp, g.d, dtype, st);
   if (s != FA2_OK) return s;
+  if (hsplit > 1) FA2_CUDA(cudaMemsetAsync(dk_acc, 0, static_cast<size_t>(dk_numel) * 8, st));
   fa2::BwdMaps maps;
   const CUtensorMapDataType dt = tma_dtype(dtype);
   if ((s = make_rows_map(&maps.q, q, dt, g, g.H, true)) != FA2_OK) return s;
@@ -449,7 +479,11 @@ fa2_status_t backward_impl(const void* q, const void* k, const void* v, const vo
   p.Hkv = g.Hkv;
   p.group = g.H / g.Hkv;
   p.num_n_blocks = (g.Nk + 127) / 128;
-  p.num_tiles = g.B * g.Hkv * p.num_n_blocks;   // one work tile per (sequence, key/value head, key block)
+  p.hsplit = hsplit;
+  p.dk_acc = dk_acc;
+  p.dv_acc = dv_acc;
+  // one work tile per (sequence, key/value head, query-head split, key block)
+  p.num_tiles = g.B * g.Hkv * hsplit * p.num_n_blocks;
   p.scale = scale;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.trace = g_trace;
@@ -474,6 +508,13 @@ fa2_status_t backward_impl(const void* q, const void* k, const void* v, const vo
     s = bf16 ? dispatch_bwd_causal<128, true>(causal, maps, p, sms, st)
              : dispatch_bwd_causal<128, false>(causal, maps, p, sms, st);
   if (s != FA2_OK) return s;
+  if (hsplit > 1) {   // dK, dV = cast(fp32 sums over the group's query-head splits)
+    const long long n8 = dk_numel / 8;
+    const long long grid = (2 * n8 + 255) / 256;
+    if (bf16) fa2::fa2_dkv_convert<true><<<static_cast<int>(grid), 256, 0, st>>>(dk_acc, dv_acc, dk, dv, n8);
+    else fa2::fa2_dkv_convert<false><<<static_cast<int>(grid), 256, 0, st>>>(dk_acc, dv_acc, dk, dv, n8);
+    FA2_CUDA(cudaGetLastError());
+  }
   // dQ = cast(dq_acc) (the softmax scale is already applied to dS), real rows only
   {
     const long long rows_out = g.packed ? static_cast<long long>(g.Tq) * g.H : static_cast<long long>(g.B) * g.H * g.Nq;
@@ -613,7 +654,8 @@ fa2_status_t fa2_forward(const void* q, const void* k, const void* v, void* o, f
 
 size_t fa2_backward_workspace_size(int B, int H, int N, int d) {
   if (B < 1 || H < 1 || N < 1 || (d != 64 && d != 128)) return 0;
-  return ws_layout(fixed_geom(B, H, H, N, N, d)).total;
+  // base layout + room for the GQA split's fp32 dK/dV accumulators (H_kv <= H, N_k = N)
+  return (ws_layout(fixed_geom(B, H, H, N, N, d)).total + 255) / 256 * 256 + static_cast<size_t>(B) * H * N * d * 8;
 }
 
 fa2_status_t fa2_backward(const void* q, const void* k, const void* v, const void* o, const float* lse,
@@ -656,7 +698,8 @@ size_t fa2_backward_varlen_workspace_size(int B, int H, int total_q, int d) {
   if (B < 1 || H < 1 || total_q < 1 || (d != 64 && d != 128)) return 0;
   Geom g;
   g.B = B; g.H = H; g.Hkv = H; g.d = d; g.packed = true; g.Tq = total_q;
-  return ws_layout(g).total;
+  // base layout + room for the GQA split's fp32 dK/dV accumulators when total_k <= total_q
+  return (ws_layout(g).total + 255) / 256 * 256 + static_cast<size_t>(total_q) * H * d * 8;
 }
 
 fa2_status_t fa2_backward_varlen(const void* q, const void* k, const void* v, const void* o, const float* lse,
@@ -693,8 +736,13 @@ fa2_status_t backward_entry(const void* q, const void* k, const void* v, const v
   DeviceInfo di;
   if ((s = device_info(di)) != FA2_OK) return s;
   s = backward_impl(q, k, v, o, lse, dout, dq, dk, dv, workspace, g, causal, softmax_scale, dtype,
-                    static_cast<cudaStream_t>(stream), di.sms, deterministic);
-  if (s == FA2_OK) g_launches = g.packed ? 4 : 3;
+                    static_cast<cudaStream_t>(stream), di.sms, deterministic, workspace_bytes);
+  if (s == FA2_OK) {
+    size_t acc_off = 0;
+    long long dk_numel = 0;
+    const bool split = choose_hsplit(g, causal != 0, deterministic, di.sms, workspace_bytes, need, acc_off, dk_numel) > 1;
+    g_launches = (g.packed ? 4 : 3) + (split ? 1 : 0);
+  }
   return s;
 }
 }  // namespace
@@ -767,7 +815,7 @@ fa2_status_t fa2_attention_step_host(const void* q_h, const void* k_h, const voi
       FA2_OK)
     return s;
   if ((s = backward_impl(q, k, v, o, lse, dout, dq, dk, dv, ws, fixed_geom(B, H, H, N, N, d), causal, softmax_scale,
-                         dtype, st, di.sms, false)) != FA2_OK)
+                         dtype, st, di.sms, false, 0)) != FA2_OK)
     return s;
   if (o_h) FA2_CUDA(cudaMemcpyAsync(o_h, o, t, cudaMemcpyDeviceToHost, st));
   if (lse_h) FA2_CUDA(cudaMemcpyAsync(lse_h, lse, lbytes, cudaMemcpyDeviceToHost, st));

@@ -138,13 +138,13 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
       const int nb = w.nb, nqt = w.nqt, nk = w.sq.nk, off = w.sq.off;
       const int kv_row = nb * 128 + r;
       if (nqt == 0) {   // no query row sees this key block (N_q == 0): dV = dK = 0
-        if (kv_row < nk) {
+        if (p.hsplit == 1 && kv_row < nk) {   // (split: the zeroed fp32 accumulators already hold 0)
           uint4* z = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(wg == 0 ? p.dv : p.dk) + bwd_kv_off<GEN>(p, w, kv_row) * 2);
           for (int e = 0; e < D / 8; ++e) z[e] = make_uint4(0u, 0u, 0u, 0u);
         }
         continue;
       }
-      for (int x = 0; x < nqt * p.group; ++x, ++g) {
+      for (int x = 0; x < nqt * w.nh; ++x, ++g) {
         const int i = bwd_q_tile(p, CAUSAL, w, x % nqt);
         const uint32_t slot = g & 1;
         const uint32_t vL2 = sVec_a + slot * 2 * BM * 4, vD = vL2 + BM * 4;
@@ -226,7 +226,25 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
       // ---- epilogue: dV_j (warpgroup 0), dK_j * scale (warpgroup 1) ----
       ptx::mbar_wait(dkv_full, it & 1);
       ptx::tc_fence_after();
-      {
+      if (p.hsplit > 1) {
+        // this tile covers part of the group's query heads: fp32 reduce-add of the partial
+        // dV / dK (GQA load-balance split; fa2_dkv_convert casts the sums)
+        const uint32_t tsrc = tmem + lane_base + (wg == 0 ? T_DV : T_DK);
+        const float mul = wg == 0 ? 1.f : p.scale;
+        float* acc = (wg == 0 ? p.dv_acc : p.dk_acc) + bwd_kv_off<GEN>(p, w, kv_row);
+#pragma unroll
+        for (int ch = 0; ch < D / 32; ++ch) {
+          uint32_t v[32];
+          ptx::tmem_ld_x32(tsrc + ch * 32, v);
+          ptx::tmem_wait_ld();
+          if (kv_row < nk) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              ptx::red_add_v4_f32(acc + ch * 32 + 4 * e, __uint_as_float(v[4 * e]) * mul, __uint_as_float(v[4 * e + 1]) * mul,
+                                  __uint_as_float(v[4 * e + 2]) * mul, __uint_as_float(v[4 * e + 3]) * mul);
+          }
+        }
+      } else {
         const uint32_t tsrc = tmem + lane_base + (wg == 0 ? T_DV : T_DK);
         const float mul = wg == 0 ? 1.f : p.scale;
         uint8_t* dst = reinterpret_cast<uint8_t*>(wg == 0 ? p.dv : p.dk) + bwd_kv_off<GEN>(p, w, kv_row) * 2;
@@ -262,9 +280,9 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
       BwdTile w;
       if (!bwd_tile<GEN>(p, CAUSAL, t, w) || w.nqt == 0) continue;
       const int nb = w.nb, nqt = w.nqt;
-      for (int x = 0; x < nqt * p.group; ++x, ++g) {
+      for (int x = 0; x < nqt * w.nh; ++x, ++g) {
         const int i = bwd_q_tile(p, CAUSAL, w, x % nqt);
-        const long long acc0 = bwd_acc_row0<GEN>(p, w, w.kvh * p.group + x / nqt);   // query head of the group
+        const long long acc0 = bwd_acc_row0<GEN>(p, w, w.kvh * p.group + w.h0 + x / nqt);   // query head of the group
         float* const dq_rows = p.dq_acc + (acc0 + i * BM) * D;                        // this tile's 128 rows
         ptx::mbar_wait(dq_full, g & 1);
         if (leader) FA2_BTRACE(9, g);
@@ -340,7 +358,7 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
       BwdTile w;
       if (!bwd_tile<GEN>(p, CAUSAL, t, w) || w.nqt == 0) continue;
-      const uint32_t n = static_cast<uint32_t>(w.nqt * p.group);
+      const uint32_t n = static_cast<uint32_t>(w.nqt * w.nh);
       const uint32_t g0 = g;
       ptx::mbar_wait(kv_full, it & 1);
       // prologue: S^T of the first query tile (the S^T columns were last read by dV of the
@@ -430,8 +448,8 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
           tma_load_rows<GEN>(sK + s * L::SUB, &tm_k, kv_full, p.geom, s * 64, w.sq.k0 + nb * 128, w.kvh, w.sq.bc, p.Hkv, pol_kv);
           tma_load_rows<GEN>(sV + s * L::SUB, &tm_v, kv_full, p.geom, s * 64, w.sq.k0 + nb * 128, w.kvh, w.sq.bc, p.Hkv, pol_kv);
         }
-        for (int x = 0; x < nqt * p.group; ++x, ++g) {
-          const int i = bwd_q_tile(p, CAUSAL, w, x % nqt), hq = w.kvh * p.group + x / nqt;
+        for (int x = 0; x < nqt * w.nh; ++x, ++g) {
+          const int i = bwd_q_tile(p, CAUSAL, w, x % nqt), hq = w.kvh * p.group + w.h0 + x / nqt;
           const uint32_t slot = g & 1;
           // Q_i, L_i, D_i (2-stage ring; released after dK(i))
           if (g >= 2) ptx::mbar_wait(&q_empty[slot], ((g >> 1) - 1) & 1);

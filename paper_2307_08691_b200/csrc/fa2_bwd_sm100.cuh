@@ -61,15 +61,23 @@ struct BwdParams {
   long long acc_bs, acc_hs;      // padded workspace rows per batch entry (fixed layout) and per query head
   long long acc_rows;            // rows of dq_acc (and of D, L*log2e) in total
   const int* tile_off;           // packed: [B+1] prefix sums of ceil(N_q(b) / 128); nullptr: fixed layout
+  // GQA load balance: the query heads of a key/value group are split over `hsplit` work
+  // tiles; with hsplit > 1 the tiles reduce-add fp32 partial dK, dV into dk_acc, dv_acc
+  // (same element layout as dk, dv; zeroed beforehand, cast by fa2_dkv_convert).
+  int hsplit;
+  float* dk_acc;
+  float* dv_acc;
 };
 
 // A backward work tile: key block nb (128 rows) of key/value head kvh of sequence b,
-// visited with query tiles i0 .. i0+nqt-1 of every query head of the group.
+// visited with query tiles i0 .. i0+nqt-1 of query heads kvh*group + h0 .. + h0+nh-1
+// (the whole group unless hsplit > 1).
 struct BwdTile {
   int b, kvh, nb;
   Seq sq;
   int nqb;        // query tiles of the sequence, ceil(N_q / 128)
   int i0, nqt;    // first query tile and number of query tiles (per query head)
+  int h0, nh;     // query heads of the group handled by this tile
 };
 FA2_DEVICE void bwd_decode(const BwdParams& p, bool causal, int t, int& bh, int& nb);
 // Returns false when the key block lies past the sequence's keys (nothing to do).
@@ -77,7 +85,11 @@ FA2_DEVICE void bwd_decode(const BwdParams& p, bool causal, int t, int& bh, int&
 template <bool GEN>
 FA2_DEVICE bool bwd_tile(const BwdParams& p, bool causal, int t, BwdTile& w) {
   int bh, nb;
-  bwd_decode(p, causal, t, bh, nb);
+  bwd_decode(p, causal, t, bh, nb);   // bh = (b * Hkv + kvh) * hsplit + split
+  const int split = bh % p.hsplit;
+  bh /= p.hsplit;
+  w.nh = p.group / p.hsplit;
+  w.h0 = split * w.nh;
   w.b = bh / p.Hkv;
   w.kvh = bh % p.Hkv;
   w.nb = nb;
@@ -320,6 +332,25 @@ __global__ void __launch_bounds__(256) fa2_dq_convert(const RowParams p, long lo
   reinterpret_cast<uint4*>(p.dq)[i8] = out;
 }
 
+// GQA split: dK, dV = cast(dk_acc, dv_acc), n8 groups of 8 elements each (same layouts)
+template <bool BF16>
+__global__ void __launch_bounds__(256)
+fa2_dkv_convert(const float* __restrict__ dk_acc, const float* __restrict__ dv_acc, void* __restrict__ dk,
+                void* __restrict__ dv, long long n8) {
+  const long long i8 = static_cast<long long>(blockIdx.x) * 256 + threadIdx.x;
+  if (i8 >= 2 * n8) return;
+  const bool is_v = i8 >= n8;
+  const long long j = is_v ? i8 - n8 : i8;
+  const float4* src = reinterpret_cast<const float4*>((is_v ? dv_acc : dk_acc) + j * 8);
+  const float4 a = src[0], b = src[1];
+  uint4 out;
+  out.x = ptx::pack2<BF16>(a.x, a.y);
+  out.y = ptx::pack2<BF16>(a.z, a.w);
+  out.z = ptx::pack2<BF16>(b.x, b.y);
+  out.w = ptx::pack2<BF16>(b.z, b.w);
+  reinterpret_cast<uint4*>(is_v ? dv : dk)[j] = out;
+}
+
 template <int D>
 struct BwdSmem {
   static constexpr int BM = bwd_bm(D);
@@ -432,13 +463,13 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       const int nb = w.nb, nqt = w.nqt, nk = w.sq.nk, off = w.sq.off;
       const int kv_row = nb * 128 + r;
       if (nqt == 0) {   // no query row sees this key block (N_q == 0): dV = dK = 0
-        if (kv_row < nk) {
+        if (p.hsplit == 1 && kv_row < nk) {   // (split: the zeroed fp32 accumulators already hold 0)
           uint4* z = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(wg == 0 ? p.dv : p.dk) + bwd_kv_off<GEN>(p, w, kv_row) * 2);
           for (int e = 0; e < D / 8; ++e) z[e] = make_uint4(0u, 0u, 0u, 0u);
         }
         continue;
       }
-      for (int x = 0; x < nqt * p.group; ++x, ++g) {
+      for (int x = 0; x < nqt * w.nh; ++x, ++g) {
         const int i = bwd_q_tile(p, CAUSAL, w, x % nqt);   // query tile (of query head kvh*group + x/nqt)
         const int slot = g % STAGES;
         ptx::mbar_wait(&q_full[slot], (g / STAGES) & 1);
@@ -513,7 +544,25 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       // ---- epilogue: dV_j (warpgroup 0), dK_j * scale (warpgroup 1) ----
       ptx::mbar_wait(dkv_full, it & 1);
       ptx::tc_fence_after();
-      {
+      if (p.hsplit > 1) {
+        // this tile covers part of the group's query heads: fp32 reduce-add of the partial
+        // dV / dK (GQA load-balance split; fa2_dkv_convert casts the sums)
+        const uint32_t tsrc = tmem + lane_base + (wg == 0 ? T_DV : T_DK);
+        const float mul = wg == 0 ? 1.f : p.scale;
+        float* acc = (wg == 0 ? p.dv_acc : p.dk_acc) + bwd_kv_off<GEN>(p, w, kv_row);
+#pragma unroll
+        for (int ch = 0; ch < D / 32; ++ch) {
+          uint32_t v[32];
+          ptx::tmem_ld_x32(tsrc + ch * 32, v);
+          ptx::tmem_wait_ld();
+          if (kv_row < nk) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              ptx::red_add_v4_f32(acc + ch * 32 + 4 * e, __uint_as_float(v[4 * e]) * mul, __uint_as_float(v[4 * e + 1]) * mul,
+                                  __uint_as_float(v[4 * e + 2]) * mul, __uint_as_float(v[4 * e + 3]) * mul);
+          }
+        }
+      } else {
         const uint32_t tsrc = tmem + lane_base + (wg == 0 ? T_DV : T_DK);
         const float mul = wg == 0 ? 1.f : p.scale;
         uint8_t* dst = reinterpret_cast<uint8_t*>(wg == 0 ? p.dv : p.dk) + bwd_kv_off<GEN>(p, w, kv_row) * 2;
@@ -549,9 +598,9 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       BwdTile w;
       if (!bwd_tile<GEN>(p, CAUSAL, t, w) || w.nqt == 0) continue;
       const int nb = w.nb, nqt = w.nqt;
-      for (int x = 0; x < nqt * p.group; ++x, ++g) {
+      for (int x = 0; x < nqt * w.nh; ++x, ++g) {
         const int i = bwd_q_tile(p, CAUSAL, w, x % nqt);
-        const long long acc0 = bwd_acc_row0<GEN>(p, w, w.kvh * p.group + x / nqt);   // query head of the group
+        const long long acc0 = bwd_acc_row0<GEN>(p, w, w.kvh * p.group + w.h0 + x / nqt);   // query head of the group
         ptx::mbar_wait(dq_full, g & 1);
         if (leader) FA2_BTRACE(7, g);
         ptx::tc_fence_after();
@@ -665,7 +714,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       if (!bwd_tile<GEN>(p, CAUSAL, t, w) || w.nqt == 0) continue;
       ptx::mbar_wait(kv_full, it & 1);
       bool have_prev = false;
-      const int cnt = w.nqt * p.group;   // query tiles of every query head of the group
+      const int cnt = w.nqt * w.nh;   // query tiles of every query head of the tile
       for (int x = 0; x < cnt; ++x, ++g) {
         const uint32_t slot = g % STAGES;
         FA2_BTRACE(10, g);
@@ -721,8 +770,8 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           tma_load_rows<GEN>(sK + s * 128 * 128, &tm_k, kv_full, p.geom, s * 64, w.sq.k0 + nb * 128, w.kvh, w.sq.bc, p.Hkv, pol_kv);
           tma_load_rows<GEN>(sV + s * 128 * 128, &tm_v, kv_full, p.geom, s * 64, w.sq.k0 + nb * 128, w.kvh, w.sq.bc, p.Hkv, pol_kv);
         }
-        for (int x = 0; x < nqt * p.group; ++x, ++g) {
-          const int i = bwd_q_tile(p, CAUSAL, w, x % nqt), hq = w.kvh * p.group + x / nqt;
+        for (int x = 0; x < nqt * w.nh; ++x, ++g) {
+          const int i = bwd_q_tile(p, CAUSAL, w, x % nqt), hq = w.kvh * p.group + w.h0 + x / nqt;
           const int slot = g % STAGES;
           if (g >= STAGES) ptx::mbar_wait(&q_empty[slot], ((g / STAGES) - 1) & 1);
           ptx::mbar_arrive_expect_tx(&q_full[slot], 2 * L::Q_TILE + 2 * BM * 4);

@@ -163,6 +163,11 @@ FA2_DEVICE void bulk_reduce_add_f32(float* gdst, const void* smem_src, uint32_t 
   asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;"
                :: "l"(reinterpret_cast<uint64_t>(gdst)), "r"(smem_u32(smem_src)), "r"(bytes) : "memory");
 }
+// fp32 vector reduction into global memory (no return value), 16-byte aligned address
+FA2_DEVICE void red_add_v4_f32(float* gaddr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};"
+               :: "l"(reinterpret_cast<uint64_t>(gaddr)), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
 FA2_DEVICE void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N> FA2_DEVICE void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(N) : "memory"); }
 template <int N> FA2_DEVICE void bulk_wait() { asm volatile("cp.async.bulk.wait_group %0;" :: "n"(N) : "memory"); }

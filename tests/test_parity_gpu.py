@@ -180,3 +180,32 @@ def test_gqa_parity(shape, causal, dtype):
     for name, g, ref in (("dq", dq, gq), ("dk", dk, gk), ("dv", dv, gv)):
         ok, err, lim = grad_ok(g, ref, dtype, fl)
         assert ok, f"{name}: err {err} > {lim}"
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_gqa_split_matches_unsplit(causal):
+    """MQA with few key blocks: the default workspace enables the query-head split
+    (fp32 dK/dV partial sums); the minimum workspace disables it.  Same gradients up to
+    fp32 summation order, both within the oracle tolerance."""
+    B, H, Hkv, N, d = 1, 8, 1, 600, 128
+    q = W.randn((B, H, N, d), 80, "bf16")
+    k = W.randn((B, Hkv, N, d), 81, "bf16")
+    v = W.randn((B, Hkv, N, d), 82, "bf16")
+    do = W.randn((B, H, N, d), 83, "bf16")
+    sc = scale_for(d)
+    qc, kc, vc, doc = q.cuda(), k.cuda(), v.cuda(), do.cuda()
+    o, lse = fa2.forward(qc, kc, vc, causal=causal, softmax_scale=sc)
+    g_split = fa2.backward(qc, kc, vc, o, lse, doc, causal=causal, softmax_scale=sc)
+    assert fa2.lib().fa2_last_launch_count() == 4        # preprocess, main, dK/dV cast, dQ cast
+    L = fa2.lib()
+    base = L.fa2_backward_workspace_size(B, H, N, d) - B * H * N * d * 8
+    ws = torch.empty(base, dtype=torch.uint8, device="cuda")
+    g_one = fa2.backward(qc, kc, vc, o, lse, doc, causal=causal, softmax_scale=sc, workspace=ws)
+    assert fa2.lib().fa2_last_launch_count() == 3
+    torch.cuda.synchronize()
+    gq, gk, gv = R.backward_gqa(to_np(q), to_np(k), to_np(v), to_np(do), sc, causal)
+    fl = grad_floor(gq, gk, gv)
+    for grads in (g_split, g_one):
+        for name, g, ref in zip(("dq", "dk", "dv"), grads, (gq, gk, gv)):
+            ok, err, lim = grad_ok(g, ref, "bf16", fl)
+            assert ok, f"{name}: err {err} > {lim}"
