@@ -200,10 +200,13 @@ FA2_API fa2_status_t fa2_backward_preprocess(const void* o, const void* dout, fl
 
 /* End-to-end step through HOST buffers: copies q,k,v,dout (pinned host memory
  * recommended) to the device arena, runs fa2_forward then fa2_backward, and
- * copies o, lse, dq, dk, dv back to host, all on `stream`; returns after the
- * stream has been synchronised.  `arena` is caller-owned device memory of at
- * least fa2_step_arena_size(B,H,N,d) bytes.  Host output pointers may be NULL
- * to skip that copy. */
+ * copies o, lse, dq, dk, dv back to host; returns after all of it completed.
+ * The (b, h) units are independent, so the step is pipelined over up
+ * to 8 chunks of units: chunk c's inputs are copied in on an internal stream
+ * while chunk c-1 computes on `stream` and chunk c-2's results are copied out on
+ * another internal stream (ordered after the caller's prior work on `stream`).
+ * `arena` is caller-owned device memory of at least fa2_step_arena_size(B,H,N,d)
+ * bytes.  Host output pointers may be NULL to skip that copy. */
 FA2_API size_t fa2_step_arena_size(int B, int H, int N, int d);
 FA2_API fa2_status_t fa2_attention_step_host(const void* q_h, const void* k_h, const void* v_h, const void* dout_h,
                                      void* o_h, float* lse_h, void* dq_h, void* dk_h, void* dv_h,

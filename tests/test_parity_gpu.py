@@ -130,8 +130,11 @@ def test_overflow_logits_finite():
 
 
 @pytest.mark.parametrize("causal", [False, True])
-def test_step_host_matches_device_path(causal):
-    B, H, N, d = 1, 2, 384, 128
+@pytest.mark.parametrize("shape", [(1, 2, 384, 128), (3, 7, 300, 64)], ids=["2units", "21units-ragged-chunks"])
+def test_step_host_matches_device_path(causal, shape):
+    """The pipelined host-buffer step (chunks of (b, h) units over 3 streams) computes
+    exactly what the device path computes (dQ up to the reduce-add order)."""
+    B, H, N, d = shape
     q, k, v, do = W.qkv(B, H, N, d, "bf16", seed=9)
     pin = [t.pin_memory() for t in (q, k, v, do)]
     outs = {"o": torch.empty_like(q).pin_memory(), "lse": torch.empty(B, H, N).pin_memory(),
