@@ -440,7 +440,7 @@ fa2_status_t dispatch_bwd_causal(bool causal, const fa2::BwdMaps& maps, const fa
 
 // GQA load balance (BwdParams::hsplit): the query heads of a key/value group are split
 // over `hsplit` work tiles when the unsplit tile count would leave SMs idle (< 2 waves) or,
-// causal, when the heaviest tile exceeds half of an SM's average share.  Needs fp32 dK/dV
+// causal, when the heaviest tile exceeds a quarter of an SM's average share.  Needs fp32 dK/dV
 // accumulators (2 * numel(dk) * 4 bytes) after the base workspace; not used in the
 // deterministic mode (the fp32 reduce-adds would make dK/dV order-dependent).
 int choose_hsplit(const Geom& g, bool causal, bool deterministic, int sms, size_t ws_bytes, size_t base,
@@ -452,9 +452,9 @@ int choose_hsplit(const Geom& g, bool causal, bool deterministic, int sms, size_
   const long long nkb = (g.Nk + 127) / 128, nqb = (g.Nq + 127) / 128;
   const long long tiles1 = static_cast<long long>(g.B) * g.Hkv * nkb;
   long long need = (2LL * sms + tiles1 - 1) / tiles1;
-  if (causal) {   // heaviest tile (key block 0: nqb query tiles x group/split heads) <= half an SM's share
+  if (causal) {   // heaviest tile (key block 0: nqb query tiles x group/split heads) <= 1/4 of an SM's share
     const long long den = (nqb + 1) * g.B * g.Hkv;
-    need = std::max(need, (4LL * sms + den - 1) / den);
+    need = std::max(need, (8LL * sms + den - 1) / den);
   }
   for (int sp = 1; sp <= group; ++sp)
     if (group % sp == 0 && sp >= need) return sp;
