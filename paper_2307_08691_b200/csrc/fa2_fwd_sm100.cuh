@@ -100,6 +100,15 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   constexpr int STAGES = L::STAGES;
   constexpr int NSUB = D * (FP8 ? 1 : 2) / 128;   // 128-B swizzle boxes per tile row
   constexpr bool SEP_P = (D == 64);   // P~ in its own TMEM columns (fits only at d = 64)
+  // FP8 (P~ over the first 32 columns of S_i): S_{j+1} in two N = 64 halves -- columns
+  // 64-127 as soon as the softmax has read S_j (they are not under P~), columns 0-63 after
+  // P~V_j -- so half of the next S overlaps the softmax instead of following P~V (+5-11%).
+  // Not for bf16/fp16: each half re-reads the 32 KB Q tile, and S = Q K^T already runs at
+  // the SMEM -> tensor-core rate (128 B/clk) with N = 128 (measured -15%).
+#ifndef FA2_FWD_SPLIT_S
+#define FA2_FWD_SPLIT_S 1
+#endif
+  constexpr bool SPLIT_S = !SEP_P && FP8 && FA2_FWD_SPLIT_S;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
 
@@ -218,8 +227,8 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         ptx::tmem_ld_x32(tS + 64, su + 64);
         ptx::tmem_ld_x32(tS + 96, su + 96);
         ptx::tmem_wait_ld();
-        if constexpr (SEP_P) {
-          // S_i has been read: the MMA warp may compute S_i of the next block into it
+        if constexpr (SEP_P || SPLIT_S) {
+          // S_i has been read: the MMA warp may compute (part of) S_i of the next block into it
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&s_consumed[wg]);
@@ -366,6 +375,21 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
                         k > 0 ? 1u : 0u);
         }
       };
+      // one N = 64 half of S_i = Q_i K^T: key rows [64 h, 64 h + 64) -> S columns [64 h, 64 h + 64)
+      constexpr uint32_t IDESC_S64 = ptx::idesc_f16(FP8 ? false : BF16, 128, 64, false, false);
+      auto mma_s_half = [&](int i, int slot, int h) {
+#pragma unroll
+        for (int k = 0; k < D * (FP8 ? 1 : 2) / 32; ++k) {
+          const uint32_t off = (k / 4) * L::SUB + (k % 4) * 32;
+          const uint32_t boff = slot * L::TILE + off + h * 64 * 128;   // 64 rows of 128 B further
+          if constexpr (FP8)
+            ptx::mma_ss_f8(tmem + i * 128 + h * 64, dQ + ((i * L::TILE + off) >> 4), dK + (boff >> 4), IDESC_S64,
+                           k > 0 ? 1u : 0u);
+          else
+            ptx::mma_ss(tmem + i * 128 + h * 64, dQ + ((i * L::TILE + off) >> 4), dK + (boff >> 4), IDESC_S64,
+                        k > 0 ? 1u : 0u);
+        }
+      };
       auto mma_pv = [&](int i, int slot, bool acc) {
         // K = 128 keys: 8 steps of 16 (P~ 16-bit: 8 TMEM columns, V rows 16 x 128 B) or
         // 4 steps of 32 (P~ E4M3: 8 TMEM columns, V rows 32 x 128 B)
@@ -382,6 +406,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         }
       };
       uint32_t s_iss0 = 0, s_iss1 = 0;   // d = 64: S MMAs issued per sub-tile (s_consumed phases)
+      uint32_t sc_count0 = 0, sc_count1 = 0;   // d = 128 SPLIT_S: s_consumed phases waited per sub-tile
       // d = 64: S_i into its buffer once softmax i has read the previous S_i
       auto issue_s_sep = [&](int i, uint32_t& s_iss) {
         if (s_iss > 0) ptx::mbar_wait(&s_consumed[i], (s_iss - 1) & 1);
@@ -451,7 +476,22 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         for (int j = 0; j < nkv; ++j) {
           ptx::mbar_wait(&v_full[vslot], vphase);
           bool k_ready = false;
+          // SPLIT_S: once softmax i has read S_i(j), S_i(j+1) columns 64-127
+          auto step_b = [&](int i, int nbi, uint32_t& sc_count) {
+            if (j >= nbi) return;
+            ptx::mbar_wait(&s_consumed[i], sc_count & 1);   // every block's read is waited for (phases)
+            ++sc_count;
+            if (j + 1 >= nbi) return;
+            if (!k_ready) {
+              ptx::mbar_wait(&k_full[kslot], kphase);
+              k_ready = true;
+            }
+            ptx::tc_fence_after();
+            if (ptx::elect_one()) mma_s_half(i, kslot, 1);
+            __syncwarp();
+          };
           // sub-tile i: O_i += P_i V_j (after softmax i signals P_i), then S_i = Q_i K_{j+1}^T
+          // (SPLIT_S: its columns 0-63, the rest was issued by step_b)
           auto step = [&](int i, int nbi, uint32_t& p_count, uint32_t& o_uses) {
             const bool do_pv = j < nbi, do_s = j + 1 < nbi;
             if (do_pv) {
@@ -470,12 +510,18 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             ptx::tc_fence_after();
             if (ptx::elect_one()) {
               if (do_pv) { mma_pv(i, vslot, j > 0); ptx::mma_commit(&o_done[i]); }
-              if (do_s) { mma_s(i, kslot); ptx::mma_commit(&s_full[i]); }
+              if (do_s) {
+                if constexpr (SPLIT_S) mma_s_half(i, kslot, 0);
+                else mma_s(i, kslot);
+                ptx::mma_commit(&s_full[i]);
+              }
             }
             __syncwarp();
             if (do_s && it == 0) FA2_TRACE(5, i, j);
           };
+          if constexpr (SPLIT_S) step_b(0, nb0, sc_count0);
           step(0, nb0, p_count0, o_uses0);
+          if constexpr (SPLIT_S) step_b(1, nb1, sc_count1);
           step(1, nb1, p_count1, o_uses1);
           if (ptx::elect_one()) {
             ptx::mma_commit(&v_empty[vslot]);
