@@ -20,8 +20,6 @@ FA2_DEVICE uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-FA2_DEVICE uint32_t lane_id() { uint32_t r; asm volatile("mov.u32 %0, %%laneid;" : "=r"(r)); return r; }
-
 FA2_DEVICE bool elect_one() {
   uint32_t pred = 0;
   asm volatile(
@@ -107,9 +105,6 @@ FA2_DEVICE void st_release_gpu(int* p, int v) {
 FA2_DEVICE void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(nthreads) : "memory");
 }
-FA2_DEVICE void named_bar_arrive(uint32_t id, uint32_t nthreads) {
-  asm volatile("bar.arrive %0, %1;" :: "r"(id), "r"(nthreads) : "memory");
-}
 template <uint32_t N> FA2_DEVICE void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :: "n"(N)); }
 template <uint32_t N> FA2_DEVICE void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(N)); }
 
@@ -119,38 +114,15 @@ template <uint32_t N> FA2_DEVICE void setmaxnreg_dec() { asm volatile("setmaxnre
 FA2_DEVICE void tma_prefetch_desc(const CUtensorMap* d) {
   asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(d)) : "memory");
 }
-FA2_DEVICE void tma_load_3d(void* smem_dst, const CUtensorMap* d, uint64_t* bar, int c0, int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
-      :: "r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(d)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-      : "memory");
-}
 FA2_DEVICE void tma_load_3d_hint(void* smem_dst, const CUtensorMap* d, uint64_t* bar, int c0, int c1, int c2, uint64_t policy) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;"
       :: "r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(d)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
-FA2_DEVICE void tma_load_4d_hint(void* smem_dst, const CUtensorMap* d, uint64_t* bar, int c0, int c1, int c2, int c3,
-                                 uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;"
-      :: "r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(d)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
-         "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
-FA2_DEVICE void tma_store_3d(const CUtensorMap* d, const void* smem_src, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];"
-               :: "l"(reinterpret_cast<uint64_t>(d)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(smem_src)) : "memory");
-}
 FA2_DEVICE void tma_reduce_add_2d(const CUtensorMap* d, const void* smem_src, int c0, int c1) {
   asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];"
                :: "l"(reinterpret_cast<uint64_t>(d)), "r"(c0), "r"(c1), "r"(smem_u32(smem_src)) : "memory");
-}
-FA2_DEVICE void tma_reduce_add_3d(const CUtensorMap* d, const void* smem_src, int c0, int c1, int c2) {
-  asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];"
-               :: "l"(reinterpret_cast<uint64_t>(d)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(smem_src)) : "memory");
 }
 // 1-D bulk copy global -> shared, completing `bytes` on an mbarrier (bytes % 16 == 0).
 FA2_DEVICE void bulk_load_1d(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
