@@ -461,6 +461,14 @@ def run_extras(fa2, dev):
         res.append({"case": "varlen", "sequences": len(lens), "total_tokens": T, "min_len": min(lens),
                     "max_len": max(lens), "H": H, "d": d, "causal": causal,
                     "fwd_tflops": round(fl / t_f / 1e9, 1), "bwd_tflops": round(2.5 * fl / t_b / 1e9, 1)})
+    # roofline fractions: measured bf16 GEMM peak; FP8 = 2x (the nominal E4M3 : bf16 ratio)
+    pk = measured_peaks()["bf16_tflops"]
+    for r in res:
+        peak = 2 * pk if "fp8" in r["case"] else pk
+        r["peak_tflops"] = peak
+        for key in ("fwd_tflops", "bwd_tflops", "bwd_deterministic_tflops"):
+            if key in r:
+                r[key.replace("_tflops", "_frac")] = round(r[key] / peak, 3)
     return res
 
 
