@@ -207,7 +207,7 @@ fa2_status_t launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUte
   if (s != FA2_OK) return s;
   const int grid = p.num_tiles < sms ? p.num_tiles : sms;
   mark(0, st);
-  kern<<<grid, 384, smem, st>>>(mq, mk, mv, p);
+  kern<<<grid, fa2::FwdCfg<D, FP8>::THREADS, smem, st>>>(mq, mk, mv, p);
   mark(1, st);
   FA2_CUDA(cudaGetLastError());
   return FA2_OK;

@@ -18,15 +18,19 @@
 // visited and the mask is only evaluated on blocks that straddle the diagonal
 // or the ragged tail.
 //
-// Warp roles (384 threads):
+// Warp roles (384 threads; FwdCfg):
 //   warps 0-3   softmax WG 0: rows of Q0 (TMEM lanes 0-127), also O0 rescale + epilogue
 //   warps 4-7   softmax WG 1: rows of Q1
-//   warp  8     MMA issuer (one thread)
-//   warp  9     TMA producer (one thread)
-//   warps 10-11 idle (complete the register-donor warpgroup)
+//   warp  8     MMA issuer (one elected thread)
+//   warp  9     TMA producer of Q and K, warp 10 TMA producer of V (one thread each)
+//   warp  11    idle (HB: MMA issuer of sub-tile 1)
 //
 // TMEM columns: S0 [0,128), S1 [128,256), O0 [256,256+D), O1 [256+D,256+2D);
-// P~_i (16-bit) is written over the first 64 columns of S_i.
+// P~_i (16-bit) is written over the first 64 columns of S_i (d = 64: own columns).
+//
+// Compile-time alternatives, measured on B200 and off by default:
+// FA2_FWD_RS=2 (two warps per row, row max exchanged through SMEM) and FA2_FWD_HB=1
+// (B_c = 64, double-buffered P~, one MMA issuer per sub-tile).
 #pragma once
 #include <cuda_fp16.h>
 #include <cuda_bf16.h>
@@ -46,6 +50,27 @@ namespace fa2 {
 #define FA2_FWD_EMU_PAIRS_D64 6
 #endif
 constexpr int kFwdEmuPairs = FA2_FWD_EMU_PAIRS;
+// Row split (bf16/fp16, d = 128): each 128-row sub-tile's softmax runs on 8 warps, two
+// per TMEM lane quarter, each owning 64 of the 128 columns of its rows (row max
+// exchanged through shared memory).  One warp per SMSP per sub-tile reaches only ~2/3
+// of the MUFU.EX2 rate (tools/micro/mufu2.cu); two reach ~90%.
+#ifndef FA2_FWD_RS
+#define FA2_FWD_RS 1
+#endif
+// 64-key blocks (bf16/fp16, d = 128): B_c = 64 gives every sub-tile its own P~ columns
+// (TMEM: O0 O1 [0,256) | S0 S1 [256,384) | P~ 2 x 2 buffers [384,512)), so S_{j+1} is issued as
+// soon as the softmax has read S_j and the softmax -> P~V -> S chain disappears.  The
+// TMA stages stay 128 key rows (two blocks each).
+#ifndef FA2_FWD_HB
+#define FA2_FWD_HB 0
+#endif
+template <int D, bool FP8> struct FwdCfg {
+  static constexpr int RS = (D == 128 && !FP8) ? FA2_FWD_RS : 1;   // warps per row quarter
+  static constexpr int SM_WARPS = 8 * RS;                          // softmax warps (both sub-tiles)
+  static constexpr int THREADS = SM_WARPS * 32 + 128;              // + MMA, TMA, 2 idle
+  static constexpr int REG_SM = RS == 2 ? 104 : 224;               // setmaxnreg per warpgroup
+  static constexpr int REG_OTHER = RS == 2 ? 64 : 56;   // RS = 2: 104*512 + 64*128 == 96*640 (the launch allocation)
+};
 constexpr int kFwdEmuPairsD64 = FA2_FWD_EMU_PAIRS_D64;
 
 struct FwdParams {
@@ -81,10 +106,12 @@ struct FwdSmem {
   static constexpr int OFF_K = OFF_Q + 2 * TILE;
   static constexpr int OFF_V = OFF_K + STAGES * TILE;
   static constexpr int OFF_BAR = OFF_V + STAGES * TILE;
-  // barriers: q_full[2] q_empty[2] k_full[S] k_empty[S] v_full[S] v_empty[S] s_full[2] p_full[2] o_done[2] o_empty[2]
-  static constexpr int NBAR = 2 + 2 + 4 * STAGES + 2 + 2 + 2 + 2 + 2;   // + s_consumed[2]
+  // barriers: q_full[2] q_empty[2] k_full[S] k_empty[S] v_full[S] v_empty[S] s_full[2] p_full[2][2] o_done[2][2] o_empty[2]
+  static constexpr int NBAR = 2 + 2 + 4 * STAGES + 2 + 4 + 4 + 2 + 2;   // + s_consumed[2]
   static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
-  static constexpr int BYTES = OFF_TMEM + 16;
+  // row-split exchange: max[2 parities][2 sub-tiles][2 halves][128 rows], l[2][2][128]
+  static constexpr int OFF_RED = OFF_TMEM + 16;
+  static constexpr int BYTES = OFF_RED + (2 * 2 * 2 * 128 + 2 * 2 * 128) * 4;
   static constexpr int ALLOC = BYTES + 1024;   // slack for 1024-B alignment
 };
 
@@ -92,14 +119,31 @@ struct FwdSmem {
 // P~ quantized to E4M3 for the P~V MMA (P~ <= 2^8 under the lazy rescale, inside E4M3's
 // 448), O written as bf16 (BF16 == true); d = 128 only (one 128-B swizzle atom per row).
 template <int D, bool BF16, bool CAUSAL, bool GEN, bool FP8 = false>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(FwdCfg<D, FP8>::THREADS, 1)
 fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
   static_assert(!FP8 || (D == 128 && BF16), "FP8 forward: d = 128, bf16 output");
   using L = FwdSmem<D, FP8 ? 1 : 2>;
+  using CFG = FwdCfg<D, FP8>;
+  constexpr int RS = CFG::RS;
+  constexpr int COLS = (((D == 128) && !FP8 && FA2_FWD_HB) ? 64 : 128) / RS;   // S columns per softmax thread
+  constexpr int W_MMA = CFG::SM_WARPS, W_TMA = CFG::SM_WARPS + 1, W_MMA2 = CFG::SM_WARPS + 3;
   constexpr int STAGES = L::STAGES;
   constexpr int NSUB = D * (FP8 ? 1 : 2) / 128;   // 128-B swizzle boxes per tile row
-  constexpr bool SEP_P = (D == 64);   // P~ in its own TMEM columns (fits only at d = 64)
+  constexpr bool HB = (D == 128) && !FP8 && FA2_FWD_HB;   // 64-key blocks
+  constexpr int BN = HB ? 64 : 128;                          // B_c: keys per block
+  constexpr bool SEP_P = (D == 64) || HB;   // P~ in its own TMEM columns
+  // TMEM columns of S_i, O_i and (SEP_P) P~_i
+  constexpr uint32_t TS0 = HB ? 2 * D : 0, TS_STEP = BN;
+  constexpr uint32_t TO0 = HB ? 0 : 256;
+  constexpr uint32_t TP0 = HB ? 2 * D + 2 * BN : 256 + 2 * D, TP_STEP = BN / 2;
+  // HB: two P~ buffers per sub-tile (P~ of block j in buffer j % 2), so the softmax of
+  // block j+1 never waits for P~V of block j.  p_full[i][b] / o_done[i][b] hand buffer b
+  // over (written / read); P~V number n of sub-tile i (counted over all tiles) uses
+  // b = n % NPB, so no barrier runs more than one phase ahead of its waiter.
+  constexpr int NPB = HB ? 2 : 1;
+  auto od_bar = [&](uint64_t* od, int i, uint32_t n) { return &od[2 * i + (NPB == 2 ? (n & 1) : 0)]; };
+  auto od_par = [&](uint32_t n) -> uint32_t { return NPB == 2 ? ((n >> 1) & 1) : (n & 1); };
   // FP8 (P~ over the first 32 columns of S_i): S_{j+1} in two N = 64 halves -- columns
   // 64-127 as soon as the softmax has read S_j (they are not under P~), columns 0-63 after
   // P~V_j -- so half of the next S overlaps the softmax instead of following P~V (+5-11%).
@@ -124,8 +168,8 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   uint64_t* v_empty = v_full + STAGES;
   uint64_t* s_full = v_empty + STAGES;
   uint64_t* p_full = s_full + 2;
-  uint64_t* o_done = p_full + 2;
-  uint64_t* o_empty = o_done + 2;
+  uint64_t* o_done = p_full + 4;   // p_full / o_done: [sub-tile][P~ buffer], see od_bar
+  uint64_t* o_empty = o_done + 4;
   uint64_t* s_consumed = o_empty + 2;   // [2] d=64 only: softmax has read S_i (4 warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
 
@@ -137,20 +181,22 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       ptx::mbar_init(&q_full[i], 1);
       ptx::mbar_init(&q_empty[i], 1);
       ptx::mbar_init(&s_full[i], 1);
-      ptx::mbar_init(&p_full[i], 4);
-      ptx::mbar_init(&o_done[i], 1);
-      ptx::mbar_init(&o_empty[i], 4);
+      ptx::mbar_init(&p_full[2 * i], 4 * RS);
+      ptx::mbar_init(&p_full[2 * i + 1], 4 * RS);
+      ptx::mbar_init(&o_done[2 * i], 1);
+      ptx::mbar_init(&o_done[2 * i + 1], 1);
+      ptx::mbar_init(&o_empty[i], 4 * RS);
       ptx::mbar_init(&s_consumed[i], 4);
     }
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&k_full[s], 1);
-      ptx::mbar_init(&k_empty[s], 1);
+      ptx::mbar_init(&k_empty[s], HB ? 2 : 1);
       ptx::mbar_init(&v_full[s], 1);
-      ptx::mbar_init(&v_empty[s], 1);
+      ptx::mbar_init(&v_empty[s], HB ? 2 : 1);
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 9 && lane == 0) {
+  if (warp == W_TMA && lane == 0) {
     ptx::tma_prefetch_desc(&tm_q);
     ptx::tma_prefetch_desc(&tm_k);
     ptx::tma_prefetch_desc(&tm_v);
@@ -176,23 +222,30 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   auto n_blocks = [&](const Seq& sq, int mb, int i) -> int {
     const int r0 = mb * 256 + i * 128;
     if (r0 >= sq.nq) return 0;
-    const int nkb = (sq.nk + 127) / 128;
+    const int nkb = (sq.nk + BN - 1) / BN;
     if (!CAUSAL) return nkb;
     const int last_col = min(sq.nq - 1, r0 + 127) + sq.off;   // last key the sub-tile's last row sees
-    return last_col < 0 ? 0 : min(nkb, last_col / 128 + 1);
+    return last_col < 0 ? 0 : min(nkb, last_col / BN + 1);
   };
 
-  if (warp < 8) {
+  if (warp < CFG::SM_WARPS) {
     // ======================= softmax warpgroups =======================
-    ptx::setmaxnreg_inc<224>();   // 224*256 + 56*128 == 168*384
-    const int wg = warp / 4;                 // sub-tile index
-    const int row = threadIdx.x % 128;       // TMEM lane == row within sub-tile
-    const uint32_t lane_base = static_cast<uint32_t>((warp % 4) * 32) << 16;
-    const uint32_t tS = tmem + lane_base + wg * 128;
-    // P~_i: over the first 64 columns of S_i (d = 128), or its own 64 columns
-    // after O0, O1 (d = 64: frees S_i for S_{j+1} as soon as it has been read)
-    const uint32_t tP = SEP_P ? (tmem + lane_base + 256 + 2 * D + wg * 64) : tS;
-    const uint32_t tO = tmem + lane_base + 256 + wg * D;
+    // RS = 1: 224*256 + 56*128 == 168*384;  RS = 2: 104*512 + 64*128 == 96*640
+    ptx::setmaxnreg_inc<CFG::REG_SM>();
+    const int wg = warp / (4 * RS);          // sub-tile index
+    const int hf = (warp / 4) % RS;          // column half (RS = 2)
+    const int quad = warp % 4;               // TMEM lane quarter
+    const int row = quad * 32 + lane;        // TMEM lane == row within sub-tile
+    const bool lead = hf == 0;               // writes L, zero rows
+    const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
+    const uint32_t tS = tmem + lane_base + TS0 + wg * TS_STEP + hf * COLS;
+    // P~_i: over the first 64 columns of S_i (B_c = 128, d = 128), or its own columns
+    // (d = 64, or B_c = 64: frees S_i for S_{j+1} as soon as it has been read)
+    const uint32_t tP0 = SEP_P ? (tmem + lane_base + TP0 + wg * NPB * TP_STEP) : (tmem + lane_base + TS0 + wg * TS_STEP + hf * COLS / 2);
+    const uint32_t tO = tmem + lane_base + TO0 + wg * D + hf * (D / RS);
+    float* red_max = reinterpret_cast<float*>(smem + L::OFF_RED);          // [2][2][2][128]
+    float* red_l = red_max + 2 * 2 * 2 * 128;                              // [2][2][128]
+    const uint32_t bar_id = 1 + wg * 4 + quad;   // named barrier of the two warps sharing these rows
     uint32_t s_count = 0;   // completed waits on s_full[wg]
     uint32_t pv_count = 0;  // PV MMAs issued so far for this sub-tile (all tiles)
     const float sl2 = p.scale_log2;
@@ -207,10 +260,11 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         // rows that see no key (R23): O = 0, L = -inf; no MMA work was scheduled
         if (grow < sq.nq) {
           uint4* dst = reinterpret_cast<uint4*>(
-              reinterpret_cast<uint8_t*>(p.o) + (sq.bc * p.o_bs + (bh % p.H) * p.o_hs + (sq.q0 + grow) * p.o_rs) * 2);
+              reinterpret_cast<uint8_t*>(p.o) + (sq.bc * p.o_bs + (bh % p.H) * p.o_hs + (sq.q0 + grow) * p.o_rs) * 2) +
+              hf * (D / RS / 8);
 #pragma unroll
-          for (int e = 0; e < D / 8; ++e) dst[e] = make_uint4(0u, 0u, 0u, 0u);
-          p.lse[sq.bc * p.l_bs + (bh % p.H) * p.l_hs + sq.q0 + grow] = -INFINITY;
+          for (int e = 0; e < D / RS / 8; ++e) dst[e] = make_uint4(0u, 0u, 0u, 0u);
+          if (lead) p.lse[sq.bc * p.l_bs + (bh % p.H) * p.l_hs + sq.q0 + grow] = -INFINITY;
         }
         continue;
       }
@@ -218,14 +272,13 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       float l_sum = 0.f;
       for (int j = 0; j < nb; ++j) {
         ptx::mbar_wait(&s_full[wg], s_count & 1);
+        const int par = s_count & 1;
         ++s_count;
-        if (threadIdx.x % 128 == 0 && t == (int)blockIdx.x) FA2_TRACE(0, wg, j);
+        if (threadIdx.x % (128 * RS) == 0 && t == (int)blockIdx.x) FA2_TRACE(0, wg, j);
         ptx::tc_fence_after();
-        uint32_t su[128];
-        ptx::tmem_ld_x32(tS + 0, su + 0);
-        ptx::tmem_ld_x32(tS + 32, su + 32);
-        ptx::tmem_ld_x32(tS + 64, su + 64);
-        ptx::tmem_ld_x32(tS + 96, su + 96);
+        uint32_t su[COLS];
+#pragma unroll
+        for (int c = 0; c < COLS; c += 32) ptx::tmem_ld_x32(tS + c, su + c);
         ptx::tmem_wait_ld();
         if constexpr (SEP_P || SPLIT_S) {
           // S_i has been read: the MMA warp may compute (part of) S_i of the next block into it
@@ -233,21 +286,29 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&s_consumed[wg]);
         }
-        float s[128];
+        float s[COLS];
 #pragma unroll
-        for (int c = 0; c < 128; ++c) s[c] = __uint_as_float(su[c]);
-        const int c0 = j * 128;
-        const bool need_mask = (c0 + 128 > sq.nk) || (CAUSAL && (c0 + 127 > row0 + sq.off));
+        for (int c = 0; c < COLS; ++c) s[c] = __uint_as_float(su[c]);
+        const int c0 = j * BN;
+        const bool need_mask = (c0 + BN > sq.nk) || (CAUSAL && (c0 + BN - 1 > row0 + sq.off));
         if (need_mask) {
           const int lim = CAUSAL ? min(sq.nk - 1, grow + sq.off) : (sq.nk - 1);
 #pragma unroll
-          for (int c = 0; c < 128; ++c)
-            if (c0 + c > lim) s[c] = -INFINITY;
+          for (int c = 0; c < COLS; ++c)
+            if (c0 + hf * COLS + c > lim) s[c] = -INFINITY;
         }
         float mx = s[0];
 #pragma unroll
-        for (int c = 1; c < 128; ++c) mx = fmaxf(mx, s[c]);
-        if (threadIdx.x % 128 == 0 && t == (int)blockIdx.x) FA2_TRACE(1, wg, j);
+        for (int c = 1; c < COLS; ++c) mx = fmaxf(mx, s[c]);
+        if constexpr (RS == 2) {
+          // the row's other half lives in the partner warp (same lanes, other columns)
+          float* mine = red_max + ((par * 2 + wg) * 2 + hf) * 128;
+          float* other = red_max + ((par * 2 + wg) * 2 + (hf ^ 1)) * 128;
+          mine[row] = mx;
+          ptx::named_bar_sync(bar_id, 64);
+          mx = fmaxf(mx, other[row]);
+        }
+        if (threadIdx.x % (128 * RS) == 0 && t == (int)blockIdx.x) FA2_TRACE(1, wg, j);
         const float m_new = fmaxf(m_used, mx * sl2);
         const bool rescale = (m_new - m_used) > 8.0f;   // also true when m_used == -inf and m_new finite
         float alpha = 1.f;
@@ -262,13 +323,15 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         // EMU of every 16 column pairs use the FMA-pipe polynomial, the rest MUFU.EX2.
         if constexpr (SEP_P) {
           // the P buffer is free once the previous P~V MMA of this sub-tile completed
-          if (pv_count > 0) ptx::mbar_wait(&o_done[wg], (pv_count - 1) & 1);
+          // (HB: the buffer this block writes was last read by P~V number pv_count - 2)
+          if (pv_count >= (uint32_t)NPB) ptx::mbar_wait(od_bar(o_done, wg, pv_count - NPB), od_par(pv_count - NPB));
           ptx::tc_fence_after();
         }
+        const uint32_t tP = tP0 + (pv_count % NPB) * TP_STEP;
         auto exp_block = [&](auto emu_tag) {
           constexpr int EMU = decltype(emu_tag)::value;
 #pragma unroll
-          for (int ch = 0; ch < 4; ++ch) {
+          for (int ch = 0; ch < COLS / 32; ++ch) {
             uint32_t pk[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
@@ -295,14 +358,14 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         if (need_mask) exp_block(std::integral_constant<int, 0>{});
         else exp_block(std::integral_constant<int, D == 64 ? kFwdEmuPairsD64 : kFwdEmuPairs>{});
         l_sum = l_sum * alpha + (rs2.x + rs2.y);
-        if (threadIdx.x % 128 == 0 && t == (int)blockIdx.x) FA2_TRACE(2, wg, j);
+        if (threadIdx.x % (128 * RS) == 0 && t == (int)blockIdx.x) FA2_TRACE(2, wg, j);
         // Rescale the un-normalised O accumulator before P~_j V_j is added
         // (needs PV_{j-1} finished; it was issued before S_j, so it usually is).
         if (j > 0 && __any_sync(0xffffffffu, rescale)) {
-          ptx::mbar_wait(&o_done[wg], (pv_count - 1) & 1);
+          ptx::mbar_wait(od_bar(o_done, wg, pv_count - 1), od_par(pv_count - 1));
           ptx::tc_fence_after();
 #pragma unroll
-          for (int ch = 0; ch < D / 32; ++ch) {
+          for (int ch = 0; ch < D / RS / 32; ++ch) {
             uint32_t o[32];
             ptx::tmem_ld_x32(tO + ch * 32, o);
             ptx::tmem_wait_ld();
@@ -314,20 +377,27 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&p_full[wg]);
-        if (threadIdx.x % 128 == 0 && t == (int)blockIdx.x) FA2_TRACE(3, wg, j);
+        if (lane == 0) ptx::mbar_arrive(od_bar(p_full, wg, pv_count));
+        if (threadIdx.x % (128 * RS) == 0 && t == (int)blockIdx.x) FA2_TRACE(3, wg, j);
         ++pv_count;
       }
       // ---- epilogue: O = O / l, L = m + log l (natural log) ----
-      ptx::mbar_wait(&o_done[wg], (pv_count - 1) & 1);
+      ptx::mbar_wait(od_bar(o_done, wg, pv_count - 1), od_par(pv_count - 1));
       ptx::tc_fence_after();
+      if constexpr (RS == 2) {   // l of the whole row: both halves' partial sums
+        float* mine = red_l + (wg * 2 + hf) * 128;
+        mine[row] = l_sum;
+        ptx::named_bar_sync(bar_id, 64);
+        l_sum += red_l[(wg * 2 + (hf ^ 1)) * 128 + row];
+        ptx::named_bar_sync(bar_id, 64);   // both read before the next tile's writes
+      }
       float inv_l = l_sum > 0.f ? 1.f / l_sum : 0.f;   // rows that saw no key: O = 0 (R23)
       if constexpr (FP8) inv_l *= p.o_descale;
       uint8_t* orow = reinterpret_cast<uint8_t*>(p.o) +
                       (GEN ? (sq.bc * p.o_bs + (bh % p.H) * p.o_hs + (sq.q0 + grow) * p.o_rs)
-                           : (static_cast<size_t>(bh) * sq.nq + grow) * D) * 2;
+                           : (static_cast<size_t>(bh) * sq.nq + grow) * D) * 2 + hf * (D / RS) * 2;
 #pragma unroll
-      for (int ch = 0; ch < D / 32; ++ch) {
+      for (int ch = 0; ch < D / RS / 32; ++ch) {
         uint32_t o[32];
         ptx::tmem_ld_x32(tO + ch * 32, o);
         ptx::tmem_wait_ld();
@@ -341,16 +411,21 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           for (int e = 0; e < 4; ++e) dst[e] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
         }
       }
-      if (grow < sq.nq)
+      if (grow < sq.nq && lead)
         p.lse[GEN ? sq.bc * p.l_bs + (bh % p.H) * p.l_hs + sq.q0 + grow : static_cast<size_t>(bh) * sq.nq + grow] = l_sum > 0.f ? (m_used + ptx::lg2(l_sum)) * 0.69314718055994531f : -INFINITY;
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&o_empty[wg]);
     }
   } else {
-    ptx::setmaxnreg_dec<56>();
-    if (warp == 8) {
+    ptx::setmaxnreg_dec<CFG::REG_OTHER>();
+    if (warp == W_MMA || (HB && warp == W_MMA2)) {
       // ================== MMA issuer: whole warp, one elected lane issues ==================
+      // HB: one issuer warp per sub-tile (me), so each sub-tile's S_{j+1} goes into the
+      // tensor pipe as soon as its own softmax has read S_j, independent of the other
+      // sub-tile's progress (a single in-order issuer serialises the two chains: 2380 ->
+      // 1785 cycles per 64-key block).  Otherwise one warp issues for both (me = 0).
+      const int me = warp == W_MMA ? 0 : 1;
       // (E4M3 has format code 0 in the kind::f8f6f4 descriptor, as F16 in kind::f16)
       constexpr uint32_t IDESC_S = ptx::idesc_f16(FP8 ? false : BF16, 128, 128, false, false);
       constexpr uint32_t IDESC_O = ptx::idesc_f16(FP8 ? false : BF16, 128, D, false, true);
@@ -362,7 +437,8 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       uint32_t kphase = 0, vphase = 0;
       uint32_t p_count0 = 0, p_count1 = 0, o_uses0 = 0, o_uses1 = 0;
       int it = 0;
-      auto mma_s = [&](int i, int slot) {
+      constexpr uint32_t IDESC_S64 = ptx::idesc_f16(FP8 ? false : BF16, 128, 64, false, false);
+      auto mma_s = [&](int i, int slot, int sub = 0) {
         // K steps of 32 bytes (16 bf16/fp16 or 32 E4M3 elements), 4 per 128-B swizzle box
 #pragma unroll
         for (int k = 0; k < D * (FP8 ? 1 : 2) / 32; ++k) {
@@ -370,13 +446,15 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           if constexpr (FP8)
             ptx::mma_ss_f8(tmem + i * 128, dQ + ((i * L::TILE + off) >> 4), dK + ((slot * L::TILE + off) >> 4),
                            IDESC_S, k > 0 ? 1u : 0u);
+          else if constexpr (HB)   // block sub of the stage: key rows [64 sub, 64 sub + 64) -> S_i (N = 64)
+            ptx::mma_ss(tmem + TS0 + i * TS_STEP, dQ + ((i * L::TILE + off) >> 4),
+                        dK + ((slot * L::TILE + off + sub * 64 * 128) >> 4), IDESC_S64, k > 0 ? 1u : 0u);
           else
             ptx::mma_ss(tmem + i * 128, dQ + ((i * L::TILE + off) >> 4), dK + ((slot * L::TILE + off) >> 4), IDESC_S,
                         k > 0 ? 1u : 0u);
         }
       };
       // one N = 64 half of S_i = Q_i K^T: key rows [64 h, 64 h + 64) -> S columns [64 h, 64 h + 64)
-      constexpr uint32_t IDESC_S64 = ptx::idesc_f16(FP8 ? false : BF16, 128, 64, false, false);
       auto mma_s_half = [&](int i, int slot, int h) {
 #pragma unroll
         for (int k = 0; k < D * (FP8 ? 1 : 2) / 32; ++k) {
@@ -390,28 +468,29 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
                         k > 0 ? 1u : 0u);
         }
       };
-      auto mma_pv = [&](int i, int slot, bool acc) {
+      auto mma_pv = [&](int i, int slot, bool acc, int sub = 0, int pb = 0) {
         // K = 128 keys: 8 steps of 16 (P~ 16-bit: 8 TMEM columns, V rows 16 x 128 B) or
         // 4 steps of 32 (P~ E4M3: 8 TMEM columns, V rows 32 x 128 B)
         if constexpr (FP8) {
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            ptx::mma_ts_f8(tmem + 256 + i * D, tmem + i * 128 + k * 8, dV + ((slot * L::TILE + k * 4096) >> 4), IDESC_O,
+            ptx::mma_ts_f8(tmem + TO0 + i * D, tmem + i * 128 + k * 8, dV + ((slot * L::TILE + k * 4096) >> 4), IDESC_O,
                            (acc || k > 0) ? 1u : 0u);
         } else {
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
-            ptx::mma_ts(tmem + 256 + i * D, tmem + (SEP_P ? 256 + 2 * D + i * 64 : i * 128) + k * 8,
-                        dV + ((slot * L::TILE + k * 2048) >> 4), IDESC_O, (acc || k > 0) ? 1u : 0u);
+          for (int k = 0; k < BN / 16; ++k)
+            ptx::mma_ts(tmem + TO0 + i * D, tmem + (SEP_P ? TP0 + (i * NPB + pb) * TP_STEP : i * 128) + k * 8,
+                        dV + ((slot * L::TILE + sub * 64 * 128 + k * 2048) >> 4), IDESC_O, (acc || k > 0) ? 1u : 0u);
         }
       };
-      uint32_t s_iss0 = 0, s_iss1 = 0;   // d = 64: S MMAs issued per sub-tile (s_consumed phases)
+      uint32_t s_iss01[2] = {0, 0};   // SEP_P: S MMAs issued per sub-tile (s_consumed phases)
+      uint32_t p_cnt01[2] = {0, 0}, o_use01[2] = {0, 0};   // SEP_P: P~V MMAs / tiles per sub-tile
       uint32_t sc_count0 = 0, sc_count1 = 0;   // d = 128 SPLIT_S: s_consumed phases waited per sub-tile
       // d = 64: S_i into its buffer once softmax i has read the previous S_i
-      auto issue_s_sep = [&](int i, uint32_t& s_iss) {
+      auto issue_s_sep = [&](int i, uint32_t& s_iss, int sub) {
         if (s_iss > 0) ptx::mbar_wait(&s_consumed[i], (s_iss - 1) & 1);
         ptx::tc_fence_after();
-        if (ptx::elect_one()) { mma_s(i, kslot); ptx::mma_commit(&s_full[i]); }
+        if (ptx::elect_one()) { mma_s(i, kslot, sub); ptx::mma_commit(&s_full[i]); }
         __syncwarp();
         ++s_iss;
       };
@@ -421,47 +500,61 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         decode(t, bh, mb, sq);
         const int nb0 = n_blocks(sq, mb, 0), nb1 = n_blocks(sq, mb, 1);
         const int nkv = max(nb0, nb1);
-        ptx::mbar_wait(&q_full[0], it & 1);
-        ptx::mbar_wait(&q_full[1], it & 1);
         if constexpr (SEP_P) {
+          // sub-tiles [i0, i1] of this issuer; HB: every K/V stage is waited for and
+          // released by both issuers (k/v_empty count 2)
+          const int i0 = HB ? me : 0, i1 = HB ? me : 1;
+          uint32_t* s_iss = s_iss01;
+          uint32_t* p_cnt = p_cnt01;
+          uint32_t* o_use = o_use01;
+          for (int i = i0; i <= i1; ++i) ptx::mbar_wait(&q_full[i], it & 1);
           // S_{j+1} is issued as soon as S_j has been read (P~ has its own buffer),
           // so the next block's scores are ready when the softmax finishes block j.
+          // HB: a TMA stage holds two 64-key blocks (sub = j & 1); it is waited for at its
+          // first block and released after its last one
           for (int j = -1; j < nkv; ++j) {
             if (j + 1 < nkv) {
-              ptx::mbar_wait(&k_full[kslot], kphase);
-              if (j + 1 < nb0) issue_s_sep(0, s_iss0);
-              if (j + 1 < nb1) issue_s_sep(1, s_iss1);
-              if (ptx::elect_one()) ptx::mma_commit(&k_empty[kslot]);
-              __syncwarp();
-              if (++kslot == STAGES) { kslot = 0; kphase ^= 1; }
+              const int jn = j + 1, subn = HB ? (jn & 1) : 0;
+              if (subn == 0) ptx::mbar_wait(&k_full[kslot], kphase);
+              if (it == 0) FA2_TRACE(4, me, jn);
+              for (int i = i0; i <= i1; ++i)
+                if (jn < (i == 0 ? nb0 : nb1)) issue_s_sep(i, s_iss[i], subn);
+              if (!HB || subn == 1 || jn + 1 == nkv) {
+                if (ptx::elect_one()) ptx::mma_commit(&k_empty[kslot]);
+                __syncwarp();
+                if (++kslot == STAGES) { kslot = 0; kphase ^= 1; }
+              }
             }
             if (j < 0) continue;
-            ptx::mbar_wait(&v_full[vslot], vphase);
-            auto pv = [&](int i, int nbi, uint32_t& p_count, uint32_t& o_uses) {
+            const int sub = HB ? (j & 1) : 0;
+            if (sub == 0) ptx::mbar_wait(&v_full[vslot], vphase);
+            auto pv = [&](int i, int nbi) {
               if (j >= nbi) return;
               if (j == 0) {
-                if (o_uses > 0) ptx::mbar_wait(&o_empty[i], (o_uses - 1) & 1);
-                ++o_uses;
+                if (o_use[i] > 0) ptx::mbar_wait(&o_empty[i], (o_use[i] - 1) & 1);
+                ++o_use[i];
               }
-              ptx::mbar_wait(&p_full[i], p_count & 1);
-              ++p_count;
+              const uint32_t n = p_cnt[i]++;
+              ptx::mbar_wait(od_bar(p_full, i, n), od_par(n));
               ptx::tc_fence_after();
-              if (ptx::elect_one()) { mma_pv(i, vslot, j > 0); ptx::mma_commit(&o_done[i]); }
+              if (ptx::elect_one()) { mma_pv(i, vslot, j > 0, sub, n % NPB); ptx::mma_commit(od_bar(o_done, i, n)); }
               __syncwarp();
             };
-            pv(0, nb0, p_count0, o_uses0);
-            pv(1, nb1, p_count1, o_uses1);
-            if (ptx::elect_one()) ptx::mma_commit(&v_empty[vslot]);
-            __syncwarp();
-            if (++vslot == STAGES) { vslot = 0; vphase ^= 1; }
+            for (int i = i0; i <= i1; ++i) pv(i, i == 0 ? nb0 : nb1);
+            if (it == 0) FA2_TRACE(5, me, j);
+            if (!HB || sub == 1 || j + 1 == nkv) {
+              if (ptx::elect_one()) ptx::mma_commit(&v_empty[vslot]);
+              __syncwarp();
+              if (++vslot == STAGES) { vslot = 0; vphase ^= 1; }
+            }
           }
-          if (ptx::elect_one()) {
-            ptx::mma_commit(&q_empty[0]);
-            ptx::mma_commit(&q_empty[1]);
-          }
+          if (ptx::elect_one())
+            for (int i = i0; i <= i1; ++i) ptx::mma_commit(&q_empty[i]);
           __syncwarp();
           continue;
         }
+        ptx::mbar_wait(&q_full[0], it & 1);
+        ptx::mbar_wait(&q_full[1], it & 1);
         if (nkv > 0) {
           ptx::mbar_wait(&k_full[kslot], kphase);
           ptx::tc_fence_after();
@@ -499,7 +592,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
                 if (o_uses > 0) ptx::mbar_wait(&o_empty[i], (o_uses - 1) & 1);
                 ++o_uses;
               }
-              ptx::mbar_wait(&p_full[i], p_count & 1);
+              ptx::mbar_wait(od_bar(p_full, i, p_count), od_par(p_count));
               ++p_count;
               if (it == 0) FA2_TRACE(4, i, j);
             }
@@ -509,7 +602,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             }
             ptx::tc_fence_after();
             if (ptx::elect_one()) {
-              if (do_pv) { mma_pv(i, vslot, j > 0); ptx::mma_commit(&o_done[i]); }
+              if (do_pv) { mma_pv(i, vslot, j > 0); ptx::mma_commit(od_bar(o_done, i, p_count - 1)); }
               if (do_s) {
                 if constexpr (SPLIT_S) mma_s_half(i, kslot, 0);
                 else mma_s(i, kslot);
@@ -537,40 +630,44 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         }
         __syncwarp();
       }
-    } else if (warp == 9 && lane == 0) {
-      // ============================ TMA producer ============================
-      int kslot = 0, vslot = 0;
-      uint32_t kphase = 0, vphase = 0;
+    } else if ((warp == W_TMA || warp == W_TMA + 1) && lane == 0) {
+      // ===================== TMA producers: Q + K (warp W_TMA), V (W_TMA + 1) =====================
+      // Two threads, so a K load never queues behind a V slot that the (later) P~V MMAs
+      // still hold: S runs up to two key blocks ahead of P~V.
+      const bool is_k = warp == W_TMA;
+      int slot = 0;
+      uint32_t phase = 0;
       int it = 0;
       const uint64_t pol_kv = ptx::l2_policy_evict_last();
       const uint64_t pol_q = ptx::l2_policy_evict_first();
+      uint64_t* full = is_k ? k_full : v_full;
+      uint64_t* empty = is_k ? k_empty : v_empty;
+      uint8_t* buf = is_k ? sK : sV;
+      const CUtensorMap* tm = is_k ? &tm_k : &tm_v;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
         int bh, mb;
         Seq sq;
         decode(t, bh, mb, sq);
-        const int nkv = max(n_blocks(sq, mb, 0), n_blocks(sq, mb, 1));
+        const int nblk = max(n_blocks(sq, mb, 0), n_blocks(sq, mb, 1));
+        const int nkv = HB ? (nblk + 1) / 2 : nblk;   // 128-row K/V stages
         // key/value head of this query head: implicit index manipulation
         const int h = bh % p.H, kvh = h / p.group;
-        for (int i = 0; i < 2; ++i) {
-          if (it > 0) ptx::mbar_wait(&q_empty[i], (it - 1) & 1);
-          ptx::mbar_arrive_expect_tx(&q_full[i], L::TILE);
-          for (int s = 0; s < NSUB; ++s)
-            tma_load_rows<GEN>(sQ + i * L::TILE + s * L::SUB, &tm_q, &q_full[i], p.geom, s * 64, sq.q0 + mb * 256 + i * 128,
-                          h, sq.bc, p.H, pol_q);
+        if (is_k) {
+          for (int i = 0; i < 2; ++i) {
+            if (it > 0) ptx::mbar_wait(&q_empty[i], (it - 1) & 1);
+            ptx::mbar_arrive_expect_tx(&q_full[i], L::TILE);
+            for (int s = 0; s < NSUB; ++s)
+              tma_load_rows<GEN>(sQ + i * L::TILE + s * L::SUB, &tm_q, &q_full[i], p.geom, s * 64,
+                                 sq.q0 + mb * 256 + i * 128, h, sq.bc, p.H, pol_q);
+          }
         }
         for (int j = 0; j < nkv; ++j) {
-          ptx::mbar_wait(&k_empty[kslot], kphase ^ 1);
-          ptx::mbar_arrive_expect_tx(&k_full[kslot], L::TILE);
+          ptx::mbar_wait(&empty[slot], phase ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[slot], L::TILE);
           for (int s = 0; s < NSUB; ++s)
-            tma_load_rows<GEN>(sK + kslot * L::TILE + s * L::SUB, &tm_k, &k_full[kslot], p.geom, s * 64, sq.k0 + j * 128,
-                          kvh, sq.bc, p.Hkv, pol_kv);
-          if (++kslot == STAGES) { kslot = 0; kphase ^= 1; }
-          ptx::mbar_wait(&v_empty[vslot], vphase ^ 1);
-          ptx::mbar_arrive_expect_tx(&v_full[vslot], L::TILE);
-          for (int s = 0; s < NSUB; ++s)
-            tma_load_rows<GEN>(sV + vslot * L::TILE + s * L::SUB, &tm_v, &v_full[vslot], p.geom, s * 64, sq.k0 + j * 128,
-                          kvh, sq.bc, p.Hkv, pol_kv);
-          if (++vslot == STAGES) { vslot = 0; vphase ^= 1; }
+            tma_load_rows<GEN>(buf + slot * L::TILE + s * L::SUB, tm, &full[slot], p.geom, s * 64, sq.k0 + j * 128,
+                               kvh, sq.bc, p.Hkv, pol_kv);
+          if (++slot == STAGES) { slot = 0; phase ^= 1; }
         }
       }
     }
