@@ -9,6 +9,10 @@
 #include <string>
 #include <mutex>
 #include <algorithm>
+#include <map>
+#include <memory>
+#include <tuple>
+#include <vector>
 
 #include "../../include/fa2.h"
 #include "fa2_fwd_sm100.cuh"
@@ -198,6 +202,65 @@ fa2_status_t set_smem(K kernel, int bytes) {
 // ----------------------------------------------------------------------------
 // Forward
 // ----------------------------------------------------------------------------
+#ifndef FA2_FWD_SCHED
+#define FA2_FWD_SCHED 1   // 0: static stride schedule for every forward (A/B builds)
+#endif
+// Balanced schedule of the causal square forward (see fa2::FwdSched): tiles in windows
+// of heads (K/V of a window ~ 64k key rows, which stays in L2), heaviest first inside a
+// window, each assigned to the least-loaded CTA.  Tile work = key blocks of its two
+// sub-tiles + 1 (prologue/epilogue).  Memoised per shape (host-side cache).
+void build_fwd_sched(fa2::FwdSched& sc, const fa2::FwdParams& p, int grid) {
+  const int nmb = p.num_m_blocks, T = p.num_tiles, N = p.geom.Nq;
+  const int nkb = (N + 127) / 128;
+  std::vector<int> work(T), ord(T);
+  for (int t = 0; t < T; ++t) {
+    const int mb = nmb - 1 - t % nmb;   // the kernel's causal decode (heavy row blocks first)
+    int w = 1;
+    for (int i = 0; i < 2; ++i) {
+      const int r0 = mb * 256 + i * 128;
+      if (r0 < N) w += std::min(nkb, std::min(N - 1, r0 + 127) / 128 + 1);
+    }
+    work[t] = w;
+    ord[t] = t;
+  }
+  const int W = std::max(1, 65536 / std::max(1, N));   // heads per window
+  std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
+    const int wa = (a / nmb) / W, wb = (b / nmb) / W;
+    return wa != wb ? wa < wb : work[a] > work[b];
+  });
+  std::vector<std::vector<uint16_t>> lists(grid);
+  std::vector<std::pair<long long, int>> heap;   // (load, cta), min-heap
+  for (int c = 0; c < grid; ++c) heap.emplace_back(0LL, c);
+  auto cmp = [](const std::pair<long long, int>& a, const std::pair<long long, int>& b) { return a > b; };
+  std::make_heap(heap.begin(), heap.end(), cmp);
+  for (int t : ord) {
+    std::pop_heap(heap.begin(), heap.end(), cmp);
+    heap.back().first += work[t];
+    lists[heap.back().second].push_back(static_cast<uint16_t>(t));
+    std::push_heap(heap.begin(), heap.end(), cmp);
+  }
+  int pos = 0;
+  for (int c = 0; c < grid; ++c) {
+    sc.start[c] = static_cast<uint16_t>(pos);
+    for (uint16_t t : lists[c]) sc.order[pos++] = t;
+  }
+  sc.start[grid] = static_cast<uint16_t>(pos);
+  sc.n = T;
+}
+
+const fa2::FwdSched& fwd_sched(const fa2::FwdParams& p, int grid) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int, int>, std::unique_ptr<fa2::FwdSched>> cache;
+  const auto key = std::make_tuple(p.num_tiles, p.num_m_blocks, p.geom.Nq, grid);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return *it->second;
+  if (cache.size() > 256) cache.clear();
+  auto sc = std::make_unique<fa2::FwdSched>();
+  build_fwd_sched(*sc, p, grid);
+  return *cache.emplace(key, std::move(sc)).first->second;
+}
+
 template <int D, bool BF16, bool CAUSAL, bool GEN, bool FP8 = false>
 fa2_status_t launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const fa2::FwdParams& p,
                         int sms, cudaStream_t st) {
@@ -206,8 +269,20 @@ fa2_status_t launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUte
   fa2_status_t s = set_smem(kern, smem);
   if (s != FA2_OK) return s;
   const int grid = p.num_tiles < sms ? p.num_tiles : sms;
+  fa2::FwdSchedT<CAUSAL, GEN> sched;
+  sched.n = 0;
+  if constexpr (CAUSAL && !GEN) {
+    if (FA2_FWD_SCHED && p.num_tiles <= fa2::kFwdSchedMaxTiles && grid <= fa2::kFwdSchedMaxCtas) {
+      const fa2::FwdSched& sc = fwd_sched(p, grid);
+      mark(0, st);
+      kern<<<grid, fa2::FwdCfg<D, FP8>::THREADS, smem, st>>>(mq, mk, mv, p, sc);
+      mark(1, st);
+      FA2_CUDA(cudaGetLastError());
+      return FA2_OK;
+    }
+  }
   mark(0, st);
-  kern<<<grid, fa2::FwdCfg<D, FP8>::THREADS, smem, st>>>(mq, mk, mv, p);
+  kern<<<grid, fa2::FwdCfg<D, FP8>::THREADS, smem, st>>>(mq, mk, mv, p, sched);
   mark(1, st);
   FA2_CUDA(cudaGetLastError());
   return FA2_OK;

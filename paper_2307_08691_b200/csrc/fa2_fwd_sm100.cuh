@@ -96,6 +96,26 @@ struct FwdParams {
       p.trace[((ev) * 2 + (who)) * 64 + (j)] = clock64();                              \
   } while (0)
 
+// Causal, square fixed-length path: a host-computed balanced tile schedule.  Work tiles
+// of a causal head differ in length (row block mb visits mb + 1 key blocks), and the
+// static stride schedule (CTA c takes tiles c, c + G, ...) leaves the busiest CTA with
+// 1.15-1.4x the mean work at the paper's shapes.  The host assigns tiles greedily
+// (heaviest first, to the least-loaded CTA) inside windows of heads whose K/V fit in
+// L2 together, and passes every CTA's list as a kernel parameter (no device memory,
+// no global state on the device).  n == 0: static stride schedule.
+constexpr int kFwdSchedMaxTiles = 8192;
+constexpr int kFwdSchedMaxCtas = 160;
+struct FwdSched {
+  int n;                                  // number of tiles (0: no table)
+  uint16_t start[kFwdSchedMaxCtas + 1];   // CTA c's tiles: order[start[c] .. start[c + 1])
+  uint16_t order[kFwdSchedMaxTiles];
+};
+struct FwdNoSched {
+  int n;
+};
+template <bool CAUSAL, bool GEN>
+using FwdSchedT = typename std::conditional<CAUSAL && !GEN, FwdSched, FwdNoSched>::type;
+
 template <int D, int EB = 2>   // EB: bytes per Q/K/V element (2: bf16/fp16, 1: FP8)
 struct FwdSmem {
   static constexpr int BM = 128, BN = 128;
@@ -121,7 +141,8 @@ struct FwdSmem {
 template <int D, bool BF16, bool CAUSAL, bool GEN, bool FP8 = false>
 __global__ void __launch_bounds__(FwdCfg<D, FP8>::THREADS, 1)
 fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-               const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
+               const __grid_constant__ CUtensorMap tm_v, const FwdParams p,
+               const __grid_constant__ FwdSchedT<CAUSAL, GEN> sched) {
   static_assert(!FP8 || (D == 128 && BF16), "FP8 forward: d = 128, bf16 output");
   using L = FwdSmem<D, FP8 ? 1 : 2>;
   using CFG = FwdCfg<D, FP8>;
@@ -208,6 +229,17 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   const uint32_t tmem = *tmem_slot;
 
 
+  // n-th work tile of this CTA (-1: done), shared by all roles
+  auto tile_at = [&](int n) -> int {
+    if constexpr (CAUSAL && !GEN) {
+      if (sched.n > 0) {
+        const int i = sched.start[blockIdx.x] + n;
+        return i < sched.start[blockIdx.x + 1] ? sched.order[i] : -1;
+      }
+    }
+    const int t = blockIdx.x + n * gridDim.x;
+    return t < p.num_tiles ? t : -1;
+  };
   // Work-tile decode, shared by all roles.  Heads are contiguous in the tile
   // order so that the CTAs running concurrently share K/V in L2; for causal the
   // heavy (late) row blocks of each head come first.  sq: the tile's sequence.
@@ -249,7 +281,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     uint32_t s_count = 0;   // completed waits on s_full[wg]
     uint32_t pv_count = 0;  // PV MMAs issued so far for this sub-tile (all tiles)
     const float sl2 = p.scale_log2;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+    for (int n = 0, t; (t = tile_at(n)) >= 0; ++n) {
       int bh, mb;
       Seq sq;
       decode(t, bh, mb, sq);
@@ -274,7 +306,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         ptx::mbar_wait(&s_full[wg], s_count & 1);
         const int par = s_count & 1;
         ++s_count;
-        if (threadIdx.x % (128 * RS) == 0 && t == (int)blockIdx.x) FA2_TRACE(0, wg, j);
+        if (threadIdx.x % (128 * RS) == 0 && n == 0) FA2_TRACE(0, wg, j);
         ptx::tc_fence_after();
         uint32_t su[COLS];
 #pragma unroll
@@ -308,7 +340,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           ptx::named_bar_sync(bar_id, 64);
           mx = fmaxf(mx, other[row]);
         }
-        if (threadIdx.x % (128 * RS) == 0 && t == (int)blockIdx.x) FA2_TRACE(1, wg, j);
+        if (threadIdx.x % (128 * RS) == 0 && n == 0) FA2_TRACE(1, wg, j);
         const float m_new = fmaxf(m_used, mx * sl2);
         const bool rescale = (m_new - m_used) > 8.0f;   // also true when m_used == -inf and m_new finite
         float alpha = 1.f;
@@ -358,7 +390,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         if (need_mask) exp_block(std::integral_constant<int, 0>{});
         else exp_block(std::integral_constant<int, D == 64 ? kFwdEmuPairsD64 : kFwdEmuPairs>{});
         l_sum = l_sum * alpha + (rs2.x + rs2.y);
-        if (threadIdx.x % (128 * RS) == 0 && t == (int)blockIdx.x) FA2_TRACE(2, wg, j);
+        if (threadIdx.x % (128 * RS) == 0 && n == 0) FA2_TRACE(2, wg, j);
         // Rescale the un-normalised O accumulator before P~_j V_j is added
         // (needs PV_{j-1} finished; it was issued before S_j, so it usually is).
         if (j > 0 && __any_sync(0xffffffffu, rescale)) {
@@ -378,7 +410,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(od_bar(p_full, wg, pv_count));
-        if (threadIdx.x % (128 * RS) == 0 && t == (int)blockIdx.x) FA2_TRACE(3, wg, j);
+        if (threadIdx.x % (128 * RS) == 0 && n == 0) FA2_TRACE(3, wg, j);
         ++pv_count;
       }
       // ---- epilogue: O = O / l, L = m + log l (natural log) ----
@@ -494,7 +526,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         __syncwarp();
         ++s_iss;
       };
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+      for (int n = 0, t; (t = tile_at(n)) >= 0; ++n, ++it) {
         int bh, mb;
         Seq sq;
         decode(t, bh, mb, sq);
@@ -644,7 +676,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       uint64_t* empty = is_k ? k_empty : v_empty;
       uint8_t* buf = is_k ? sK : sV;
       const CUtensorMap* tm = is_k ? &tm_k : &tm_v;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+      for (int n = 0, t; (t = tile_at(n)) >= 0; ++n, ++it) {
         int bh, mb;
         Seq sq;
         decode(t, bh, mb, sq);
