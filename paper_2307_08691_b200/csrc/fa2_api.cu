@@ -202,36 +202,24 @@ fa2_status_t set_smem(K kernel, int bytes) {
 // ----------------------------------------------------------------------------
 // Forward
 // ----------------------------------------------------------------------------
-#ifndef FA2_FWD_SCHED
-#define FA2_FWD_SCHED 1   // 0: static stride schedule for every forward (A/B builds)
+#ifndef FA2_SCHED
+#define FA2_SCHED 1   // 0: static stride schedule everywhere (A/B builds)
 #endif
-// Balanced schedule of the causal square forward (see fa2::FwdSched): tiles in windows
-// of heads (K/V of a window ~ 64k key rows, which stays in L2), heaviest first inside a
-// window, each assigned to the least-loaded CTA.  Tile work = key blocks of its two
-// sub-tiles + 1 (prologue/epilogue).  Memoised per shape (host-side cache).
-void build_fwd_sched(fa2::FwdSched& sc, const fa2::FwdParams& p, int grid) {
-  const int nmb = p.num_m_blocks, T = p.num_tiles, N = p.geom.Nq;
-  const int nkb = (N + 127) / 128;
-  std::vector<int> work(T), ord(T);
-  for (int t = 0; t < T; ++t) {
-    const int mb = nmb - 1 - t % nmb;   // the kernel's causal decode (heavy row blocks first)
-    int w = 1;
-    for (int i = 0; i < 2; ++i) {
-      const int r0 = mb * 256 + i * 128;
-      if (r0 < N) w += std::min(nkb, std::min(N - 1, r0 + 127) / 128 + 1);
-    }
-    work[t] = w;
-    ord[t] = t;
-  }
-  const int W = std::max(1, 65536 / std::max(1, N));   // heads per window
+// Balanced schedules (fa2::TileSched): tiles in windows of heads (window = `win` tiles
+// of consecutive heads, ~64k rows of K/V or Q/dO, which stays in L2), heaviest first
+// inside a window, each assigned to the least-loaded CTA.  Memoised per shape.
+void build_sched(fa2::TileSched& sc, const std::vector<int>& work, int tiles_per_head, int heads_per_win, int grid) {
+  const int T = static_cast<int>(work.size());
+  std::vector<int> ord(T);
+  for (int t = 0; t < T; ++t) ord[t] = t;
   std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
-    const int wa = (a / nmb) / W, wb = (b / nmb) / W;
+    const int wa = (a / tiles_per_head) / heads_per_win, wb = (b / tiles_per_head) / heads_per_win;
     return wa != wb ? wa < wb : work[a] > work[b];
   });
   std::vector<std::vector<uint16_t>> lists(grid);
   std::vector<std::pair<long long, int>> heap;   // (load, cta), min-heap
   for (int c = 0; c < grid; ++c) heap.emplace_back(0LL, c);
-  auto cmp = [](const std::pair<long long, int>& a, const std::pair<long long, int>& b) { return a > b; };
+  auto cmp = [](const std::pair<long long, int>& x, const std::pair<long long, int>& y) { return x > y; };
   std::make_heap(heap.begin(), heap.end(), cmp);
   for (int t : ord) {
     std::pop_heap(heap.begin(), heap.end(), cmp);
@@ -248,17 +236,49 @@ void build_fwd_sched(fa2::FwdSched& sc, const fa2::FwdParams& p, int grid) {
   sc.n = T;
 }
 
-const fa2::FwdSched& fwd_sched(const fa2::FwdParams& p, int grid) {
+// key: (kind, tiles, tiles per head, rows, heads per tile, grid); make_work(work) fills the tile works
+template <typename F>
+const fa2::TileSched& cached_sched(int kind, int T, int tiles_per_head, int N, int nh, int grid, F make_work) {
   static std::mutex mu;
-  static std::map<std::tuple<int, int, int, int>, std::unique_ptr<fa2::FwdSched>> cache;
-  const auto key = std::make_tuple(p.num_tiles, p.num_m_blocks, p.geom.Nq, grid);
+  static std::map<std::tuple<int, int, int, int, int, int>, std::unique_ptr<fa2::TileSched>> cache;
+  const auto key = std::make_tuple(kind, T, tiles_per_head, N, nh, grid);
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
   if (it != cache.end()) return *it->second;
   if (cache.size() > 256) cache.clear();
-  auto sc = std::make_unique<fa2::FwdSched>();
-  build_fwd_sched(*sc, p, grid);
+  auto sc = std::make_unique<fa2::TileSched>();
+  std::vector<int> work(T);
+  make_work(work);
+  build_sched(*sc, work, tiles_per_head, std::max(1, 65536 / std::max(1, N)), grid);
   return *cache.emplace(key, std::move(sc)).first->second;
+}
+
+// Forward (causal, square): tile t = (head, row block mb = nmb - 1 - t % nmb), work = key
+// blocks of its two 128-row sub-tiles + 1 (prologue / epilogue).
+const fa2::TileSched& fwd_sched(const fa2::FwdParams& p, int grid) {
+  const int nmb = p.num_m_blocks, N = p.geom.Nq;
+  return cached_sched(0, p.num_tiles, nmb, N, 1, grid, [&](std::vector<int>& work) {
+    const int nkb = (N + 127) / 128;
+    for (int t = 0; t < p.num_tiles; ++t) {
+      const int mb = nmb - 1 - t % nmb;
+      int w = 1;
+      for (int i = 0; i < 2; ++i) {
+        const int r0 = mb * 256 + i * 128;
+        if (r0 < N) w += std::min(nkb, std::min(N - 1, r0 + 127) / 128 + 1);
+      }
+      work[t] = w;
+    }
+  });
+}
+
+// Backward (causal, square, arrival-order dQ): tile t = (head split, key block nb = t % nnb),
+// work = query tiles i >= nb times the query heads of the tile, + 1.
+const fa2::TileSched& bwd_sched(const fa2::BwdParams& p, int grid) {
+  const int nnb = p.num_n_blocks, N = p.geom.Nq, nh = p.group / p.hsplit;
+  return cached_sched(1, p.num_tiles, nnb, N, nh, grid, [&](std::vector<int>& work) {
+    const int nqb = (N + 127) / 128;
+    for (int t = 0; t < p.num_tiles; ++t) work[t] = (nqb - t % nnb) * nh + 1;
+  });
 }
 
 template <int D, bool BF16, bool CAUSAL, bool GEN, bool FP8 = false>
@@ -272,8 +292,8 @@ fa2_status_t launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUte
   fa2::FwdSchedT<CAUSAL, GEN> sched;
   sched.n = 0;
   if constexpr (CAUSAL && !GEN) {
-    if (FA2_FWD_SCHED && p.num_tiles <= fa2::kFwdSchedMaxTiles && grid <= fa2::kFwdSchedMaxCtas) {
-      const fa2::FwdSched& sc = fwd_sched(p, grid);
+    if (FA2_SCHED && p.num_tiles <= fa2::kSchedMaxTiles && grid <= fa2::kSchedMaxCtas) {
+      const fa2::TileSched& sc = fwd_sched(p, grid);
       mark(0, st);
       kern<<<grid, fa2::FwdCfg<D, FP8>::THREADS, smem, st>>>(mq, mk, mv, p, sc);
       mark(1, st);
@@ -481,7 +501,7 @@ fa2_status_t make_acc_map(CUtensorMap* m, float* dq_acc, int d, long long rows) 
   return FA2_OK;
 }
 
-template <typename Kern>
+template <bool SCHED, typename Kern>
 fa2_status_t launch_bwd_kernel(Kern kern, int smem, const fa2::BwdMaps& maps, const fa2::BwdParams& p, int sms,
                                cudaStream_t st) {
   fa2_status_t s = set_smem(kern, smem);
@@ -489,8 +509,20 @@ fa2_status_t launch_bwd_kernel(Kern kern, int smem, const fa2::BwdMaps& maps, co
   int grid = p.num_tiles < sms ? p.num_tiles : sms;
   // deterministic cyclic schedule: whole heads per wave (see bwd_q_tile in fa2_bwd_sm100.cuh)
   if (p.dq_sem != nullptr && p.det_cyclic) grid = (grid / p.num_n_blocks) * p.num_n_blocks;
+  fa2::SchedT<SCHED> sched;
+  sched.n = 0;
+  if constexpr (SCHED) {   // causal square arrival-order backward: balanced tile lists
+    if (FA2_SCHED && p.dq_sem == nullptr && p.num_tiles <= fa2::kSchedMaxTiles && grid <= fa2::kSchedMaxCtas) {
+      const fa2::TileSched& sc = bwd_sched(p, grid);
+      mark(3, st);
+      kern<<<grid, fa2::kBwdThreads, smem, st>>>(maps.q, maps.k, maps.v, maps.dout, maps.dq_acc, p, sc);
+      mark(4, st);
+      FA2_CUDA(cudaGetLastError());
+      return FA2_OK;
+    }
+  }
   mark(3, st);
-  kern<<<grid, fa2::kBwdThreads, smem, st>>>(maps.q, maps.k, maps.v, maps.dout, maps.dq_acc, p);
+  kern<<<grid, fa2::kBwdThreads, smem, st>>>(maps.q, maps.k, maps.v, maps.dout, maps.dq_acc, p, sched);
   mark(4, st);
   FA2_CUDA(cudaGetLastError());
   return FA2_OK;
@@ -500,9 +532,11 @@ template <int D, bool BF16, bool CAUSAL, bool GEN>
 fa2_status_t launch_bwd(const fa2::BwdMaps& maps, const fa2::BwdParams& p, int sms, cudaStream_t st) {
   // d = 128: fa2_bwd128_sm100.cuh; d = 64: fa2_bwd_kernel
   if constexpr (D == 128)
-    return launch_bwd_kernel(fa2::fa2_bwd128_kernel<BF16, CAUSAL, GEN>, fa2::Bwd128Smem::ALLOC, maps, p, sms, st);
+    return launch_bwd_kernel<CAUSAL && !GEN>(fa2::fa2_bwd128_kernel<BF16, CAUSAL, GEN>, fa2::Bwd128Smem::ALLOC, maps, p,
+                                             sms, st);
   else
-    return launch_bwd_kernel(fa2::fa2_bwd_kernel<D, BF16, CAUSAL, GEN>, fa2::BwdSmem<D>::ALLOC, maps, p, sms, st);
+    return launch_bwd_kernel<CAUSAL && !GEN>(fa2::fa2_bwd_kernel<D, BF16, CAUSAL, GEN>, fa2::BwdSmem<D>::ALLOC, maps, p,
+                                             sms, st);
 }
 
 template <int D, bool BF16>

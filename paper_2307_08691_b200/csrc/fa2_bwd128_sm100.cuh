@@ -61,7 +61,8 @@ template <bool BF16, bool CAUSAL, bool GEN>
 __global__ void __launch_bounds__(kBwdThreads, 1)
 fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
-                  const __grid_constant__ CUtensorMap tm_dq, const BwdParams p) {
+                  const __grid_constant__ CUtensorMap tm_dq, const BwdParams p,
+               const __grid_constant__ SchedT<CAUSAL && !GEN> sched) {
   using L = Bwd128Smem;
   constexpr int D = 128, BM = 128, NSUB = 2;
   extern __shared__ uint8_t smem_raw[];
@@ -132,7 +133,7 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
     const int c0 = wg * 64;                             // this warpgroup's 64 query columns
     uint32_t g = 0;
     int it = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+    for (int n_ = 0, t; (t = sched_tile(sched, n_, p.num_tiles)) >= 0; ++n_) {
       BwdTile w;
       if (!bwd_tile<GEN>(p, CAUSAL, t, w)) continue;
       const int nb = w.nb, nqt = w.nqt, nk = w.sq.nk, off = w.sq.off;
@@ -276,7 +277,7 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
     const bool leader = (r == 0);
     const uint32_t sDQ_a = ptx::smem_u32(sDQ);
     uint32_t g = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+    for (int n_ = 0, t; (t = sched_tile(sched, n_, p.num_tiles)) >= 0; ++n_) {
       BwdTile w;
       if (!bwd_tile<GEN>(p, CAUSAL, t, w) || w.nqt == 0) continue;
       const int nb = w.nb, nqt = w.nqt;
@@ -355,7 +356,7 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
     uint32_t g = 0;
     int it = 0;
     uint32_t dkv_uses = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+    for (int n_ = 0, t; (t = sched_tile(sched, n_, p.num_tiles)) >= 0; ++n_) {
       BwdTile w;
       if (!bwd_tile<GEN>(p, CAUSAL, t, w) || w.nqt == 0) continue;
       const uint32_t n = static_cast<uint32_t>(w.nqt * w.nh);
@@ -438,7 +439,7 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
       int it = 0;
       const uint64_t pol_q = ptx::l2_policy_evict_last();
       const uint64_t pol_kv = ptx::l2_policy_evict_first();
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      for (int n_ = 0, t; (t = sched_tile(sched, n_, p.num_tiles)) >= 0; ++n_) {
         BwdTile w;
         if (!bwd_tile<GEN>(p, CAUSAL, t, w) || w.nqt == 0) continue;
         const int nb = w.nb, nqt = w.nqt;

@@ -381,7 +381,8 @@ template <int D, bool BF16, bool CAUSAL, bool GEN>
 __global__ void __launch_bounds__(kBwdThreads, 1)
 fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
-               const __grid_constant__ CUtensorMap tm_dq, const BwdParams p) {
+               const __grid_constant__ CUtensorMap tm_dq, const BwdParams p,
+               const __grid_constant__ SchedT<CAUSAL && !GEN> sched) {
   using L = BwdSmem<D>;
   constexpr int BM = L::BM;
   constexpr int STAGES = L::STAGES;
@@ -457,7 +458,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     const uint32_t sVec_a = ptx::smem_u32(sVec), sDST_a = ptx::smem_u32(sDST);
     uint32_t g = 0;          // global query-tile counter
     int it = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+    for (int n_ = 0, t; (t = sched_tile(sched, n_, p.num_tiles)) >= 0; ++n_) {
       BwdTile w;
       if (!bwd_tile<GEN>(p, CAUSAL, t, w)) continue;
       const int nb = w.nb, nqt = w.nqt, nk = w.sq.nk, off = w.sq.off;
@@ -594,7 +595,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     const bool leader = (r == 0);
     const uint32_t sDQ_a = ptx::smem_u32(sDQ);
     uint32_t g = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+    for (int n_ = 0, t; (t = sched_tile(sched, n_, p.num_tiles)) >= 0; ++n_) {
       BwdTile w;
       if (!bwd_tile<GEN>(p, CAUSAL, t, w) || w.nqt == 0) continue;
       const int nb = w.nb, nqt = w.nqt;
@@ -709,7 +710,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       __syncwarp();
       FA2_BTRACE(6, h);
     };
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+    for (int n_ = 0, t; (t = sched_tile(sched, n_, p.num_tiles)) >= 0; ++n_) {
       BwdTile w;
       if (!bwd_tile<GEN>(p, CAUSAL, t, w) || w.nqt == 0) continue;
       ptx::mbar_wait(kv_full, it & 1);
@@ -760,7 +761,7 @@ fa2_bwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       int it = 0;
       const uint64_t pol_q = ptx::l2_policy_evict_last();
       const uint64_t pol_kv = ptx::l2_policy_evict_first();
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      for (int n_ = 0, t; (t = sched_tile(sched, n_, p.num_tiles)) >= 0; ++n_) {
         BwdTile w;
         if (!bwd_tile<GEN>(p, CAUSAL, t, w) || w.nqt == 0) continue;
         const int nb = w.nb, nqt = w.nqt;

@@ -96,25 +96,9 @@ struct FwdParams {
       p.trace[((ev) * 2 + (who)) * 64 + (j)] = clock64();                              \
   } while (0)
 
-// Causal, square fixed-length path: a host-computed balanced tile schedule.  Work tiles
-// of a causal head differ in length (row block mb visits mb + 1 key blocks), and the
-// static stride schedule (CTA c takes tiles c, c + G, ...) leaves the busiest CTA with
-// 1.15-1.4x the mean work at the paper's shapes.  The host assigns tiles greedily
-// (heaviest first, to the least-loaded CTA) inside windows of heads whose K/V fit in
-// L2 together, and passes every CTA's list as a kernel parameter (no device memory,
-// no global state on the device).  n == 0: static stride schedule.
-constexpr int kFwdSchedMaxTiles = 8192;
-constexpr int kFwdSchedMaxCtas = 160;
-struct FwdSched {
-  int n;                                  // number of tiles (0: no table)
-  uint16_t start[kFwdSchedMaxCtas + 1];   // CTA c's tiles: order[start[c] .. start[c + 1])
-  uint16_t order[kFwdSchedMaxTiles];
-};
-struct FwdNoSched {
-  int n;
-};
+// Causal, square fixed-length path: host-computed balanced tile schedule (fa2_seq.cuh).
 template <bool CAUSAL, bool GEN>
-using FwdSchedT = typename std::conditional<CAUSAL && !GEN, FwdSched, FwdNoSched>::type;
+using FwdSchedT = SchedT<CAUSAL && !GEN>;
 
 template <int D, int EB = 2>   // EB: bytes per Q/K/V element (2: bf16/fp16, 1: FP8)
 struct FwdSmem {
@@ -230,16 +214,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 
 
   // n-th work tile of this CTA (-1: done), shared by all roles
-  auto tile_at = [&](int n) -> int {
-    if constexpr (CAUSAL && !GEN) {
-      if (sched.n > 0) {
-        const int i = sched.start[blockIdx.x] + n;
-        return i < sched.start[blockIdx.x + 1] ? sched.order[i] : -1;
-      }
-    }
-    const int t = blockIdx.x + n * gridDim.x;
-    return t < p.num_tiles ? t : -1;
-  };
+  auto tile_at = [&](int n) -> int { return sched_tile(sched, n, p.num_tiles); };
   // Work-tile decode, shared by all roles.  Heads are contiguous in the tile
   // order so that the CTAs running concurrently share K/V in L2; for causal the
   // heavy (late) row blocks of each head come first.  sq: the tile's sequence.

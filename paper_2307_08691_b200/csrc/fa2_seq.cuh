@@ -9,9 +9,43 @@
 // so the row coordinate is dimension 1 or 2; both give the same 128-row x 128-B
 // swizzled SMEM tile (box {64, 128, 1} or {64, 1, 128}).
 #pragma once
+#include <type_traits>
 #include "sm100_ptx.cuh"
 
 namespace fa2 {
+
+// Balanced static tile schedule (causal, square fixed-length paths of the forward and the
+// arrival-order backward).  Causal work tiles differ in length, and the static stride
+// schedule (CTA c takes tiles c, c + G, ...) leaves the busiest CTA with 1.15-1.4x the
+// mean work at the paper's shapes.  The host assigns tiles greedily (heaviest first, to
+// the least-loaded CTA) inside windows of heads whose K/V (forward) or Q/dO (backward)
+// fit in L2 together, and passes every CTA's list as a kernel parameter: no device
+// memory, no global state on the device.  n == 0: static stride schedule.
+constexpr int kSchedMaxTiles = 8192;
+constexpr int kSchedMaxCtas = 160;
+struct TileSched {
+  int n;                               // number of tiles (0: no table)
+  uint16_t start[kSchedMaxCtas + 1];   // CTA c's tiles: order[start[c] .. start[c + 1])
+  uint16_t order[kSchedMaxTiles];
+};
+struct NoSched {
+  int n;
+};
+template <bool ON>
+using SchedT = typename std::conditional<ON, TileSched, NoSched>::type;
+
+// n-th work tile of this CTA (-1: none left)
+template <class S>
+FA2_DEVICE int sched_tile(const S& sc, int n, int num_tiles) {
+  if constexpr (std::is_same<S, TileSched>::value) {
+    if (sc.n > 0) {
+      const int i = sc.start[blockIdx.x] + n;
+      return i < sc.start[blockIdx.x + 1] ? sc.order[i] : -1;
+    }
+  }
+  const int t = blockIdx.x + n * gridDim.x;
+  return t < num_tiles ? t : -1;
+}
 
 struct SeqGeom {
   const int* cu_q;     // packed: [B+1] query row offsets (device); nullptr: fixed lengths
