@@ -32,7 +32,12 @@ def to_bytes(unit, val):
     return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
 
 
-def summarise(rep, name):
+# algorithmic FLOPs per launch at the bench workload (B=2, H=16, N=8192, d=128, non-causal;
+# paper count P:617-625): forward 4 N^2 d B H, backward 2.5x that
+FLOPS = {"fwd": 4.0 * 8192 ** 2 * 128 * 32, "bwd": 2.5 * 4.0 * 8192 ** 2 * 128 * 32}
+
+
+def summarise(rep, name, key=None):
     h, u, v = raw(rep)
     m = {n: (u[i], v[i]) for i, n in enumerate(h)}
     kname = v[h.index("Kernel Name")] if "Kernel Name" in h else name
@@ -44,6 +49,17 @@ def summarise(rep, name):
     if "dram__bytes_read.sum" in m and "dram__bytes_write.sum" in m:
         traffic = to_bytes(*m["dram__bytes_read.sum"]) + to_bytes(*m["dram__bytes_write.sum"])
         lines.append(f"| DRAM traffic per launch | {traffic/1e6:.1f} MB |")
+    if key in FLOPS and "gpu__time_duration.sum" in m and "sm__cycles_elapsed.avg.per_second" in m:
+        un, dur = m["gpu__time_duration.sum"]
+        sec = float(dur.replace(",", "")) * {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "nsecond": 1e-9, "ms": 1e-3,
+                                             "msecond": 1e-3}.get(un, 1e-9)
+        cu, clk = m["sm__cycles_elapsed.avg.per_second"]
+        hz = float(clk.replace(",", "")) * {"Ghz": 1e9, "Mhz": 1e6, "hz": 1}.get(cu, 1e9)
+        tf = FLOPS[key] / sec / 1e12
+        at_clock = 148 * 8192 * hz / 1e12   # dense bf16 floor: 8192 FLOP/clk/SM
+        lines.append(f"| achieved (algorithmic FLOPs / duration) | {tf:.0f} TFLOP/s |")
+        lines.append(f"| tensor utilisation at the captured SM clock (achieved / (148 x 8192 FLOP/clk x clock)) "
+                     f"| {100 * tf / at_clock:.1f}% |")
     return "\n".join(lines) + "\n", traffic
 
 
@@ -71,7 +87,10 @@ if __name__ == "__main__":
              "Captured with `ncu --set full --clock-control none` (one launch each, 1 GPU) on the bench.py workload "
              "(PS-128: B=2, H=16, N=8192, d=128, bf16, non-causal).  Launch list: "
              "`ncu --metrics gpu__time_duration.sum --clock-control none` over `bench.py --steps 2 --warmup 3` "
-             "(cold-cache, serialised: compare shares, not absolutes).", ""]
+             "(cold-cache, serialised: compare shares, not absolutes).  The `sm__pipe_tensor_cycles_active_realtime` "
+             "percentage is not stable across captures of the same kernel (49% and 25% at the same duration); the "
+             "computed tensor-utilisation row (algorithmic FLOPs / duration against 8192 FLOP/clk/SM at the captured "
+             "clock) is the direct measure.", ""]
     lf = os.path.join(g, f"{tag}_launches.csv")
     if os.path.exists(lf):
         parts += ["## Launch list (our kernels)", "", launches(lf)]
@@ -80,7 +99,7 @@ if __name__ == "__main__":
                        ("pre", "fa2_bwd_preprocess"), ("dq", "fa2_dq_convert")):
         rep = os.path.join(g, f"{tag}_prof_{key}.ncu-rep")
         if os.path.exists(rep):
-            md, t = summarise(rep, label)
+            md, t = summarise(rep, label, key)
             parts += [md]
             traffic[{"fwd": "fwd", "bwd": "bwd_main", "pre": "bwd_pre", "dq": "bwd_dq"}[key]] = t
     open(out_md, "w").write("\n".join(parts))
