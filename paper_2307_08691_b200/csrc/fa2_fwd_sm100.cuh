@@ -524,8 +524,14 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
               const int jn = j + 1, subn = HB ? (jn & 1) : 0;
               if (subn == 0) ptx::mbar_wait(&k_full[kslot], kphase);
               if (it == 0) FA2_TRACE(4, me, jn);
-              for (int i = i0; i <= i1; ++i)
-                if (jn < (i == 0 ? nb0 : nb1)) issue_s_sep(i, s_iss[i], subn);
+              for (int i = i0; i <= i1; ++i) {
+                const int nbi = i == 0 ? nb0 : nb1;
+                if (jn < nbi) issue_s_sep(i, s_iss[i], subn);
+                if (jn + 1 == nbi) {   // Q_i's last S: release Q_i for the next tile
+                  if (ptx::elect_one()) ptx::mma_commit(&q_empty[i]);
+                  __syncwarp();
+                }
+              }
               if (!HB || subn == 1 || jn + 1 == nkv) {
                 if (ptx::elect_one()) ptx::mma_commit(&k_empty[kslot]);
                 __syncwarp();
@@ -555,8 +561,9 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
               if (++vslot == STAGES) { vslot = 0; vphase ^= 1; }
             }
           }
-          if (ptx::elect_one())
-            for (int i = i0; i <= i1; ++i) ptx::mma_commit(&q_empty[i]);
+          if (ptx::elect_one())   // sub-tiles without key blocks release Q_i here
+            for (int i = i0; i <= i1; ++i)
+              if ((i == 0 ? nb0 : nb1) == 0) ptx::mma_commit(&q_empty[i]);
           __syncwarp();
           continue;
         }
@@ -567,12 +574,18 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           ptx::tc_fence_after();
           if (ptx::elect_one()) {
             if (nb0 > 0) { mma_s(0, kslot); ptx::mma_commit(&s_full[0]); }
+            if (nb0 <= 1) ptx::mma_commit(&q_empty[0]);   // Q_0's last S (see below)
             if (nb1 > 0) { mma_s(1, kslot); ptx::mma_commit(&s_full[1]); }
+            if (nb1 <= 1) ptx::mma_commit(&q_empty[1]);
             ptx::mma_commit(&k_empty[kslot]);
           }
           __syncwarp();
           if (++kslot == STAGES) { kslot = 0; kphase ^= 1; }
+        } else if (ptx::elect_one()) {
+          ptx::mma_commit(&q_empty[0]);
+          ptx::mma_commit(&q_empty[1]);
         }
+        __syncwarp();
         for (int j = 0; j < nkv; ++j) {
           ptx::mbar_wait(&v_full[vslot], vphase);
           bool k_ready = false;
@@ -614,6 +627,9 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
                 if constexpr (SPLIT_S) mma_s_half(i, kslot, 0);
                 else mma_s(i, kslot);
                 ptx::mma_commit(&s_full[i]);
+                // Q_i is free once its last S completes: the producer loads the next
+                // tile's Q_i while this tile's last softmax, P~V and epilogue run
+                if (j + 2 == nbi) ptx::mma_commit(&q_empty[i]);
               }
             }
             __syncwarp();
@@ -631,11 +647,6 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           if (++vslot == STAGES) { vslot = 0; vphase ^= 1; }
           if (k_ready && ++kslot == STAGES) { kslot = 0; kphase ^= 1; }
         }
-        if (ptx::elect_one()) {
-          ptx::mma_commit(&q_empty[0]);
-          ptx::mma_commit(&q_empty[1]);
-        }
-        __syncwarp();
       }
     } else if ((warp == W_TMA || warp == W_TMA + 1) && lane == 0) {
       // ===================== TMA producers: Q + K (warp W_TMA), V (W_TMA + 1) =====================
