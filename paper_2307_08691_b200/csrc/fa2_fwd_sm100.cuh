@@ -57,6 +57,9 @@ constexpr int kFwdEmuPairs = FA2_FWD_EMU_PAIRS;
 #ifndef FA2_FWD_RS
 #define FA2_FWD_RS 1
 #endif
+#ifndef FA2_FWD_RS64
+#define FA2_FWD_RS64 1
+#endif
 // 64-key blocks (bf16/fp16, d = 128): B_c = 64 gives every sub-tile its own P~ columns
 // (TMEM: O0 O1 [0,256) | S0 S1 [256,384) | P~ 2 x 2 buffers [384,512)), so S_{j+1} is issued as
 // soon as the softmax has read S_j and the softmax -> P~V -> S chain disappears.  The
@@ -65,7 +68,7 @@ constexpr int kFwdEmuPairs = FA2_FWD_EMU_PAIRS;
 #define FA2_FWD_HB 0
 #endif
 template <int D, bool FP8> struct FwdCfg {
-  static constexpr int RS = (D == 128 && !FP8) ? FA2_FWD_RS : 1;   // warps per row quarter
+  static constexpr int RS = (D == 128 && !FP8) ? FA2_FWD_RS : (D == 64 ? FA2_FWD_RS64 : 1);   // warps per row quarter
   static constexpr int SM_WARPS = 8 * RS;                          // softmax warps (both sub-tiles)
   static constexpr int THREADS = SM_WARPS * 32 + 128;              // + MMA, TMA, 2 idle
   static constexpr int REG_SM = RS == 2 ? 104 : 224;               // setmaxnreg per warpgroup
@@ -191,7 +194,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       ptx::mbar_init(&o_done[2 * i], 1);
       ptx::mbar_init(&o_done[2 * i + 1], 1);
       ptx::mbar_init(&o_empty[i], 4 * RS);
-      ptx::mbar_init(&s_consumed[i], 4);
+      ptx::mbar_init(&s_consumed[i], 4 * RS);
     }
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&k_full[s], 1);
@@ -248,7 +251,8 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     const uint32_t tS = tmem + lane_base + TS0 + wg * TS_STEP + hf * COLS;
     // P~_i: over the first 64 columns of S_i (B_c = 128, d = 128), or its own columns
     // (d = 64, or B_c = 64: frees S_i for S_{j+1} as soon as it has been read)
-    const uint32_t tP0 = SEP_P ? (tmem + lane_base + TP0 + wg * NPB * TP_STEP) : (tmem + lane_base + TS0 + wg * TS_STEP + hf * COLS / 2);
+    const uint32_t tP0 = SEP_P ? (tmem + lane_base + TP0 + wg * NPB * TP_STEP + hf * COLS / 2)
+                               : (tmem + lane_base + TS0 + wg * TS_STEP + hf * COLS / 2);
     const uint32_t tO = tmem + lane_base + TO0 + wg * D + hf * (D / RS);
     float* red_max = reinterpret_cast<float*>(smem + L::OFF_RED);          // [2][2][2][128]
     float* red_l = red_max + 2 * 2 * 2 * 128;                              // [2][2][128]
