@@ -221,6 +221,22 @@ FA2_API fa2_status_t fa2_attention_step_host(const void* q_h, const void* k_h, c
  * FA2_ERR_INVALID_ARG. */
 FA2_API fa2_status_t fa2_kv_block_range(int N, int Br, int Bc, int i, int causal, int* n_blocks, int* first_masked);
 
+/* Host-side balanced tile schedule (no GPU needed) that the causal square-length
+ * forward (`pass` = 0) and arrival-order backward (`pass` = 1) launches pass to
+ * their kernels (the row-block loops of Alg. 1/2, P:345-351,
+ * P:421-436, with the causal skip of P:378-386 making tiles unequal).
+ *   heads: B * H query heads (forward) or B * H_kv * hsplit work heads (backward)
+ *   N: sequence length; heads_per_tile: query heads one backward tile visits
+ *   (H / H_kv / hsplit; 1 for MHA; ignored by the forward); grid: CTAs (<= 160).
+ * Tiles are numbered as the kernels decode them (forward: head * ceil(N/256) + r,
+ * row block ceil(N/256)-1-r; backward: head * ceil(N/128) + key block).  On
+ * success CTA c runs order[start[c] .. start[c+1]) and *n_tiles is the tile count;
+ * `order` holds `capacity` entries (>= tiles), `start` grid + 1.  Returns
+ * FA2_ERR_INVALID_ARG for bad sizes or more than 8192 tiles (the kernels then
+ * use the stride schedule).  Caller owns both arrays; nothing is allocated. */
+FA2_API fa2_status_t fa2_tile_schedule(int pass, int heads, int N, int heads_per_tile, int grid, unsigned short* order,
+                                       unsigned short* start, int capacity, int* n_tiles);
+
 /* Optional benchmark timing hook (per calling thread).  `events` points to 6
  * cudaEvent_t created by the caller (or is NULL to disable).  While set,
  * fa2_forward records events[0] / events[1] on `stream` immediately before /

@@ -72,6 +72,9 @@ def lib() -> ctypes.CDLL:
         L.fa2_attention_step_host.restype = i
         L.fa2_kv_block_range.argtypes = [i, i, i, i, i, ctypes.POINTER(i), ctypes.POINTER(i)]
         L.fa2_kv_block_range.restype = i
+        us = ctypes.POINTER(ctypes.c_ushort)
+        L.fa2_tile_schedule.argtypes = [i, i, i, i, i, us, us, i, ctypes.POINTER(i)]
+        L.fa2_tile_schedule.restype = i
         L.fa2_status_string.argtypes = [i]
         L.fa2_status_string.restype = ctypes.c_char_p
         L.fa2_last_error_detail.argtypes = []
@@ -317,6 +320,18 @@ def set_timing_events(events):
     arr = (ctypes.c_void_p * 6)(*[ctypes.c_void_p(e.cuda_event) for e in events])
     lib().fa2_set_timing_events(ctypes.cast(arr, ctypes.c_void_p))
     return arr
+
+
+def tile_schedule(pass_: int, heads: int, N: int, heads_per_tile: int = 1, grid: int = 148):
+    """Host balanced schedule of the causal square forward (pass_=0) / backward (1):
+    returns (order, start) with CTA c running order[start[c]:start[c+1]]."""
+    per_head = -(-N // (256 if pass_ == 0 else 128))
+    cap = max(1, per_head * heads)
+    order = (ctypes.c_ushort * cap)()
+    start = (ctypes.c_ushort * (grid + 1))()
+    nt = ctypes.c_int(0)
+    _check(lib().fa2_tile_schedule(pass_, heads, N, heads_per_tile, grid, order, start, cap, ctypes.byref(nt)))
+    return list(order[:nt.value]), list(start)
 
 
 def kv_block_range(N: int, Br: int, Bc: int, i: int, causal: bool):

@@ -709,6 +709,38 @@ fa2_status_t fa2_kv_block_range(int N, int Br, int Bc, int i, int causal, int* n
   return FA2_OK;
 }
 
+fa2_status_t fa2_tile_schedule(int pass, int heads, int N, int heads_per_tile, int grid, unsigned short* order,
+                               unsigned short* start, int capacity, int* n_tiles) {
+  if ((pass != 0 && pass != 1) || heads < 1 || N < 1 || heads_per_tile < 1 || grid < 1 ||
+      grid > fa2::kSchedMaxCtas || order == nullptr || start == nullptr || n_tiles == nullptr)
+    return fail(FA2_ERR_INVALID_ARG, "fa2_tile_schedule: bad arguments");
+  const long long per_head = pass == 0 ? (N + 255) / 256 : (N + 127) / 128;
+  const long long T = per_head * heads;
+  if (T > fa2::kSchedMaxTiles || T > capacity)
+    return fail(FA2_ERR_INVALID_ARG, "fa2_tile_schedule: %lld tiles (max %d, capacity %d)", T, fa2::kSchedMaxTiles,
+                capacity);
+  const fa2::TileSched* sc;
+  if (pass == 0) {
+    fa2::FwdParams p{};
+    p.num_m_blocks = static_cast<int>(per_head);
+    p.num_tiles = static_cast<int>(T);
+    p.geom.Nq = p.geom.Nk = N;
+    sc = &fwd_sched(p, grid);
+  } else {
+    fa2::BwdParams p{};
+    p.num_n_blocks = static_cast<int>(per_head);
+    p.num_tiles = static_cast<int>(T);
+    p.geom.Nq = p.geom.Nk = N;
+    p.group = heads_per_tile;
+    p.hsplit = 1;
+    sc = &bwd_sched(p, grid);
+  }
+  for (int c = 0; c <= grid; ++c) start[c] = sc->start[c];
+  for (long long t = 0; t < T; ++t) order[t] = sc->order[t];
+  *n_tiles = static_cast<int>(T);
+  return FA2_OK;
+}
+
 fa2_status_t fa2_forward_gqa(const void* q, const void* k, const void* v, void* o, float* lse, int B, int H, int H_kv,
                              int N, int d, int causal, float softmax_scale, fa2_dtype_t dtype, void* stream) {
   g_detail.clear();
