@@ -25,6 +25,44 @@ __global__ void k(float* out, unsigned long long* cyc, int iters) {
   __syncthreads();
   unsigned long long t0 = clock64();
   for (int it = 0; it < iters; ++it) {
+    if constexpr (MODE >= 22 && MODE <= 24) {   // 22: +F2FP, 23: +FADD2, 24: +FADD2 + integer RNE pack
+      float2 accf = make_float2(0.f, 0.f);
+      uint32_t acc_u = 0;
+#pragma unroll
+      for (int e = 0; e < 64; ++e) {
+        const float2 x = ptx::ffma2(make_float2(s[2 * e], s[2 * e + 1]), sc, nb);
+        const float a = ptx::ex2(x.x), b = ptx::ex2(x.y);
+        if constexpr (MODE == 22) acc_u ^= ptx::pack2<true>(a, b);
+        if constexpr (MODE >= 23) accf = ptx::fadd2(accf, make_float2(a, b));
+        if constexpr (MODE == 24) {
+          const uint32_t ua = __float_as_uint(a), ub = __float_as_uint(b);
+          const uint32_t ra = ua + 0x7FFFu + ((ua >> 16) & 1u), rb = ub + 0x7FFFu + ((ub >> 16) & 1u);
+          acc_u ^= __byte_perm(ra, rb, 0x7632);
+        }
+        if constexpr (MODE == 23) acc_u ^= __float_as_uint(a) ^ __float_as_uint(b);
+      }
+      sink ^= acc_u ^ __float_as_uint(accf.x + accf.y);
+      s[it & 127] += accf.x * 1e-30f;
+      continue;
+    }
+    if constexpr (MODE == 20 || MODE == 21) {   // pure MUFU.EX2 stream (20) / EX2 + FFMA2 per pair (21)
+      uint32_t acc_u = 0;
+#pragma unroll
+      for (int e = 0; e < 64; ++e) {
+        float a = s[2 * e], b = s[2 * e + 1];
+        if constexpr (MODE == 21) {
+          const float2 x = ptx::ffma2(make_float2(a, b), sc, nb);
+          a = x.x; b = x.y;
+        }
+        s[2 * e] = ptx::ex2(a);
+        s[2 * e + 1] = ptx::ex2(b);
+      }
+#pragma unroll
+      for (int e = 0; e < 128; ++e) acc_u ^= __float_as_uint(s[e]);
+      sink ^= acc_u;
+      s[it & 127] = -((it * 7) % 97) * 0.05f;
+      continue;
+    }
     if constexpr (MODE >= 4) {   // two passes: all exponentials first (in place), then sums and packs
       float p[128];
 #pragma unroll
@@ -94,6 +132,11 @@ int main() {
   run<1>("ex2.f16x2", out, cyc);
   run<2>("ex2.bf16x2", out, cyc);
   run<3>("poly", out, cyc);
+  run<20>("pure EX2", out, cyc);
+  run<22>("EX2+FFMA2+F2FP", out, cyc);
+  run<23>("EX2+FFMA2+FADD2", out, cyc);
+  run<24>("EX2+FFMA2+FADD2+intRNE", out, cyc);
+  run<21>("EX2 + FFMA2", out, cyc);
   run<4>("2pass emu0", out, cyc);
   run<8>("2pass emu4", out, cyc);
   run<10>("2pass emu6", out, cyc);

@@ -23,6 +23,10 @@ for d in (64, 128):
         kv_, vv = mk(529, 2, d), mk(529, 2, d)
         ov, lv = fa2.forward_varlen(qv, kv_, vv, cu_q, cu_k, 257, 300, causal=causal)
         fa2.backward_varlen(qv, kv_, vv, ov, lv, dov, cu_q, cu_k, 257, 300, causal=causal)
+    # causal square shapes long enough for the balanced tile schedule to reorder tiles
+    q3, k3, v3, do3 = (mk(1, 3, 1500, d) for _ in range(4))
+    o3, l3 = fa2.forward(q3, k3, v3, causal=True)
+    fa2.backward(q3, k3, v3, o3, l3, do3, causal=True)
     if d == 128:
         q8, k8, v8 = (mk(1, 2, 300, 128).to(torch.float8_e4m3fn) for _ in range(3))
         fa2.forward_fp8(q8, k8, v8, causal=True)
