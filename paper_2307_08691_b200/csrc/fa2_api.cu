@@ -18,6 +18,7 @@
 #include "fa2_fwd_sm100.cuh"
 #include "fa2_bwd_sm100.cuh"
 #include "fa2_bwd128_sm100.cuh"
+#include "fa2_fwd2_sm100.cuh"
 
 namespace {
 
@@ -138,7 +139,7 @@ Geom fixed_geom(int B, int H, int Hkv, int Nq, int Nk, int d) {
 // 3-D row-tile map in memory order (fa2_seq.cuh): fixed {d, N, B*heads}, packed
 // {d, heads, T}; box = 64 columns x 128 rows of one head.
 fa2_status_t make_rows_map(CUtensorMap* m, const void* base, CUtensorMapDataType dt, const Geom& g, int heads,
-                           bool is_q, int elem_bytes = 2) {
+                           bool is_q, int elem_bytes = 2, int box_rows = 128) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return fail(FA2_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   const cuuint64_t d = static_cast<cuuint64_t>(g.d), eb = static_cast<cuuint64_t>(elem_bytes);
@@ -149,7 +150,7 @@ fa2_status_t make_rows_map(CUtensorMap* m, const void* base, CUtensorMapDataType
     const cuuint64_t n = static_cast<cuuint64_t>(is_q ? g.Nq : g.Nk);
     dims[0] = d; dims[1] = n; dims[2] = static_cast<cuuint64_t>(heads) * static_cast<cuuint64_t>(g.B);
     strides[0] = d * eb; strides[1] = n * d * eb;
-    box[0] = box_cols; box[1] = 128; box[2] = 1;
+    box[0] = box_cols; box[1] = static_cast<cuuint32_t>(box_rows); box[2] = 1;
   } else {
     const cuuint64_t t = static_cast<cuuint64_t>(std::max(1, is_q ? g.Tq : g.Tk));
     dims[0] = d; dims[1] = static_cast<cuuint64_t>(heads); dims[2] = t;
@@ -319,13 +320,36 @@ fa2_status_t dispatch_fwd_causal(bool causal, const CUtensorMap& mq, const CUten
                 : launch_fwd<D, BF16, false, false>(mq, mk, mv, p, sms, st);
 }
 
+#ifndef FA2_FWD_PAIR
+#define FA2_FWD_PAIR 1   // 0: the one-SM forward kernel for every shape (A/B builds)
+#endif
+// CTA-pair forward (fa2_fwd2_sm100.cuh): non-causal, square fixed-length, d = 128, bf16/fp16
+template <bool BF16>
+fa2_status_t launch_fwd_pair(const CUtensorMap& mq, const CUtensorMap& mk64, const CUtensorMap& mv,
+                             fa2::FwdParams p, int sms, cudaStream_t st) {
+  auto kern = fa2::fa2_fwd_pair_kernel<BF16>;
+  constexpr int smem = fa2::FwdPairSmem::ALLOC;
+  fa2_status_t s = set_smem(kern, smem);
+  if (s != FA2_OK) return s;
+  p.num_m_blocks = (p.geom.Nq + 511) / 512;
+  p.num_tiles = p.BH * p.num_m_blocks;
+  int grid = 2 * p.num_tiles < sms ? 2 * p.num_tiles : sms;
+  grid &= ~1;
+  mark(0, st);
+  kern<<<grid, 384, smem, st>>>(mq, mk64, mv, p);
+  mark(1, st);
+  FA2_CUDA(cudaGetLastError());
+  return FA2_OK;
+}
+
 fa2_status_t forward_impl(const void* q, const void* k, const void* v, void* o, float* lse, const Geom& g,
                           int causal, float scale, fa2_dtype_t dtype, cudaStream_t st, int sms) {
   CUtensorMap mq, mk, mv;
   const CUtensorMapDataType dt = tma_dtype(dtype);
   fa2_status_t s;
   if ((s = make_rows_map(&mq, q, dt, g, g.H, true)) != FA2_OK) return s;
-  if ((s = make_rows_map(&mk, k, dt, g, g.Hkv, false)) != FA2_OK) return s;
+  const bool pair = FA2_FWD_PAIR && !causal && g.d == 128 && !g.packed && g.Nq == g.Nk;
+  if ((s = make_rows_map(&mk, k, dt, g, g.Hkv, false, 2, pair ? 64 : 128)) != FA2_OK) return s;
   if ((s = make_rows_map(&mv, v, dt, g, g.Hkv, false)) != FA2_OK) return s;
   fa2::FwdParams p;
   p.o = o;
@@ -348,6 +372,7 @@ fa2_status_t forward_impl(const void* q, const void* k, const void* v, void* o, 
   p.scale_log2 = scale * 1.4426950408889634f;
   p.trace = g_trace;
   const bool bf16 = dtype == FA2_BF16;
+  if (pair) return bf16 ? launch_fwd_pair<true>(mq, mk, mv, p, sms, st) : launch_fwd_pair<false>(mq, mk, mv, p, sms, st);
   if (g.d == 64)
     s = bf16 ? dispatch_fwd_causal<64, true>(causal, mq, mk, mv, p, sms, st)
              : dispatch_fwd_causal<64, false>(causal, mq, mk, mv, p, sms, st);

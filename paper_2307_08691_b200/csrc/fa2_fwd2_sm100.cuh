@@ -1,0 +1,440 @@
+// FlashAttention-2 forward (Alg. 1) on a CTA pair (cta_group::2):
+// the non-causal, square, d = 128, bf16/fp16 path (the paper's benchmark shape).
+//
+// Why a pair: on one SM the chain softmax_i -> P~V_i -> S_i ->
+// softmax_i bounds the forward, and breaking it needs P~ outside the S columns -- TMEM
+// is full (S0 S1 O0 O1) and P~ in shared memory pushes one SM past its 128 B/clk
+// SMEM -> tensor-core rate.  With cta_group::2 every MMA has M = 256 (128 rows per
+// CTA) and each CTA holds only half of B (K: 64 of the block's 128 keys, V: 64 of the
+// 128 head-dim columns), so S = Q K^T reads 96 B/clk per SM, K/V loads halve, and P~
+// fits in shared memory as the A operand of P~V.  S_{j+1} is then issued as soon as
+// the softmax has read S_j, so the softmax runs back to back.
+//
+// A work tile is (b*h, 512 query rows): CTA rank r of the pair owns rows
+// [512 m + 256 r, +256) as two 128-row sub-tiles (TMEM lanes = rows).  Per key block j:
+//   S_i  = Q_i K_j^T                    leader-issued M = 256 SS MMA -> S_i in both CTAs' TMEM
+//   m, P~, l (online softmax)           softmax warpgroup i of each CTA; P~ -> SMEM (SW128)
+//   O_i  = diag(e^{m_old-m_new}) O_i + P~ V_j    M = 256 SS MMA (A = P~ of both CTAs)
+// The rescale is lazy as in fa2_fwd_sm100.cuh (threshold 2^8, exact).
+//
+// Barriers: "full"-type barriers the MMA warps wait on live in the leader (rank 0):
+// TMA loads of both CTAs signal the leader's q_full/k_full/v_full (cta_group::2 TMA),
+// the softmax warps of both CTAs arrive remotely on the leader's s_consumed/p_full/
+// o_empty.  Barriers the MMAs release (s_full, o_done, q/k/v_empty) are signalled in
+// both CTAs by multicast tcgen05.commit.
+//
+// Warp roles (384 threads per CTA): warps 0-3 / 4-7 softmax of sub-tile 0 / 1; warp 8
+// (leader) MMA issuer of sub-tile 0, warp 11 (leader) of sub-tile 1; warp 9 TMA of Q
+// and K, warp 10 TMA of V.
+#pragma once
+#include "fa2_fwd_sm100.cuh"
+
+namespace fa2 {
+
+// FMA-pipe exponential pairs per 16 in the pair kernel, whose two sub-tiles' softmaxes run
+// concurrently (two warps per SMSP): measured 1327 / 1394 / 1308 / 1250 TFLOP/s for
+// 0 / 2 / 4 / 6 (d = 128, N = 8k, non-causal).
+#ifndef FA2_FWD_PAIR_EMU
+#define FA2_FWD_PAIR_EMU 2
+#endif
+constexpr int kFwdPairEmuPairs = FA2_FWD_PAIR_EMU;
+
+namespace pair {
+
+FA2_DEVICE uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+FA2_DEVICE uint32_t cluster_id() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+FA2_DEVICE uint32_t num_clusters() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+FA2_DEVICE void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the mbarrier at the same shared-memory offset in CTA `cta` of the cluster
+FA2_DEVICE void arrive_remote(uint64_t* bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}"
+      :: "r"(ptx::smem_u32(bar)), "r"(cta) : "memory");
+}
+// wait on a local mbarrier whose arrivals come from the whole cluster
+FA2_DEVICE void wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = ptx::smem_u32(bar);
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+  }
+}
+// arrive (once) on `bar` in both CTAs of the pair when this thread's tcgen05 ops complete
+FA2_DEVICE void commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+      :: "r"(ptx::smem_u32(bar)), "h"(static_cast<uint16_t>(0x3)) : "memory");
+}
+FA2_DEVICE void mma_ss2(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+      :: "r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate) : "memory");
+}
+// TMA 3-D load into this CTA's SMEM whose completion bytes land on the leader's mbarrier
+// at the same offset (peer bit of the shared::cluster address cleared)
+FA2_DEVICE void tma_load_pair(void* smem_dst, const CUtensorMap* d, uint64_t* bar, int c0, int c1, int c2,
+                              uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;"
+      :: "r"(ptx::smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(d)), "r"(c0), "r"(c1), "r"(c2),
+         "r"(ptx::smem_u32(bar) & 0xFEFFFFFFu), "l"(policy)
+      : "memory");
+}
+
+}  // namespace pair
+
+struct FwdPairSmem {
+  static constexpr int D = 128;
+  static constexpr int STAGES = 3;
+  static constexpr int Q_TILE = 128 * D * 2;       // one 128-row sub-tile of Q (32 KB, 2 SW128 boxes)
+  static constexpr int Q_BOX = 128 * 128;          // 128 rows x 128 B
+  static constexpr int K_HALF = 64 * D * 2;        // 64 key rows x 128 d (16 KB, 2 boxes of 64 x 128 B)
+  static constexpr int K_BOX = 64 * 128;
+  static constexpr int V_HALF = 128 * 64 * 2;      // 128 key rows x 64 d columns (16 KB, 1 box)
+  static constexpr int P_TILE = 128 * 128 * 2;     // P~ of one sub-tile: 128 rows x 128 keys (2 boxes)
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + 2 * Q_TILE;
+  static constexpr int OFF_V = OFF_K + STAGES * K_HALF;
+  static constexpr int OFF_P = OFF_V + STAGES * V_HALF;
+  static constexpr int OFF_BAR = OFF_P + 2 * P_TILE;
+  // q_full[2] q_empty[2] k_full[S] k_empty[S] v_full[S] v_empty[S] s_full[2] s_consumed[2]
+  // p_full[2] o_done[2] o_empty[2]
+  static constexpr int NBAR = 4 + 4 * STAGES + 10;
+  static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
+  static constexpr int BYTES = OFF_TMEM + 16;
+  static constexpr int ALLOC = BYTES + 1024;
+  static_assert(ALLOC <= 232448, "shared memory budget");
+};
+
+// p: as for fa2_fwd_kernel with num_m_blocks = ceil(N / 512), num_tiles = BH * num_m_blocks
+template <bool BF16>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k64,
+                    const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
+  using L = FwdPairSmem;
+  constexpr int D = 128, STAGES = L::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem + L::OFF_Q;
+  uint8_t* sK = smem + L::OFF_K;
+  uint8_t* sV = smem + L::OFF_V;
+  uint8_t* sP = smem + L::OFF_P;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint64_t* q_full = bars;
+  uint64_t* q_empty = bars + 2;
+  uint64_t* k_full = bars + 4;
+  uint64_t* k_empty = k_full + STAGES;
+  uint64_t* v_full = k_empty + STAGES;
+  uint64_t* v_empty = v_full + STAGES;
+  uint64_t* s_full = v_empty + STAGES;
+  uint64_t* s_consumed = s_full + 2;
+  uint64_t* p_full = s_consumed + 2;
+  uint64_t* o_done = p_full + 2;
+  uint64_t* o_empty = o_done + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t rank = pair::cta_rank();
+  const int pair_id = static_cast<int>(pair::cluster_id()), npairs = static_cast<int>(pair::num_clusters());
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&q_full[i], 1);
+      ptx::mbar_init(&q_empty[i], 1);
+      ptx::mbar_init(&s_full[i], 1);
+      ptx::mbar_init(&s_consumed[i], 8);   // 4 softmax warps x 2 CTAs (leader's copy)
+      ptx::mbar_init(&p_full[i], 8);
+      ptx::mbar_init(&o_done[i], 1);
+      ptx::mbar_init(&o_empty[i], 8);
+    }
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&k_full[s], 1);
+      ptx::mbar_init(&k_empty[s], 2);      // one multicast commit per MMA-issuer warp
+      ptx::mbar_init(&v_full[s], 1);
+      ptx::mbar_init(&v_empty[s], 2);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 9 && lane == 0) {
+    ptx::tma_prefetch_desc(&tm_q);
+    ptx::tma_prefetch_desc(&tm_k64);
+    ptx::tma_prefetch_desc(&tm_v);
+  }
+  if (warp == 0)
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(ptx::smem_u32(tmem_slot)), "r"(512));
+  ptx::tc_fence_before();
+  pair::cluster_sync();   // barriers initialised and TMEM allocated in both CTAs
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int N = p.geom.Nq;
+  const int nkb = (N + 127) / 128;
+
+  if (warp < 8) {
+    // ======================= softmax warpgroups =======================
+    ptx::setmaxnreg_inc<224>();
+    const int wg = warp / 4;
+    const int row = threadIdx.x % 128;
+    const uint32_t lane_base = static_cast<uint32_t>((warp % 4) * 32) << 16;
+    const uint32_t tS = tmem + lane_base + wg * 128;
+    const uint32_t tO = tmem + lane_base + 256 + wg * D;
+    // P~ row `row` of sub-tile wg: SW128 K-major, box b = keys [64 b, 64 b + 64)
+    const uint32_t sP_row = ptx::smem_u32(sP + wg * L::P_TILE) + row * 128;
+    uint32_t s_count = 0, pv_count = 0;
+    const float sl2 = p.scale_log2;
+    for (int t = pair_id; t < p.num_tiles; t += npairs) {
+      const int bh = t / p.num_m_blocks, mb = t % p.num_m_blocks;
+      const int grow = mb * 512 + static_cast<int>(rank) * 256 + wg * 128 + row;
+      float m_used = -INFINITY, l_sum = 0.f;
+      const bool tr = threadIdx.x % 128 == 0 && t == pair_id;
+      for (int j = 0; j < nkb; ++j) {
+        ptx::mbar_wait(&s_full[wg], s_count & 1);
+        ++s_count;
+        if (tr) FA2_TRACE(0, wg, j);
+        ptx::tc_fence_after();
+        uint32_t su[128];
+        ptx::tmem_ld_x32(tS + 0, su + 0);
+        ptx::tmem_ld_x32(tS + 32, su + 32);
+        ptx::tmem_ld_x32(tS + 64, su + 64);
+        ptx::tmem_ld_x32(tS + 96, su + 96);
+        ptx::tmem_wait_ld();
+        // S_i has been read: the leader may compute S_i of the next block into it
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) pair::arrive_remote(&s_consumed[wg], 0);
+        float s[128];
+#pragma unroll
+        for (int c = 0; c < 128; ++c) s[c] = __uint_as_float(su[c]);
+        const int c0 = j * 128;
+        const bool need_mask = c0 + 128 > N;
+        if (need_mask) {
+#pragma unroll
+          for (int c = 0; c < 128; ++c)
+            if (c0 + c >= N) s[c] = -INFINITY;
+        }
+        float mx = s[0];
+#pragma unroll
+        for (int c = 1; c < 128; ++c) mx = fmaxf(mx, s[c]);
+        if (tr) FA2_TRACE(1, wg, j);
+        const float m_new = fmaxf(m_used, mx * sl2);
+        const bool rescale = (m_new - m_used) > 8.0f;
+        float alpha = 1.f;
+        if (rescale) {
+          alpha = ptx::ex2(m_used - m_new);
+          m_used = m_new;
+        }
+        const float base = (m_used == -INFINITY) ? 0.f : m_used;
+        const float2 sl2x2 = make_float2(sl2, sl2), nb2 = make_float2(-base, -base);
+        float2 rs2 = make_float2(0.f, 0.f);
+        // P~ buffer and O: the previous P~V of this sub-tile must have completed (it was
+        // issued a whole softmax ago, so this rarely waits); O is rescaled first, then P~
+        // is stored chunk by chunk as the exponentials produce it, spreading the 32 KB of
+        // SMEM writes over the MUFU-bound exponential phase instead of a burst at its end
+        if (pv_count > 0) ptx::mbar_wait(&o_done[wg], (pv_count - 1) & 1);
+        ptx::tc_fence_after();
+        if (j > 0 && __any_sync(0xffffffffu, rescale)) {
+#pragma unroll
+          for (int ch = 0; ch < D / 32; ++ch) {
+            uint32_t o[32];
+            ptx::tmem_ld_x32(tO + ch * 32, o);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            ptx::tmem_st_x32(tO + ch * 32, o);
+          }
+          ptx::tmem_wait_st();
+        }
+        auto exp_block = [&](auto emu_tag) {
+          constexpr int EMU = decltype(emu_tag)::value;
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {   // chunk c: keys [8c, 8c + 8), 16 B of P~
+            uint32_t pk[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int e = 4 * c + q;
+              const float2 x = ptx::ffma2(make_float2(s[2 * e], s[2 * e + 1]), sl2x2, nb2);
+              float2 pr;
+              if (e % 16 < EMU) {
+                pr = ptx::exp2_poly2(x);
+              } else {
+                pr.x = ptx::ex2(x.x);
+                pr.y = ptx::ex2(x.y);
+              }
+              rs2 = ptx::fadd2(rs2, pr);
+              pk[q] = ptx::pack2<BF16>(pr.x, pr.y);
+            }
+            // SW128 K-major: chunk c of box c / 8 at row * 128 + ((c ^ row) & 7) * 16
+            ptx::sts_v4(sP_row + (c / 8) * L::Q_BOX + (((c % 8) ^ (row % 8)) * 16), pk[0], pk[1], pk[2], pk[3]);
+          }
+        };
+        if (need_mask) exp_block(std::integral_constant<int, 0>{});
+        else exp_block(std::integral_constant<int, kFwdPairEmuPairs>{});
+        l_sum = l_sum * alpha + (rs2.x + rs2.y);
+        if (tr) FA2_TRACE(2, wg, j);
+        ptx::fence_proxy_async_smem();   // generic-proxy P~ writes -> visible to the tensor core
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) pair::arrive_remote(&p_full[wg], 0);
+        if (tr) FA2_TRACE(3, wg, j);
+        ++pv_count;
+      }
+      // ---- epilogue: O = O / l, L = m + log l ----
+      ptx::mbar_wait(&o_done[wg], (pv_count - 1) & 1);
+      ptx::tc_fence_after();
+      const float inv_l = l_sum > 0.f ? 1.f / l_sum : 0.f;
+      uint8_t* orow = reinterpret_cast<uint8_t*>(p.o) + (static_cast<size_t>(bh) * N + grow) * D * 2;
+#pragma unroll
+      for (int ch = 0; ch < D / 32; ++ch) {
+        uint32_t o[32];
+        ptx::tmem_ld_x32(tO + ch * 32, o);
+        ptx::tmem_wait_ld();
+        uint32_t q[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          q[e] = ptx::pack2<BF16>(__uint_as_float(o[2 * e]) * inv_l, __uint_as_float(o[2 * e + 1]) * inv_l);
+        if (grow < N) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + ch * 64);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) dst[e] = make_uint4(q[4 * e], q[4 * e + 1], q[4 * e + 2], q[4 * e + 3]);
+        }
+      }
+      if (grow < N)
+        p.lse[static_cast<size_t>(bh) * N + grow] = l_sum > 0.f ? (m_used + ptx::lg2(l_sum)) * 0.69314718055994531f : -INFINITY;
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) pair::arrive_remote(&o_empty[wg], 0);
+    }
+  } else {
+    ptx::setmaxnreg_dec<56>();
+    if ((warp == 8 || warp == 11) && rank == 0) {
+      // ============ MMA issuers (leader CTA): warp 8 -> sub-tile 0, warp 11 -> sub-tile 1 ============
+      const int i = warp == 8 ? 0 : 1;
+      constexpr uint32_t IDESC_S = ptx::idesc_f16(BF16, 256, 128, false, false);
+      constexpr uint32_t IDESC_O = ptx::idesc_f16(BF16, 256, D, false, true);
+      const uint64_t dQ = ptx::sw128_desc(ptx::smem_u32(sQ + i * L::Q_TILE), 16, 1024);
+      const uint64_t dK = ptx::sw128_desc(ptx::smem_u32(sK), 16, 1024);
+      const uint64_t dV = ptx::sw128_desc(ptx::smem_u32(sV), L::V_HALF, 1024);
+      const uint64_t dP = ptx::sw128_desc(ptx::smem_u32(sP + i * L::P_TILE), 16, 1024);
+      int kslot = 0, vslot = 0;
+      uint32_t kphase = 0, vphase = 0, s_iss = 0, p_cnt = 0, o_use = 0;
+      int it = 0;
+      for (int t = pair_id; t < p.num_tiles; t += npairs, ++it) {
+        ptx::mbar_wait(&q_full[i], it & 1);
+        for (int j = -1; j < nkb; ++j) {
+          if (j + 1 < nkb) {   // S_i(j+1) = Q_i K_{j+1}^T once the softmax has read S_i(j)
+            ptx::mbar_wait(&k_full[kslot], kphase);
+            if (s_iss > 0) pair::wait_cluster(&s_consumed[i], (s_iss - 1) & 1);
+            ptx::tc_fence_after();
+            if (ptx::elect_one()) {
+#pragma unroll
+              for (int k = 0; k < D * 2 / 32; ++k) {   // K = 16 per MMA: 4 per 128-B swizzle box
+                const uint32_t offa = (k / 4) * L::Q_BOX + (k % 4) * 32;
+                const uint32_t offb = kslot * L::K_HALF + (k / 4) * L::K_BOX + (k % 4) * 32;
+                pair::mma_ss2(tmem + i * 128, dQ + (offa >> 4), dK + (offb >> 4), IDESC_S, k > 0 ? 1u : 0u);
+              }
+              pair::commit_both(&s_full[i]);
+              if (j + 2 == nkb) pair::commit_both(&q_empty[i]);   // Q_i's last S
+              pair::commit_both(&k_empty[kslot]);
+            }
+            __syncwarp();
+            if (it == 0) FA2_TRACE(5, i, j + 1);
+            ++s_iss;
+            if (++kslot == STAGES) { kslot = 0; kphase ^= 1; }
+          }
+          if (j < 0) continue;
+          // O_i += P~_i(j) V_j once both CTAs' softmax wrote P~_i(j)
+          ptx::mbar_wait(&v_full[vslot], vphase);
+          if (j == 0) {
+            if (o_use > 0) pair::wait_cluster(&o_empty[i], (o_use - 1) & 1);
+            ++o_use;
+          }
+          pair::wait_cluster(&p_full[i], p_cnt & 1);
+          ++p_cnt;
+          if (it == 0) FA2_TRACE(4, i, j);
+          ptx::tc_fence_after();
+          if (ptx::elect_one()) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {   // 16 keys per MMA
+              const uint32_t offa = (k / 4) * L::Q_BOX + (k % 4) * 32;
+              const uint32_t offb = vslot * L::V_HALF + k * 2048;
+              pair::mma_ss2(tmem + 256 + i * D, dP + (offa >> 4), dV + (offb >> 4), IDESC_O, (j > 0 || k > 0) ? 1u : 0u);
+            }
+            pair::commit_both(&o_done[i]);
+            pair::commit_both(&v_empty[vslot]);
+          }
+          __syncwarp();
+          if (++vslot == STAGES) { vslot = 0; vphase ^= 1; }
+        }
+      }
+    } else if ((warp == 9 || warp == 10) && lane == 0) {
+      // ======= TMA producers: Q + K halves (warp 9), V halves (warp 10), into this CTA's SMEM =======
+      const bool is_k = warp == 9;
+      const uint64_t pol_kv = ptx::l2_policy_evict_last();
+      const uint64_t pol_q = ptx::l2_policy_evict_first();
+      int slot = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = pair_id; t < p.num_tiles; t += npairs, ++it) {
+        const int bh = t / p.num_m_blocks, mb = t % p.num_m_blocks;
+        const int kvh = (bh % p.H) / p.group, b = bh / p.H;
+        if (is_k) {
+          for (int i = 0; i < 2; ++i) {
+            if (it > 0) ptx::mbar_wait(&q_empty[i], (it - 1) & 1);
+            if (rank == 0) ptx::mbar_arrive_expect_tx(&q_full[i], 2 * L::Q_TILE);
+            for (int s = 0; s < 2; ++s)
+              pair::tma_load_pair(sQ + i * L::Q_TILE + s * L::Q_BOX, &tm_q, &q_full[i], s * 64,
+                                  mb * 512 + static_cast<int>(rank) * 256 + i * 128, bh, pol_q);
+          }
+        }
+        for (int j = 0; j < nkb; ++j) {
+          ptx::mbar_wait(is_k ? &k_empty[slot] : &v_empty[slot], phase ^ 1);
+          if (is_k) {   // key rows [128 j + 64 rank, +64), all d
+            if (rank == 0) ptx::mbar_arrive_expect_tx(&k_full[slot], 2 * L::K_HALF);
+            for (int s = 0; s < 2; ++s)
+              pair::tma_load_pair(sK + slot * L::K_HALF + s * L::K_BOX, &tm_k64, &k_full[slot], s * 64,
+                                  j * 128 + static_cast<int>(rank) * 64, b * p.Hkv + kvh, pol_kv);
+          } else {      // key rows [128 j, +128), head-dim columns [64 rank, +64)
+            if (rank == 0) ptx::mbar_arrive_expect_tx(&v_full[slot], 2 * L::V_HALF);
+            pair::tma_load_pair(sV + slot * L::V_HALF, &tm_v, &v_full[slot], static_cast<int>(rank) * 64, j * 128,
+                                b * p.Hkv + kvh, pol_kv);
+          }
+          if (++slot == STAGES) { slot = 0; phase ^= 1; }
+        }
+      }
+    }
+  }
+  __syncwarp();
+  ptx::tc_fence_before();
+  pair::cluster_sync();
+  if (warp == 0) {
+    ptx::tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::);
+  }
+}
+
+}  // namespace fa2

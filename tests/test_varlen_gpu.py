@@ -101,8 +101,11 @@ def test_varlen_parity(case, d, causal, dtype):
 
 @pytest.mark.parametrize("causal", [False, True])
 def test_varlen_equal_lengths_match_fixed_layout(causal):
-    """Equal lengths: the packed path computes exactly what the [B,H,N,d] path does
-    (forward bitwise; backward up to the dQ summation order)."""
+    """Equal lengths: the packed path computes what the [B,H,N,d] path does.  Causal:
+    the same kernel, forward bitwise.  Non-causal d=128: the fixed layout runs the
+    CTA-pair forward, whose exponential split (2 of 16 pairs on the FMA pipe instead of
+    4) rounds P~ differently, so forward to within a bf16 rounding step.  Backward up to
+    the dQ summation order (and the forward difference)."""
     B, H, N, d = 3, 2, 300, 128
     q, k, v, do = W.qkv(B, H, N, d, "bf16", seed=320)
     qc, kc, vc, doc = q.cuda(), k.cuda(), v.cuda(), do.cuda()
@@ -113,8 +116,13 @@ def test_varlen_equal_lengths_match_fixed_layout(causal):
     o2, lse2 = fa2.forward_varlen(pk(qc), pk(kc), pk(vc), cu, cu, N, N, causal=causal)
     dq2, dk2, dv2 = fa2.backward_varlen(pk(qc), pk(kc), pk(vc), o2, lse2, pk(doc), cu, cu, N, N, causal=causal)
     torch.cuda.synchronize()
-    assert torch.equal(pk(o), o2)
-    assert torch.equal(lse.transpose(0, 1).reshape(H, B * N), lse2)
+    if causal:
+        assert torch.equal(pk(o), o2)
+        assert torch.equal(lse.transpose(0, 1).reshape(H, B * N), lse2)
+    else:
+        diff = (pk(o).float() - o2.float()).abs()
+        assert bool((diff <= 2 ** -7 * o2.float().abs() + 1e-3).all()), float(diff.max())
+        assert float((lse.transpose(0, 1).reshape(H, B * N) - lse2).abs().max()) <= 1e-4
     for a, b in ((dq, dq2), (dk, dk2), (dv, dv2)):
         rel = float((pk(a).float() - b.float()).abs().max()) / float(b.float().abs().max())
         assert rel <= 2 ** -6, rel
