@@ -95,7 +95,7 @@ if __name__ == "__main__":
     if os.path.exists(lf):
         parts += ["## Launch list (our kernels)", "", launches(lf)]
     traffic = {}
-    for key, label in (("fwd", "fa2_fwd_kernel"), ("bwd", "fa2_bwd128_kernel (bwd main)"),
+    for key, label in (("fwd", "fa2_fwd_pair_kernel (CTA pair, cta_group::2)"), ("bwd", "fa2_bwd128_kernel (bwd main)"),
                        ("pre", "fa2_bwd_preprocess"), ("dq", "fa2_dq_convert")):
         rep = os.path.join(g, f"{tag}_prof_{key}.ncu-rep")
         if os.path.exists(rep):
