@@ -333,8 +333,25 @@ fa2_status_t launch_fwd_pair(const CUtensorMap& mq, const CUtensorMap& mk64, con
   if (s != FA2_OK) return s;
   p.num_m_blocks = (p.geom.Nq + 511) / 512;
   p.num_tiles = p.BH * p.num_m_blocks;
+  // persistent grid of co-resident pairs: no more clusters than can be active at once
+  // (the static pair-tile list would otherwise wait for a second wave)
+  static int max_clusters = -1;   // per process; the library targets one B200 model
+  if (max_clusters < 0) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 2; attr.val.clusterDim.y = 1; attr.val.clusterDim.z = 1;
+    cfg.gridDim = dim3(static_cast<unsigned>(sms & ~1));
+    cfg.blockDim = dim3(384);
+    cfg.dynamicSmemBytes = smem;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    max_clusters = cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0 ? n : sms / 2;
+  }
   int grid = 2 * p.num_tiles < sms ? 2 * p.num_tiles : sms;
   grid &= ~1;
+  if (grid > 2 * max_clusters) grid = 2 * max_clusters;
   mark(0, st);
   kern<<<grid, 384, smem, st>>>(mq, mk64, mv, p);
   mark(1, st);
