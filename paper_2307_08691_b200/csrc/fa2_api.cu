@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <mutex>
 #include <algorithm>
@@ -19,6 +20,7 @@
 #include "fa2_bwd_sm100.cuh"
 #include "fa2_bwd128_sm100.cuh"
 #include "fa2_fwd2_sm100.cuh"
+#include "fa2_bwd2_sm100.cuh"
 
 namespace {
 
@@ -237,26 +239,59 @@ void build_sched(fa2::TileSched& sc, const std::vector<int>& work, int tiles_per
   sc.n = T;
 }
 
-// key: (kind, tiles, tiles per head, rows, heads per tile, grid); make_work(work) fills the tile works
+// key: (device, kind, tiles, tiles per head, rows, heads per tile, grid); make_work(work) fills the
+// tile works.  Entries are shared_ptr so a caller's schedule outlives a concurrent eviction.
+using SchedPtr = std::shared_ptr<const fa2::TileSched>;
 template <typename F>
-const fa2::TileSched& cached_sched(int kind, int T, int tiles_per_head, int N, int nh, int grid, F make_work) {
+SchedPtr cached_sched(int kind, int T, int tiles_per_head, int N, int nh, int grid, F make_work) {
   static std::mutex mu;
-  static std::map<std::tuple<int, int, int, int, int, int>, std::unique_ptr<fa2::TileSched>> cache;
-  const auto key = std::make_tuple(kind, T, tiles_per_head, N, nh, grid);
-  std::lock_guard<std::mutex> lock(mu);
-  auto it = cache.find(key);
-  if (it != cache.end()) return *it->second;
-  if (cache.size() > 256) cache.clear();
-  auto sc = std::make_unique<fa2::TileSched>();
+  static std::map<std::tuple<int, int, int, int, int, int, int>, SchedPtr> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(dev, kind, T, tiles_per_head, N, nh, grid);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  auto sc = std::make_shared<fa2::TileSched>();
   std::vector<int> work(T);
   make_work(work);
   build_sched(*sc, work, tiles_per_head, std::max(1, 65536 / std::max(1, N)), grid);
-  return *cache.emplace(key, std::move(sc)).first->second;
+  std::lock_guard<std::mutex> lock(mu);
+  if (cache.size() > 256) cache.clear();   // live schedules stay alive through their shared_ptr
+  return cache.emplace(key, std::move(sc)).first->second;
+}
+
+// Co-resident clusters of 2 for a kernel (the persistent pair kernels' grid cap), per device.
+template <typename K>
+int max_active_pairs(K kern, int smem, int threads, int sms) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_pair(dev, reinterpret_cast<const void*>(kern));
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = 2; attr.val.clusterDim.y = 1; attr.val.clusterDim.z = 1;
+  cfg.gridDim = dim3(static_cast<unsigned>(sms & ~1));
+  cfg.blockDim = dim3(static_cast<unsigned>(threads));
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  const int v = cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0 ? n : sms / 2;
+  cache.emplace(key, v);
+  return v;
 }
 
 // Forward (causal, square): tile t = (head, row block mb = nmb - 1 - t % nmb), work = key
 // blocks of its two 128-row sub-tiles + 1 (prologue / epilogue).
-const fa2::TileSched& fwd_sched(const fa2::FwdParams& p, int grid) {
+SchedPtr fwd_sched(const fa2::FwdParams& p, int grid) {
   const int nmb = p.num_m_blocks, N = p.geom.Nq;
   return cached_sched(0, p.num_tiles, nmb, N, 1, grid, [&](std::vector<int>& work) {
     const int nkb = (N + 127) / 128;
@@ -274,7 +309,7 @@ const fa2::TileSched& fwd_sched(const fa2::FwdParams& p, int grid) {
 
 // Backward (causal, square, arrival-order dQ): tile t = (head split, key block nb = t % nnb),
 // work = query tiles i >= nb times the query heads of the tile, + 1.
-const fa2::TileSched& bwd_sched(const fa2::BwdParams& p, int grid) {
+SchedPtr bwd_sched(const fa2::BwdParams& p, int grid) {
   const int nnb = p.num_n_blocks, N = p.geom.Nq, nh = p.group / p.hsplit;
   return cached_sched(1, p.num_tiles, nnb, N, nh, grid, [&](std::vector<int>& work) {
     const int nqb = (N + 127) / 128;
@@ -294,9 +329,9 @@ fa2_status_t launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUte
   sched.n = 0;
   if constexpr (CAUSAL && !GEN) {
     if (FA2_SCHED && p.num_tiles <= fa2::kSchedMaxTiles && grid <= fa2::kSchedMaxCtas) {
-      const fa2::TileSched& sc = fwd_sched(p, grid);
+      const SchedPtr sc = fwd_sched(p, grid);
       mark(0, st);
-      kern<<<grid, fa2::FwdCfg<D, FP8>::THREADS, smem, st>>>(mq, mk, mv, p, sc);
+      kern<<<grid, fa2::FwdCfg<D, FP8>::THREADS, smem, st>>>(mq, mk, mv, p, *sc);
       mark(1, st);
       FA2_CUDA(cudaGetLastError());
       return FA2_OK;
@@ -335,20 +370,7 @@ fa2_status_t launch_fwd_pair(const CUtensorMap& mq, const CUtensorMap& mk64, con
   p.num_tiles = p.BH * p.num_m_blocks;
   // persistent grid of co-resident pairs: no more clusters than can be active at once
   // (the static pair-tile list would otherwise wait for a second wave)
-  static int max_clusters = -1;   // per process; the library targets one B200 model
-  if (max_clusters < 0) {
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr;
-    attr.id = cudaLaunchAttributeClusterDimension;
-    attr.val.clusterDim.x = 2; attr.val.clusterDim.y = 1; attr.val.clusterDim.z = 1;
-    cfg.gridDim = dim3(static_cast<unsigned>(sms & ~1));
-    cfg.blockDim = dim3(384);
-    cfg.dynamicSmemBytes = smem;
-    cfg.attrs = &attr;
-    cfg.numAttrs = 1;
-    int n = 0;
-    max_clusters = cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0 ? n : sms / 2;
-  }
+  const int max_clusters = max_active_pairs(kern, smem, 384, sms);
   int grid = 2 * p.num_tiles < sms ? 2 * p.num_tiles : sms;
   grid &= ~1;
   if (grid > 2 * max_clusters) grid = 2 * max_clusters;
@@ -555,9 +577,9 @@ fa2_status_t launch_bwd_kernel(Kern kern, int smem, const fa2::BwdMaps& maps, co
   sched.n = 0;
   if constexpr (SCHED) {   // causal square arrival-order backward: balanced tile lists
     if (FA2_SCHED && p.dq_sem == nullptr && p.num_tiles <= fa2::kSchedMaxTiles && grid <= fa2::kSchedMaxCtas) {
-      const fa2::TileSched& sc = bwd_sched(p, grid);
+      const SchedPtr sc = bwd_sched(p, grid);
       mark(3, st);
-      kern<<<grid, fa2::kBwdThreads, smem, st>>>(maps.q, maps.k, maps.v, maps.dout, maps.dq_acc, p, sc);
+      kern<<<grid, fa2::kBwdThreads, smem, st>>>(maps.q, maps.k, maps.v, maps.dout, maps.dq_acc, p, *sc);
       mark(4, st);
       FA2_CUDA(cudaGetLastError());
       return FA2_OK;
@@ -587,6 +609,45 @@ fa2_status_t dispatch_bwd_causal(bool causal, const fa2::BwdMaps& maps, const fa
   if (p.geom.cu_q != nullptr || p.geom.Nq != p.geom.Nk)   // general geometry
     return causal ? launch_bwd<D, BF16, true, true>(maps, p, sms, st) : launch_bwd<D, BF16, false, true>(maps, p, sms, st);
   return causal ? launch_bwd<D, BF16, true, false>(maps, p, sms, st) : launch_bwd<D, BF16, false, false>(maps, p, sms, st);
+}
+
+#ifndef FA2_BWD_PAIR
+#define FA2_BWD_PAIR 1   // 0: the one-SM d = 128 backward kernel for every shape (A/B builds)
+#endif
+// CTA-pair backward (fa2_bwd2_sm100.cuh): d = 128, square fixed-length, arrival-order dQ.
+// p arrives with the 128-row tiling; the pair kernel tiles keys by 256.
+template <bool BF16, bool CAUSAL>
+fa2_status_t launch_bwd_pair(const fa2::BwdMaps& maps, const CUtensorMap& mq64, const CUtensorMap& mdo64,
+                             fa2::BwdParams p, int sms, cudaStream_t st) {
+  auto kern = fa2::fa2_bwd_pair_kernel<BF16, CAUSAL>;
+  constexpr int smem = fa2::BwdPairSmem::ALLOC;
+  fa2_status_t s = set_smem(kern, smem);
+  if (s != FA2_OK) return s;
+  const int N = p.geom.Nq;
+  p.num_n_blocks = (N + 255) / 256;
+  p.num_tiles = (p.BH / p.group) * p.num_n_blocks;
+  int npairs = std::min(p.num_tiles, std::min(sms / 2, max_active_pairs(kern, smem, fa2::kBwdThreads, sms)));
+  fa2::SchedT<CAUSAL> sched;
+  sched.n = 0;
+  if constexpr (CAUSAL) {   // balanced pair-tile lists: key block nb2 sees nqb - 2 nb2 query tiles per head
+    if (FA2_SCHED && p.num_tiles <= fa2::kSchedMaxTiles && npairs <= fa2::kSchedMaxCtas) {
+      const int nnb2 = p.num_n_blocks, group = p.group, nt = p.num_tiles;
+      const SchedPtr sc = cached_sched(2, nt, nnb2, N, group, npairs, [&](std::vector<int>& work) {
+        const int nqb = (N + 127) / 128;
+        for (int t = 0; t < nt; ++t) work[t] = (nqb - 2 * (t % nnb2)) * group + 1;
+      });
+      mark(3, st);
+      kern<<<2 * npairs, fa2::kBwdThreads, smem, st>>>(mq64, maps.q, maps.k, maps.v, mdo64, maps.dout, p, *sc);
+      mark(4, st);
+      FA2_CUDA(cudaGetLastError());
+      return FA2_OK;
+    }
+  }
+  mark(3, st);
+  kern<<<2 * npairs, fa2::kBwdThreads, smem, st>>>(mq64, maps.q, maps.k, maps.v, mdo64, maps.dout, p, sched);
+  mark(4, st);
+  FA2_CUDA(cudaGetLastError());
+  return FA2_OK;
 }
 
 // GQA load balance (BwdParams::hsplit): the query heads of a key/value group are split
@@ -674,7 +735,19 @@ fa2_status_t backward_impl(const void* q, const void* k, const void* v, const vo
   p.acc_rows = wl.rows;
   p.tile_off = rp.tile_off;
   const bool bf16 = dtype == FA2_BF16;
-  if (g.d == 64)
+  // the CTA-pair kernel is opt-in (FA2_BWD_PAIR=1 in the environment): measured slower than the
+  // one-SM kernel on B200, kept as a tested alternative
+  static const bool pair_env = [] { const char* e = std::getenv("FA2_BWD_PAIR"); return e && e[0] == '1'; }();
+  const bool pair = FA2_BWD_PAIR && pair_env && g.d == 128 && !g.packed && g.Nq == g.Nk && !deterministic && hsplit == 1;
+  if (pair) {
+    CUtensorMap mq64, mdo64;
+    if ((s = make_rows_map(&mq64, q, dt, g, g.H, true, 2, 64)) != FA2_OK) return s;
+    if ((s = make_rows_map(&mdo64, dout, dt, g, g.H, true, 2, 64)) != FA2_OK) return s;
+    s = bf16 ? (causal ? launch_bwd_pair<true, true>(maps, mq64, mdo64, p, sms, st)
+                       : launch_bwd_pair<true, false>(maps, mq64, mdo64, p, sms, st))
+             : (causal ? launch_bwd_pair<false, true>(maps, mq64, mdo64, p, sms, st)
+                       : launch_bwd_pair<false, false>(maps, mq64, mdo64, p, sms, st));
+  } else if (g.d == 64)
     s = bf16 ? dispatch_bwd_causal<64, true>(causal, maps, p, sms, st) : dispatch_bwd_causal<64, false>(causal, maps, p, sms, st);
   else
     s = bf16 ? dispatch_bwd_causal<128, true>(causal, maps, p, sms, st)
@@ -695,6 +768,14 @@ fa2_status_t backward_impl(const void* q, const void* k, const void* v, const vo
     if (g.d == 64) {
       if (bf16) fa2::fa2_dq_convert<64, true><<<static_cast<int>(grid), 256, 0, st>>>(rp, rows_out);
       else fa2::fa2_dq_convert<64, false><<<static_cast<int>(grid), 256, 0, st>>>(rp, rows_out);
+    } else if (pair) {   // the pair kernel's chunked accumulator layout, one thread per (padded row, 8 columns)
+      const long long pgrid = (wl.rows * (g.d / 8) + 255) / 256;
+      if (bf16) fa2::fa2_dq_convert_pair<true><<<static_cast<int>(pgrid), 256, 0, st>>>(rp);
+      else fa2::fa2_dq_convert_pair<false><<<static_cast<int>(pgrid), 256, 0, st>>>(rp);
+    } else if (fa2::kBwdDqLsu) {   // fa2_bwd128_kernel's chunked accumulator layout
+      const long long cgrid = (wl.rows / 4 * (g.d / 8) + 255) / 256;
+      if (bf16) fa2::fa2_dq_convert_chunked<true><<<static_cast<int>(cgrid), 256, 0, st>>>(rp);
+      else fa2::fa2_dq_convert_chunked<false><<<static_cast<int>(cgrid), 256, 0, st>>>(rp);
     } else {
       if (bf16) fa2::fa2_dq_convert<128, true><<<static_cast<int>(grid), 256, 0, st>>>(rp, rows_out);
       else fa2::fa2_dq_convert<128, false><<<static_cast<int>(grid), 256, 0, st>>>(rp, rows_out);
@@ -761,13 +842,13 @@ fa2_status_t fa2_tile_schedule(int pass, int heads, int N, int heads_per_tile, i
   if (T > fa2::kSchedMaxTiles || T > capacity)
     return fail(FA2_ERR_INVALID_ARG, "fa2_tile_schedule: %lld tiles (max %d, capacity %d)", T, fa2::kSchedMaxTiles,
                 capacity);
-  const fa2::TileSched* sc;
+  SchedPtr sc;
   if (pass == 0) {
     fa2::FwdParams p{};
     p.num_m_blocks = static_cast<int>(per_head);
     p.num_tiles = static_cast<int>(T);
     p.geom.Nq = p.geom.Nk = N;
-    sc = &fwd_sched(p, grid);
+    sc = fwd_sched(p, grid);
   } else {
     fa2::BwdParams p{};
     p.num_n_blocks = static_cast<int>(per_head);
@@ -775,7 +856,7 @@ fa2_status_t fa2_tile_schedule(int pass, int heads, int N, int heads_per_tile, i
     p.geom.Nq = p.geom.Nk = N;
     p.group = heads_per_tile;
     p.hsplit = 1;
-    sc = &bwd_sched(p, grid);
+    sc = bwd_sched(p, grid);
   }
   for (int c = 0; c <= grid; ++c) start[c] = sc->start[c];
   for (long long t = 0; t < T; ++t) order[t] = sc->order[t];

@@ -28,7 +28,23 @@
 #pragma once
 #include "fa2_bwd_sm100.cuh"
 
+// dQ^T reduce-added straight from registers (red.global.add.v4.f32) into a chunked dQ_acc
+// layout ([q/4][d][4] per 128-row tile) instead of SMEM staging + TMA bulk reduce-adds
+#ifndef FA2_BWD_DQ_LSU
+#define FA2_BWD_DQ_LSU 1
+#endif
+#ifndef FA2_BWD_RED_PACE
+#define FA2_BWD_RED_PACE 0
+#endif
+
+// FMA-pipe exponential pairs per 16 in the P^T phase (unmasked tiles, square geometry)
+#ifndef FA2_BWD_EMU
+#define FA2_BWD_EMU 4
+#endif
+
 namespace fa2 {
+
+constexpr bool kBwdDqLsu = FA2_BWD_DQ_LSU != 0;
 
 struct Bwd128Smem {
   static constexpr int D = 128, BM = 128;
@@ -157,23 +173,48 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
         ptx::mbar_wait(s_full, g & 1);
         if (threadIdx.x == 0) FA2_BTRACE(0, g);
         ptx::tc_fence_after();
+        // L, D of the warpgroup's 64 query columns come as float4 broadcasts; the exponent
+        // argument as packed FFMA2; in unmasked tiles FA2_BWD_EMU of every 16 exponential
+        // pairs run as the degree-3 polynomial on the FMA pipe (MUFU.EX2 is this phase's bound)
         float pf[64];
+        const float2 sl2x2 = make_float2(p.scale_log2, p.scale_log2);
+        auto p_block = [&](auto emu_tag) {
+          constexpr int EMU = decltype(emu_tag)::value;
 #pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
-          uint32_t sv[32];
-          ptx::tmem_ld_x32(tmem + lane_base + T_S + c0 + ch * 32, sv);
-          ptx::tmem_wait_ld();
+          for (int ch = 0; ch < 2; ++ch) {
+            uint32_t sv[32];
+            ptx::tmem_ld_x32(tmem + lane_base + T_S + c0 + ch * 32, sv);
+            ptx::tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const int c = c0 + ch * 32 + e;
-            float pv = ptx::ex2(fmaf(__uint_as_float(sv[e]), p.scale_log2, -ptx::lds_f32(vL2 + c * 4)));
-            if (need_mask) {
-              const int q_row = i * BM + c;
-              if ((CAUSAL && kv_row > q_row + off) || kv_row >= nk) pv = 0.f;
+            for (int e4 = 0; e4 < 8; ++e4) {
+              const float4 l4 = ptx::lds_v4f(vL2 + (c0 + ch * 32 + e4 * 4) * 4);
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int e = e4 * 4 + 2 * h;   // column within this 32-column chunk
+                const float2 x2 = ptx::ffma2(make_float2(__uint_as_float(sv[e]), __uint_as_float(sv[e + 1])), sl2x2,
+                                             h == 0 ? make_float2(-l4.x, -l4.y) : make_float2(-l4.z, -l4.w));
+                float2 pr;
+                if ((ch * 16 + e / 2) % 16 < EMU) {
+                  pr = ptx::exp2_poly2(x2);
+                } else {
+                  pr.x = ptx::ex2(x2.x);
+                  pr.y = ptx::ex2(x2.y);
+                }
+                if (EMU == 0 && need_mask) {
+                  const int q_row = i * BM + c0 + ch * 32 + e;
+                  if ((CAUSAL && kv_row > q_row + off) || kv_row >= nk) pr.x = 0.f;
+                  if ((CAUSAL && kv_row > q_row + 1 + off) || kv_row >= nk) pr.y = 0.f;
+                }
+                pf[ch * 32 + e] = pr.x;
+                pf[ch * 32 + e + 1] = pr.y;
+              }
             }
-            pf[ch * 32 + e] = pv;
           }
-        }
+        };
+        // rows that see no key (R23) carry L*log2e = +inf: the polynomial would give 2^-125
+        // instead of 0, so the general geometry keeps MUFU everywhere
+        if (need_mask || GEN) p_block(std::integral_constant<int, 0>{});
+        else p_block(std::integral_constant<int, FA2_BWD_EMU>{});
         if (threadIdx.x == 0) FA2_BTRACE(15, g);
         {
           uint32_t pk[32];
@@ -198,11 +239,16 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
           ptx::tmem_ld_x32(tmem + lane_base + T_DP + c0 + ch * 32, dv);
           ptx::tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int c = c0 + ch * 32 + 2 * e;
-            const float d0 = pf[ch * 32 + 2 * e] * (__uint_as_float(dv[2 * e]) - ptx::lds_f32(vD + c * 4));
-            const float d1 = pf[ch * 32 + 2 * e + 1] * (__uint_as_float(dv[2 * e + 1]) - ptx::lds_f32(vD + c * 4 + 4));
-            dk[ch * 16 + e] = ptx::pack2<BF16>(d0, d1);
+          for (int e4 = 0; e4 < 8; ++e4) {
+            const float4 d4 = ptx::lds_v4f(vD + (c0 + ch * 32 + e4 * 4) * 4);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int e = e4 * 4 + 2 * h;
+              const float2 t2 = ptx::fadd2(make_float2(__uint_as_float(dv[e]), __uint_as_float(dv[e + 1])),
+                                           h == 0 ? make_float2(-d4.x, -d4.y) : make_float2(-d4.z, -d4.w));
+              const float2 s2 = ptx::fmul2(make_float2(pf[ch * 32 + e], pf[ch * 32 + e + 1]), t2);
+              dk[ch * 16 + e / 2] = ptx::pack2<BF16>(s2.x, s2.y);
+            }
           }
         }
         if (threadIdx.x == 0) FA2_BTRACE(11, g);
@@ -297,6 +343,31 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(dq_empty);
         if (leader) FA2_BTRACE(10, g);
+        if constexpr (kBwdDqLsu) {
+          // straight from registers: the tile's dQ_acc block is laid out [q/4][d][4], so one
+          // red.v4 of a warp (32 consecutive d, 4 query rows each) covers 512 contiguous bytes
+          if (p.dq_sem != nullptr) {
+            if (leader) dq_sem_wait(dq_sem_ptr(p, acc0, i), dq_rank(p, nb, x % nqt));
+            ptx::named_bar_sync(1, 128);
+          }
+          float* const dst = dq_rows + r * 4;
+          const long long t0 = clock64();
+#pragma unroll
+          for (int qc = 0; qc < BM / 4; ++qc) {
+            if (FA2_BWD_RED_PACE > 0 && qc % 4 == 0 && qc > 0)
+              while (clock64() - t0 < static_cast<long long>(qc / 4) * FA2_BWD_RED_PACE) {}
+            ptx::red_add_v4_f32(dst + qc * (4 * D), __uint_as_float(v[4 * qc]) * p.scale,
+                                __uint_as_float(v[4 * qc + 1]) * p.scale, __uint_as_float(v[4 * qc + 2]) * p.scale,
+                                __uint_as_float(v[4 * qc + 3]) * p.scale);
+          }
+          if (p.dq_sem != nullptr) {   // the reductions are performed before the release is observed
+            __threadfence();
+            ptx::named_bar_sync(1, 128);
+            if (leader) ptx::st_release_gpu(dq_sem_ptr(p, acc0, i), dq_rank(p, nb, x % nqt) + 1);
+          }
+          if (leader) FA2_BTRACE(16, g);
+          continue;
+        }
         // rounds of DQ_ROWS query rows, row-major [rows][128] fp32 staging (a warp's 32 lanes
         // write 128 contiguous bytes: conflict-free), each round one contiguous 8 KB bulk
         // reduce-add (dQ_acc rows are d*4 = 512 B apart, so DQ_ROWS rows are contiguous)
@@ -324,7 +395,7 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
         if (leader) FA2_BTRACE(16, g);
       }
     }
-    if (leader) ptx::bulk_wait<0>();
+    if (!kBwdDqLsu && leader) ptx::bulk_wait<0>();
   } else if (warp == 12) {
     // ================== MMA issuer: whole warp, one elected lane issues ==================
     ptx::setmaxnreg_dec<48>();

@@ -1,0 +1,681 @@
+// FlashAttention-2 backward (Alg. 2) on a CTA pair (cluster of 2,
+// tcgen05 cta_group::2): the d = 128, square fixed-length, arrival-order path.
+//
+// Why a pair.  On one SM (fa2_bwd128_sm100.cuh) every 128 x 128 tile
+// sends 64 KB of fp32 dQ partials to L2, and the chip's L2 reduction rate (~6 TB/s,
+// ~20 B/clk/SM) then needs >= ~3100 cycles per tile against a 2560-cycle MMA floor; the
+// staging of those partials also costs 128 KB of the SM's 128 B/clk shared-memory
+// bandwidth per tile.  Here a work tile is a 256-row key block split over the pair
+// (CTA r owns key rows [256 nb2 + 128 r, +128)), and dQ_i = dS_i K_j contracts over all
+// 256 keys in ONE M = 128 cta_group::2 MMA whose output rows are split between the CTAs
+// (CTA r: query rows [64 r, 64 r + 64) of the tile, all of d).  Each CTA then reduce-adds
+// 32 KB per tile instead of 64 KB; the price is 16 KB of dS exchanged through DSMEM.
+// The B operands of S^T, dP^T, dV and dK are split between the CTAs too (each SM reads
+// half of them), so the SMEM -> tensor-core traffic per tile drops by a quarter.
+//
+// Per query tile i (128 rows) and query head (all heads of the GQA group),
+// every MMA issued by the leader CTA (rank 0):
+//   S^T  = K_j Q_i^T     M=256 N=128 K=d   A = own K (SS)       B = own 64 query rows, all d
+//   dP^T = V_j dO_i^T    M=256 N=128 K=d   A = own V            B = own 64 dO rows, all d
+//   dV  += P^T dO_i      M=256 N=d   K=128 A = P^T (TMEM, TS)   B = all 128 dO rows, own 64 d
+//   dK  += dS^T Q_i      M=256 N=d   K=128 A = dS^T (TMEM, TS)  B = all 128 Q rows, own 64 d
+//   dQ_i = dS_i K_j      M=128 N=d   K=256 A = dS (own 64 query rows x 256 keys, SMEM)
+//                                          B = K (256 keys x own 64 d, SMEM)
+// dQ lands in each CTA's TMEM as 64 rows x 128 d folded onto 128 lanes x 64 columns
+// (lanes 0-63: d [0,64), lanes 64-127: d [64,128), lane % 64 = query row).
+//
+// TMEM (512 columns per CTA): S^T [0,128) | dP^T [128,256) | dV [256,384) | dK [384,512);
+// P^T / dS^T overwrite S^T / dP^T in place (packed pairs), dQ overwrites dP^T [128,192)
+// after dK has read dS^T.  MMA issue order per query tile as in the one-SM kernel:
+//   dV(i), dP^T(i) [dQ(i-1) read out], S^T(i+1), dK(i) + dQ(i) [dS(i) ready].
+//
+// Shared memory per CTA (1024-B aligned boxes of 128-B swizzled rows):
+//   K   32 KB  own key rows, d halves 0 | 1               (A of S^T, K-major)
+//   V   32 KB  own key rows                               (A of dP^T)
+//   Kd  32 KB  K rows of CTA 0 | CTA 1, own d half        (B of dQ, MN-major)
+//   QS  2 x 16 KB  own 64 query rows, d halves 0 | 1     (B of S^T; 2-stage ring)
+//   QK  16 KB  128 query rows, own d half                 (B of dK, MN-major)
+//   DOP 16 KB  own 64 dO rows, d halves 0 | 1             (B of dP^T)
+//   DOV 16 KB  128 dO rows, own d half                    (B of dV)
+//   DS  32 KB  dS of the own query half: keys of CTA 0 | CTA 1 (A of dQ, MN-major);
+//              the compute warpgroup of query half h writes its rows into CTA h
+//   DQ  8 KB   2 x 4 KB fp32 staging of the dQ reduce-add
+//   VEC 2 KB   L_i * log2(e), D_i (2 stages)
+//
+// dQ_acc layout (workspace, fp32): inside every 128-row tile of the padded rows, element
+// (q, c) at float ((q / 64) * 32 + c / 4) * 256 + (q % 64) * 4 + c % 4, so each red.v4 of a
+// dQ warp (32 consecutive rows, 4 columns) covers 512 contiguous bytes; fa2_dq_convert_pair
+// casts it back.
+//
+// Barriers the leader's MMA warp waits on live in the leader: TMA loads of both CTAs
+// complete on them (cta_group::2 TMA), warps of both CTAs arrive on them remotely.
+// Barriers released by MMAs (s_full, dp_full, dq_full, dkv_full, *_empty) are signalled
+// in both CTAs by multicast tcgen05.commit.  L_i / D_i are per-CTA (local barriers).
+//
+// Warp roles (512 threads per CTA): warps 0-7 compute (P^T, dS^T; warpgroup w owns query
+// columns [64 w, 64 w + 64)), warps 8-11 dQ read-out + reduce-add, warp 12 MMA issuer
+// (leader only), warp 13 TMA producer, warps 14-15 idle.
+#pragma once
+#include "fa2_bwd_sm100.cuh"
+#include "sm100_pair.cuh"
+
+// FMA-pipe exponential pairs per 16 in the P^T phase (unmasked tiles)
+#ifndef FA2_BWD_PAIR_EMU
+#define FA2_BWD_PAIR_EMU 4
+#endif
+// stages of the own-query-rows Q ring (B operand of S^T)
+#ifndef FA2_BWD_PAIR_QSTAGES
+#define FA2_BWD_PAIR_QSTAGES 1
+#endif
+
+namespace fa2 {
+
+struct BwdPairSmem {
+  static constexpr int BOX128 = 128 * 128;      // 128 rows x 128 B
+  static constexpr int BOX64 = 64 * 128;        // 64 rows x 128 B
+  static constexpr int QSTAGES = FA2_BWD_PAIR_QSTAGES;
+  static constexpr int OFF_K = 0;
+  static constexpr int OFF_V = OFF_K + 2 * BOX128;
+  static constexpr int OFF_KD = OFF_V + 2 * BOX128;
+  static constexpr int OFF_QS = OFF_KD + 2 * BOX128;
+  static constexpr int QS_STAGE = 2 * BOX64;
+  static constexpr int OFF_QK = OFF_QS + QSTAGES * QS_STAGE;
+  static constexpr int OFF_DOP = OFF_QK + BOX128;
+  static constexpr int OFF_DOV = OFF_DOP + 2 * BOX64;
+  static constexpr int OFF_DS = OFF_DOV + BOX128;      // [2 buffers] A0 | A1 (dQ's A operand)
+  static constexpr int DS_BUF = 2 * BOX128;
+  static constexpr int OFF_VEC = OFF_DS + 2 * DS_BUF;  // [2][2][128] floats: L2, D
+  static constexpr int OFF_BAR = OFF_VEC + 2 * 2 * 128 * 4;
+  static constexpr int NBAR = 32;
+  static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
+  static constexpr int BYTES = OFF_TMEM + 16;
+  // no alignment slack: the dynamic shared window starts 1024-B aligned (checked in the kernel)
+  static constexpr int ALLOC = BYTES;
+  static_assert(ALLOC <= 232448, "shared memory budget");
+};
+
+// A pair work tile: key block nb2 (256 rows) of key/value head kvh of batch b, visited
+// with query tiles i0 .. nqb-1 of every query head of the group.
+struct PairTile {
+  int b, kvh, nb2, i0, nqt;
+};
+FA2_DEVICE PairTile pair_tile(const BwdParams& p, bool causal, int t) {
+  PairTile w;
+  const int bh = t / p.num_n_blocks;
+  w.nb2 = t % p.num_n_blocks;
+  w.b = bh / p.Hkv;
+  w.kvh = bh % p.Hkv;
+  const int nqb = (p.geom.Nq + 127) / 128;
+  w.i0 = causal ? 2 * w.nb2 : 0;   // first query tile that sees key 256 nb2 (CTA 0's first key)
+  w.nqt = nqb - w.i0;
+  return w;
+}
+
+template <bool BF16, bool CAUSAL>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBwdThreads, 1)
+fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_constant__ CUtensorMap tm_q128,
+                    const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                    const __grid_constant__ CUtensorMap tm_do64, const __grid_constant__ CUtensorMap tm_do128,
+                    const BwdParams p, const __grid_constant__ SchedT<CAUSAL> sched) {
+  using L = BwdPairSmem;
+  constexpr int D = 128, BM = 128;
+  constexpr uint32_t QST = L::QSTAGES;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if (ptx::smem_u32(smem) & 1023u) __trap();   // SW128 tiles and descriptors need 1024-B alignment
+  uint8_t* sK = smem + L::OFF_K;
+  uint8_t* sV = smem + L::OFF_V;
+  uint8_t* sKd = smem + L::OFF_KD;
+  uint8_t* sQS = smem + L::OFF_QS;
+  uint8_t* sQK = smem + L::OFF_QK;
+  uint8_t* sDOP = smem + L::OFF_DOP;
+  uint8_t* sDOV = smem + L::OFF_DOV;
+  uint8_t* sDS = smem + L::OFF_DS;
+  float* sVec = reinterpret_cast<float*>(smem + L::OFF_VEC);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  // leader-side (the MMA warp waits; arrivals / tx from both CTAs)
+  uint64_t* kv_full = bars + 0;
+  uint64_t* q_full = bars + 1;      // [2]
+  uint64_t* qk_full = bars + 3;
+  uint64_t* dop_full = bars + 4;
+  uint64_t* dov_full = bars + 5;
+  uint64_t* p_ready = bars + 6;     // 16 arrivals: 8 compute warps x 2 CTAs
+  uint64_t* ds_ready = bars + 7;    // 16
+  uint64_t* dq_empty = bars + 8;    // 8: 4 dQ warps x 2 CTAs
+  uint64_t* dkv_empty = bars + 9;   // 16
+  // released by the MMAs (multicast commit: both CTAs)
+  uint64_t* kv_empty = bars + 10;
+  uint64_t* q_empty = bars + 11;    // [2]
+  uint64_t* qk_empty = bars + 13;
+  uint64_t* dop_empty = bars + 14;
+  uint64_t* dov_empty = bars + 15;
+  uint64_t* s_full = bars + 16;
+  uint64_t* dp_full = bars + 17;
+  uint64_t* dq_full = bars + 18;
+  uint64_t* dkv_full = bars + 19;
+  // local
+  uint64_t* vec_full = bars + 20;   // [2]
+  uint64_t* vec_empty = bars + 22;  // [2]
+  uint64_t* dsx_full = bars + 24;   // [2] local: the peer's dS half of buffer b has landed here (tx bytes)
+  uint64_t* dsx_ready = bars + 26;  // [2] leader: CTA 1's dsx_full[b] completed (relayed by its warp 14)
+  uint64_t* dq_done = bars + 28;    // [2] dQ of the last step that used dS buffer b has completed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t rank = pair::cta_rank();
+  const int pair_id = static_cast<int>(pair::cluster_id()), npairs = static_cast<int>(pair::num_clusters());
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(kv_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(&dsx_full[s], 1);
+      ptx::mbar_init(&dsx_ready[s], 1);
+      ptx::mbar_init(&dq_done[s], 1);
+      ptx::mbar_init(&q_full[s], 1);
+      ptx::mbar_init(&q_empty[s], 1);
+      ptx::mbar_init(&vec_full[s], 1);
+      ptx::mbar_init(&vec_empty[s], 8);
+    }
+    ptx::mbar_init(qk_full, 1);
+    ptx::mbar_init(dop_full, 1);
+    ptx::mbar_init(dov_full, 1);
+    ptx::mbar_init(p_ready, 16);
+    ptx::mbar_init(ds_ready, 16);
+    ptx::mbar_init(dq_empty, 8);
+    ptx::mbar_init(dkv_empty, 16);
+    ptx::mbar_init(kv_empty, 1);
+    ptx::mbar_init(qk_empty, 1);
+    ptx::mbar_init(dop_empty, 1);
+    ptx::mbar_init(dov_empty, 1);
+    ptx::mbar_init(s_full, 1);
+    ptx::mbar_init(dp_full, 1);
+    ptx::mbar_init(dq_full, 1);
+    ptx::mbar_init(dkv_full, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 13 && lane == 0) {
+    ptx::tma_prefetch_desc(&tm_q64); ptx::tma_prefetch_desc(&tm_q128); ptx::tma_prefetch_desc(&tm_k);
+    ptx::tma_prefetch_desc(&tm_v); ptx::tma_prefetch_desc(&tm_do64); ptx::tma_prefetch_desc(&tm_do128);
+  }
+  if (warp == 0)
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(ptx::smem_u32(tmem_slot)), "r"(512));
+  ptx::tc_fence_before();
+  pair::cluster_sync();   // barriers initialised and TMEM allocated in both CTAs
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t T_S = 0, T_DP = 128, T_DV = 256, T_DK = 384, T_DQ = 64;
+  const int N = p.geom.Nq;
+
+  if (warp < 8) {
+    // ====================== compute warpgroups: P^T, dS^T ======================
+    ptx::setmaxnreg_inc<152>();
+    const int wg = warp / 4;
+    const int r = threadIdx.x % 128;                   // key row within the CTA's block == TMEM lane
+    const uint32_t lane_base = static_cast<uint32_t>((warp % 4) * 32) << 16;
+    const uint32_t sVec_a = ptx::smem_u32(sVec);
+    const int c0 = wg * 64;                             // this warpgroup's 64 query columns
+    // dS row r, query columns [c0, c0 + 64) (128-B swizzled MN-major rows) -> key slot A_rank of
+    // the CTA whose dQ rows they are: the own query half (wg == rank) with plain stores, the
+    // other half straight into the peer's shared memory with st.async, whose bytes complete on
+    // the peer's dsx_full (no fence or wait on this side)
+    const bool own_half = static_cast<uint32_t>(wg) == rank;
+    const uint32_t ds_row = ptx::smem_u32(sDS) + rank * L::BOX128 + (r / 8) * 1024 + (r % 8) * 128;
+    const uint32_t peer = rank ^ 1u;
+    const uint32_t ds_row_peer = pair::map_cta(ds_row, peer);
+    const uint32_t x_bar = pair::map_cta(ptx::smem_u32(dsx_full), peer);   // + 8 * buffer
+    const uint32_t qbar = 2 + (warp % 4);   // named barrier of the two warps sharing these TMEM lanes
+    const float sl2 = p.scale_log2;
+    uint32_t g = 0;
+    int it = 0;
+    for (int n_ = 0, t; (t = pair::sched_tile_pair(sched, n_, p.num_tiles, pair_id, npairs)) >= 0; ++n_, ++it) {
+      const PairTile w = pair_tile(p, CAUSAL, t);
+      const int kv_row = w.nb2 * 256 + static_cast<int>(rank) * 128 + r;
+      const int nx = w.nqt * p.group;
+      for (int x = 0; x < nx; ++x, ++g) {
+        const int i = w.i0 + x % w.nqt;
+        const uint32_t slot = g & 1;
+        const uint32_t vL2 = sVec_a + slot * 2 * BM * 4 + c0 * 4, vD = vL2 + BM * 4;
+        // mask: causal tiles crossing the diagonal and the ragged key tail (query rows past N
+        // need none: their L*log2e is +inf, so P = 0)
+        const int kv_first = w.nb2 * 256 + static_cast<int>(rank) * 128;
+        const bool need_mask = (CAUSAL && kv_first + 127 > i * BM) || (kv_first + 128 > N);
+        ptx::mbar_wait(&vec_full[slot], (g >> 1) & 1);
+        ptx::mbar_wait(s_full, g & 1);
+        if (threadIdx.x == 0) FA2_BTRACE(0, g);
+        ptx::tc_fence_after();
+        // ---- P^T = exp2(S^T * scale*log2e - L*log2e), masked ----
+        float pf[64];
+        const float2 sl2x2 = make_float2(sl2, sl2);
+        auto p_block = [&](auto emu_tag) {
+          constexpr int EMU = decltype(emu_tag)::value;
+#pragma unroll
+          for (int ch = 0; ch < 2; ++ch) {
+            uint32_t sv[32];
+            ptx::tmem_ld_x32(tmem + lane_base + T_S + c0 + ch * 32, sv);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int e4 = 0; e4 < 8; ++e4) {
+              const float4 l4 = ptx::lds_v4f(vL2 + (ch * 32 + e4 * 4) * 4);
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int e = ch * 32 + e4 * 4 + 2 * h;   // column within the warpgroup's 64
+                const float2 x2 = ptx::ffma2(make_float2(__uint_as_float(sv[e - ch * 32]), __uint_as_float(sv[e - ch * 32 + 1])),
+                                             sl2x2, h == 0 ? make_float2(-l4.x, -l4.y) : make_float2(-l4.z, -l4.w));
+                float2 pr;
+                if ((e / 2) % 16 < EMU) {
+                  pr = ptx::exp2_poly2(x2);
+                } else {
+                  pr.x = ptx::ex2(x2.x);
+                  pr.y = ptx::ex2(x2.y);
+                }
+                if (!EMU && need_mask) {
+                  const int q_row = i * BM + c0 + e;
+                  if ((CAUSAL && kv_row > q_row) || kv_row >= N) pr.x = 0.f;
+                  if ((CAUSAL && kv_row > q_row + 1) || kv_row >= N) pr.y = 0.f;
+                }
+                pf[e] = pr.x;
+                pf[e + 1] = pr.y;
+              }
+            }
+          }
+        };
+        if (need_mask) p_block(std::integral_constant<int, 0>{});
+        else p_block(std::integral_constant<int, FA2_BWD_PAIR_EMU>{});
+        if (threadIdx.x == 0) FA2_BTRACE(15, g);
+        {
+          // packed P^T, contiguous: query columns [0,64) at TMEM cols [0,32), [64,128) at [32,64)
+          // (A operand of dV); warpgroup 1 overwrites S^T columns warpgroup 0 reads, so it waits
+          // for its partner warp (same lanes) to have loaded them.  Cols [64,128) are then free
+          // for dQ.
+          uint32_t pk[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) pk[e] = ptx::pack2<BF16>(pf[2 * e], pf[2 * e + 1]);
+          if (wg == 0) ptx::named_bar_arrive(qbar, 64);
+          else ptx::named_bar_sync(qbar, 64);
+          ptx::tmem_st_x32(tmem + lane_base + T_S + wg * 32, pk);
+        }
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) pair::arrive_remote(p_ready, 0);
+        if (threadIdx.x == 0) FA2_BTRACE(1, g);
+        // ---- dS^T = P^T o (dP^T - D) ----
+        ptx::mbar_wait(dp_full, g & 1);
+        if (threadIdx.x == 0) FA2_BTRACE(2, g);
+        ptx::tc_fence_after();
+        uint32_t dk[32];
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+          uint32_t dv[32];
+          ptx::tmem_ld_x32(tmem + lane_base + T_DP + c0 + ch * 32, dv);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int e4 = 0; e4 < 8; ++e4) {
+            const float4 d4 = ptx::lds_v4f(vD + (ch * 32 + e4 * 4) * 4);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int e = e4 * 4 + 2 * h;
+              const float2 t2 = ptx::fadd2(make_float2(__uint_as_float(dv[e]), __uint_as_float(dv[e + 1])),
+                                           h == 0 ? make_float2(-d4.x, -d4.y) : make_float2(-d4.z, -d4.w));
+              const float2 s2 = ptx::fmul2(make_float2(pf[ch * 32 + e], pf[ch * 32 + e + 1]), t2);
+              dk[ch * 16 + e / 2] = ptx::pack2<BF16>(s2.x, s2.y);
+            }
+          }
+        }
+        if (threadIdx.x == 0) FA2_BTRACE(11, g);
+        ptx::tmem_st_x32(tmem + lane_base + T_DP + c0, dk);   // A operand of dK
+        // dS buffer g % 2 was last read by dQ two steps ago: wait for it (usually long done)
+        const uint32_t db = g & 1;
+        if (g >= 2) ptx::mbar_wait(&dq_done[db], ((g >> 1) - 1) & 1);
+        if (own_half) {
+#pragma unroll
+          for (int q8 = 0; q8 < 8; ++q8)
+            ptx::sts_v4(ds_row + db * L::DS_BUF + ((q8 ^ (r % 8)) * 16), dk[4 * q8], dk[4 * q8 + 1], dk[4 * q8 + 2],
+                        dk[4 * q8 + 3]);
+        } else {
+#pragma unroll
+          for (int q8 = 0; q8 < 8; ++q8)
+            pair::st_async_v4(ds_row_peer + db * L::DS_BUF + ((q8 ^ (r % 8)) * 16), dk[4 * q8], dk[4 * q8 + 1],
+                              dk[4 * q8 + 2], dk[4 * q8 + 3], x_bar + db * 8);
+        }
+        if (threadIdx.x == 0) FA2_BTRACE(12, g);
+        ptx::tmem_wait_st();
+        if (threadIdx.x == 0) FA2_BTRACE(13, g);
+        ptx::fence_proxy_async_smem();
+        if (threadIdx.x == 0) FA2_BTRACE(14, g);
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          pair::arrive_remote(ds_ready, 0);
+          ptx::mbar_arrive(&vec_empty[slot]);
+        }
+        if (threadIdx.x == 0) FA2_BTRACE(3, g);
+      }
+      // ---- epilogue: dV_j (warpgroup 0), dK_j * scale (warpgroup 1) ----
+      ptx::mbar_wait(dkv_full, it & 1);
+      ptx::tc_fence_after();
+      {
+        const uint32_t tsrc = tmem + lane_base + (wg == 0 ? T_DV : T_DK);
+        const float mul = wg == 0 ? 1.f : p.scale;
+        uint8_t* dst = reinterpret_cast<uint8_t*>(wg == 0 ? p.dv : p.dk) +
+                       (static_cast<long long>(w.b * p.Hkv + w.kvh) * N + kv_row) * D * 2;
+#pragma unroll
+        for (int ch = 0; ch < D / 32; ++ch) {
+          uint32_t v[32];
+          ptx::tmem_ld_x32(tsrc + ch * 32, v);
+          ptx::tmem_wait_ld();
+          uint32_t o16[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) o16[e] = ptx::pack2<BF16>(__uint_as_float(v[2 * e]) * mul, __uint_as_float(v[2 * e + 1]) * mul);
+          if (kv_row < N) {
+            uint4* o = reinterpret_cast<uint4*>(dst + ch * 64);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) o[e] = make_uint4(o16[4 * e], o16[4 * e + 1], o16[4 * e + 2], o16[4 * e + 3]);
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) pair::arrive_remote(dkv_empty, 0);
+    }
+  } else if (warp < 12) {
+    // ====================== dQ read-out + fp32 reduce-add ======================
+    // straight from registers (red.global.add.v4.f32): a warp's 32 lanes hold 32 consecutive
+    // query rows, so with the [d/4][64 rows][4] accumulator layout every red.v4 of a warp covers
+    // 512 contiguous bytes; no shared-memory staging, no barriers
+    ptx::setmaxnreg_inc<152>();
+    const int quarter = warp % 4;
+    const int row = (quarter % 2) * 32 + lane;          // query row within this CTA's 64
+    const int dh = quarter / 2;                          // d half held by this lane
+    const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
+    const bool leader = (threadIdx.x == 256);
+    uint32_t g = 0;
+    for (int n_ = 0, t; (t = pair::sched_tile_pair(sched, n_, p.num_tiles, pair_id, npairs)) >= 0; ++n_) {
+      const PairTile w = pair_tile(p, CAUSAL, t);
+      const int nx = w.nqt * p.group;
+      for (int x = 0; x < nx; ++x, ++g) {
+        const int i = w.i0 + x % w.nqt;
+        const int hq = w.kvh * p.group + x / w.nqt;
+        // this CTA's 32 KB of the tile (query rows [64 rank, +64)), this lane's d half and row
+        float* const acc = p.dq_acc + ((static_cast<long long>(w.b) * p.H + hq) * p.acc_hs + static_cast<long long>(i) * BM) * D +
+                           (rank * 32 + dh * 16) * 256 + row * 4;
+        ptx::mbar_wait(dq_full, g & 1);
+        if (leader) FA2_BTRACE(9, g);
+        ptx::tc_fence_after();
+        uint32_t v[64];
+        ptx::tmem_ld_x32(tmem + lane_base + T_DQ, v);
+        ptx::tmem_ld_x32(tmem + lane_base + T_DQ + 32, v + 32);
+        ptx::tmem_wait_ld();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) pair::arrive_remote(dq_empty, 0);
+        if (leader) FA2_BTRACE(10, g);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          ptx::red_add_v4_f32(acc + j * 256, __uint_as_float(v[4 * j]) * p.scale, __uint_as_float(v[4 * j + 1]) * p.scale,
+                              __uint_as_float(v[4 * j + 2]) * p.scale, __uint_as_float(v[4 * j + 3]) * p.scale);
+        if (leader) FA2_BTRACE(16, g);
+      }
+    }
+  } else if (warp == 12) {
+    // ================== MMA issuer (leader CTA): whole warp, one elected lane ==================
+    ptx::setmaxnreg_dec<48>();
+    if (rank == 0) {
+      constexpr uint32_t IDESC_S = ptx::idesc_f16(BF16, 256, 128, false, false);   // S^T, dP^T
+      constexpr uint32_t IDESC_G = ptx::idesc_f16(BF16, 256, D, false, true);      // dV, dK
+      constexpr uint32_t IDESC_Q = ptx::idesc_f16(BF16, 128, D, true, true);       // dQ
+      const uint64_t dK_k = ptx::sw128_desc(ptx::smem_u32(sK), 16, 1024);
+      const uint64_t dV_k = ptx::sw128_desc(ptx::smem_u32(sV), 16, 1024);
+      const uint64_t dQS_k = ptx::sw128_desc(ptx::smem_u32(sQS), 16, 1024);
+      const uint64_t dDOP_k = ptx::sw128_desc(ptx::smem_u32(sDOP), 16, 1024);
+      const uint64_t dDOV_mn = ptx::sw128_desc(ptx::smem_u32(sDOV), L::BOX128, 1024);
+      const uint64_t dQK_mn = ptx::sw128_desc(ptx::smem_u32(sQK), L::BOX128, 1024);
+      const uint64_t dDS_mn = ptx::sw128_desc(ptx::smem_u32(sDS), L::BOX128, 1024);
+      const uint64_t dKD_mn = ptx::sw128_desc(ptx::smem_u32(sKd), L::BOX128, 1024);
+      auto mma_s = [&](uint32_t slot) {   // S^T = K Q^T: K = d, 4 steps per 64-column box
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t offa = (k / 4) * L::BOX128 + (k % 4) * 32;
+          const uint32_t offb = slot * L::QS_STAGE + (k / 4) * L::BOX64 + (k % 4) * 32;
+          pair::mma_ss2(tmem + T_S, dK_k + (offa >> 4), dQS_k + (offb >> 4), IDESC_S, k > 0 ? 1u : 0u);
+        }
+      };
+      auto mma_dp = [&]() {   // dP^T = V dO^T
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t offa = (k / 4) * L::BOX128 + (k % 4) * 32;
+          const uint32_t offb = (k / 4) * L::BOX64 + (k % 4) * 32;
+          pair::mma_ss2(tmem + T_DP, dV_k + (offa >> 4), dDOP_k + (offb >> 4), IDESC_S, k > 0 ? 1u : 0u);
+        }
+      };
+      // dQ(y) = dS K over the pair's 256 keys into S^T cols [64,128), once both CTAs' A slots
+      // hold step y's dS (own half stored locally, the peer's half landed by st.async)
+      auto issue_dq = [&](uint32_t y) {
+        const uint32_t db = y & 1, ph = (y >> 1) & 1;
+        ptx::mbar_wait(&dsx_full[db], ph);                 // CTA 1's half landed here
+        pair::wait_cluster_acquire(&dsx_ready[db], ph);   // CTA 0's half landed in CTA 1
+        ptx::fence_proxy_async_smem();
+        ptx::tc_fence_after();
+        if (ptx::elect_one()) {
+#pragma unroll
+          for (int k = 0; k < 256 / 16; ++k) {
+            const uint32_t off = (db * L::DS_BUF + (k / 8) * L::BOX128 + (k % 8) * 2048) >> 4;
+            const uint32_t offb = ((k / 8) * L::BOX128 + (k % 8) * 2048) >> 4;
+            pair::mma_ss2(tmem + T_DQ, dDS_mn + off, dKD_mn + offb, IDESC_Q, k > 0 ? 1u : 0u);
+          }
+          pair::commit_both(dq_full);
+          pair::commit_both(&dq_done[db]);
+        }
+        __syncwarp();
+      };
+      // Issue order for query step x (steady state):
+      //   dV(x) [P^T(x)], dQ(x-1) [dS(x-1) exchanged; S^T cols [64,128) read by P(x)],
+      //   S^T(x+1) [dQ(x-1) read out], dK(x) [dS^T(x)], dP^T(x+1) [dK(x) read dS^T(x), in order]
+      // so dP^T(x+1) never waits for the dQ read-out or the exchange.
+      uint32_t g = 0;
+      int it = 0;
+      for (int n_ = 0, t; (t = pair::sched_tile_pair(sched, n_, p.num_tiles, pair_id, npairs)) >= 0; ++n_, ++it) {
+        const PairTile w = pair_tile(p, CAUSAL, t);
+        const uint32_t n = static_cast<uint32_t>(w.nqt * p.group);
+        const uint32_t g0 = g;
+        ptx::mbar_wait(kv_full, it & 1);
+        ptx::mbar_wait(&q_full[g0 % QST], (g0 / QST) & 1);
+        if (g0 > 0) pair::wait_cluster(dq_empty, (g0 - 1) & 1);   // previous tile's last dQ read out
+        ptx::tc_fence_after();
+        if (ptx::elect_one()) {
+          mma_s(g0 % QST);
+          pair::commit_both(s_full);
+          pair::commit_both(&q_empty[g0 % QST]);
+        }
+        __syncwarp();
+        ptx::mbar_wait(dop_full, g0 & 1);
+        ptx::tc_fence_after();
+        if (ptx::elect_one()) {
+          mma_dp();
+          pair::commit_both(dp_full);
+          pair::commit_both(dop_empty);
+        }
+        __syncwarp();
+        if (it > 0) pair::wait_cluster(dkv_empty, (it - 1) & 1);   // previous dK / dV drained
+        for (uint32_t x = g0; x < g0 + n; ++x) {
+          const bool first = (x == g0);
+          // dV += P^T dO  (A: packed P^T, query columns [0,128) at TMEM cols [0,64))
+          ptx::mbar_wait(dov_full, x & 1);
+          pair::wait_cluster(p_ready, x & 1);
+          FA2_BTRACE(4, x);
+          ptx::tc_fence_after();
+          if (ptx::elect_one()) {
+#pragma unroll
+            for (int k = 0; k < BM / 16; ++k)
+              pair::mma_ts2(tmem + T_DV, tmem + T_S + k * 8, dDOV_mn + ((k * 2048) >> 4), IDESC_G, (!first || k > 0) ? 1u : 0u);
+            pair::commit_both(dov_empty);
+          }
+          __syncwarp();
+          if (!first) issue_dq(x - 1);
+          FA2_BTRACE(5, x);
+          // S^T of the next query tile (its P^T columns were just consumed by dV, in order)
+          if (x + 1 < g0 + n) {
+            ptx::mbar_wait(&q_full[(x + 1) % QST], ((x + 1) / QST) & 1);
+            if (!first) pair::wait_cluster(dq_empty, (x - 1) & 1);
+            ptx::tc_fence_after();
+            if (ptx::elect_one()) {
+              mma_s((x + 1) % QST);
+              pair::commit_both(s_full);
+              pair::commit_both(&q_empty[(x + 1) % QST]);
+            }
+            __syncwarp();
+            FA2_BTRACE(6, x);
+          }
+          // dK += dS^T Q
+          pair::wait_cluster(ds_ready, x & 1);
+          FA2_BTRACE(7, x);
+          ptx::mbar_wait(qk_full, x & 1);
+          ptx::tc_fence_after();
+          if (ptx::elect_one()) {
+#pragma unroll
+            for (int k = 0; k < BM / 16; ++k)
+              pair::mma_ts2(tmem + T_DK, tmem + T_DP + (k / 4) * 64 + (k % 4) * 8, dQK_mn + ((k * 2048) >> 4), IDESC_G,
+                            (!first || k > 0) ? 1u : 0u);
+            pair::commit_both(qk_empty);
+          }
+          __syncwarp();
+          // dP^T of the next query tile (dK just read dS^T(x) out of these columns, in order)
+          if (x + 1 < g0 + n) {
+            ptx::mbar_wait(dop_full, (x + 1) & 1);
+            ptx::tc_fence_after();
+            if (ptx::elect_one()) {
+              mma_dp();
+              pair::commit_both(dp_full);
+              pair::commit_both(dop_empty);
+            }
+            __syncwarp();
+          }
+          FA2_BTRACE(8, x);
+        }
+        issue_dq(g0 + n - 1);
+        g = g0 + n;
+        if (ptx::elect_one()) {
+          pair::commit_both(dkv_full);
+          pair::commit_both(kv_empty);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 13) {
+    // ============================ TMA producer (both CTAs) ============================
+    ptx::setmaxnreg_dec<48>();
+    if (lane == 0) {
+      const float* gD = p.dvec;
+      const float* gL2 = p.dvec + p.acc_rows;
+      const uint64_t pol_q = ptx::l2_policy_evict_last();
+      const uint64_t pol_kv = ptx::l2_policy_evict_first();
+      const int ro = static_cast<int>(rank);
+      uint32_t g = 0;
+      int it = 0;
+      for (int n_ = 0, t; (t = pair::sched_tile_pair(sched, n_, p.num_tiles, pair_id, npairs)) >= 0; ++n_, ++it) {
+        const PairTile w = pair_tile(p, CAUSAL, t);
+        const int kvb = w.b * p.Hkv + w.kvh;
+        if (it > 0) ptx::mbar_wait(kv_empty, (it - 1) & 1);
+        if (rank == 0) ptx::mbar_arrive_expect_tx(kv_full, 2 * 6 * L::BOX128);
+        const int k0 = w.nb2 * 256;
+        for (int s = 0; s < 2; ++s) {
+          pair::tma_load_pair(sK + s * L::BOX128, &tm_k, kv_full, s * 64, k0 + ro * 128, kvb, pol_kv);
+          pair::tma_load_pair(sV + s * L::BOX128, &tm_v, kv_full, s * 64, k0 + ro * 128, kvb, pol_kv);
+          pair::tma_load_pair(sKd + s * L::BOX128, &tm_k, kv_full, ro * 64, k0 + s * 128, kvb, pol_kv);
+        }
+        const int nx = w.nqt * p.group;
+        for (int x = 0; x < nx; ++x, ++g) {
+          const int i = w.i0 + x % w.nqt;
+          const int hq = w.kvh * p.group + x / w.nqt;
+          const int bhq = w.b * p.H + hq;
+          const uint32_t slot = g & 1;
+          // L_i * log2(e), D_i: this CTA's own copy (local barrier)
+          if (g >= 2) ptx::mbar_wait(&vec_empty[slot], ((g >> 1) - 1) & 1);
+          ptx::mbar_arrive_expect_tx(&vec_full[slot], 2 * BM * 4);
+          const long long voff = static_cast<long long>(bhq) * p.acc_hs + static_cast<long long>(i) * BM;
+          ptx::bulk_load_1d(sVec + slot * 2 * BM, gL2 + voff, BM * 4, &vec_full[slot]);
+          ptx::bulk_load_1d(sVec + slot * 2 * BM + BM, gD + voff, BM * 4, &vec_full[slot]);
+          // Q_i rows of this CTA's query half, all d (QST-stage ring; released after S^T(i))
+          const uint32_t qs = g % QST;
+          if (g >= QST) ptx::mbar_wait(&q_empty[qs], ((g / QST) - 1) & 1);
+          if (rank == 0) ptx::mbar_arrive_expect_tx(&q_full[qs], 2 * L::QS_STAGE);
+          for (int s = 0; s < 2; ++s)
+            pair::tma_load_pair(sQS + qs * L::QS_STAGE + s * L::BOX64, &tm_q64, &q_full[qs], s * 64,
+                                i * BM + ro * 64, bhq, pol_q);
+          // dO_i rows of this CTA's query half, all d (released after dP^T(i))
+          if (g >= 1) ptx::mbar_wait(dop_empty, (g - 1) & 1);
+          if (rank == 0) ptx::mbar_arrive_expect_tx(dop_full, 2 * 2 * L::BOX64);
+          for (int s = 0; s < 2; ++s)
+            pair::tma_load_pair(sDOP + s * L::BOX64, &tm_do64, dop_full, s * 64, i * BM + ro * 64, bhq, pol_q);
+          // dO_i all rows, this CTA's d half (released after dV(i))
+          if (g >= 1) ptx::mbar_wait(dov_empty, (g - 1) & 1);
+          if (rank == 0) ptx::mbar_arrive_expect_tx(dov_full, 2 * L::BOX128);
+          pair::tma_load_pair(sDOV, &tm_do128, dov_full, ro * 64, i * BM, bhq, pol_q);
+          // Q_i all rows, this CTA's d half (released after dK(i))
+          if (g >= 1) ptx::mbar_wait(qk_empty, (g - 1) & 1);
+          if (rank == 0) ptx::mbar_arrive_expect_tx(qk_full, 2 * L::BOX128);
+          pair::tma_load_pair(sQK, &tm_q128, qk_full, ro * 64, i * BM, bhq, pol_q);
+        }
+      }
+    }
+  } else if (warp == 14) {
+    // ============ dS exchange bookkeeping (both CTAs) ============
+    // each step the peer's compute warps bulk-copy 4 x 4 KB into this CTA's A slot, completing
+    // on dsx_full; CTA 1 relays its completion to the leader (whose MMA cannot wait on a
+    // remote barrier)
+    ptx::setmaxnreg_dec<48>();
+    if (lane == 0) {
+      uint32_t g = 0;
+      for (int n_ = 0, t; (t = pair::sched_tile_pair(sched, n_, p.num_tiles, pair_id, npairs)) >= 0; ++n_) {
+        const PairTile w = pair_tile(p, CAUSAL, t);
+        const int nx = w.nqt * p.group;
+        for (int x = 0; x < nx; ++x, ++g) {
+          const uint32_t db = g & 1;
+          ptx::mbar_arrive_expect_tx(&dsx_full[db], L::BOX128);
+          ptx::mbar_wait(&dsx_full[db], (g >> 1) & 1);
+          if (rank == 1) {
+            ptx::fence_proxy_async_smem();   // st.async (generic) writes -> visible to the tensor core
+            pair::arrive_remote_release(&dsx_ready[db], 0);
+          }
+        }
+      }
+    }
+  } else {
+    ptx::setmaxnreg_dec<48>();
+  }
+  __syncwarp();
+  ptx::tc_fence_before();
+  pair::cluster_sync();
+  if (warp == 0) {
+    ptx::tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::);
+  }
+}
+
+// dQ = cast(dq_acc) for the pair kernel's accumulator layout (see the header comment):
+// one thread per (padded workspace row, 8 columns).
+template <bool BF16>
+__global__ void __launch_bounds__(256) fa2_dq_convert_pair(const RowParams p) {
+  constexpr int D = 128;
+  const long long t = static_cast<long long>(blockIdx.x) * 256 + threadIdx.x;
+  if (t >= p.acc_rows * (D / 8)) return;
+  const long long R = t / (D / 8);
+  const int c = static_cast<int>(t % (D / 8)) * 8;
+  long long q_off = 0, l_off = 0;
+  if (!acc_row_ref(p, R, q_off, l_off)) return;
+  const int q = static_cast<int>(R % 128);
+  const float* src = p.dq_acc + (R / 128) * (128 * D) + ((q / 64) * 32 + c / 4) * 256 + (q % 64) * 4;
+  const float4 a = *reinterpret_cast<const float4*>(src);
+  const float4 b = *reinterpret_cast<const float4*>(src + 256);
+  uint4 out;
+  out.x = ptx::pack2<BF16>(a.x, a.y);
+  out.y = ptx::pack2<BF16>(a.z, a.w);
+  out.z = ptx::pack2<BF16>(b.x, b.y);
+  out.w = ptx::pack2<BF16>(b.z, b.w);
+  *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.dq) + q_off + c) = out;
+}
+
+}  // namespace fa2

@@ -332,6 +332,37 @@ __global__ void __launch_bounds__(256) fa2_dq_convert(const RowParams p, long lo
   reinterpret_cast<uint4*>(p.dq)[i8] = out;
 }
 
+// dQ = cast(dq_acc) for the d = 128 kernel's chunked accumulator (FA2_BWD_DQ_LSU): inside each
+// 128-row tile of the padded workspace, element (q, c) sits at float (q / 4) * 512 + c * 4 + q % 4
+// (the layout its register-direct red.global.add.v4 writes).  One thread per 4 workspace rows
+// x 8 columns: eight float4 loads of 128 contiguous bytes, four 16-byte stores.
+template <bool BF16>
+__global__ void __launch_bounds__(256) fa2_dq_convert_chunked(const RowParams p) {
+  constexpr int D = 128;
+  const long long t = static_cast<long long>(blockIdx.x) * 256 + threadIdx.x;
+  if (t >= (p.acc_rows / 4) * (D / 8)) return;
+  const long long R0 = (t / (D / 8)) * 4;
+  const int c = static_cast<int>(t % (D / 8)) * 8;
+  const float4* src = reinterpret_cast<const float4*>(p.dq_acc + (R0 / 128) * (128 * D) + ((R0 % 128) / 4) * (4 * D)) + c;
+  float4 f[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) f[k] = src[k];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    long long q_off = 0, l_off = 0;
+    if (!acc_row_ref(p, R0 + j, q_off, l_off)) continue;
+    float e[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) e[k] = j == 0 ? f[k].x : j == 1 ? f[k].y : j == 2 ? f[k].z : f[k].w;
+    uint4 out;
+    out.x = ptx::pack2<BF16>(e[0], e[1]);
+    out.y = ptx::pack2<BF16>(e[2], e[3]);
+    out.z = ptx::pack2<BF16>(e[4], e[5]);
+    out.w = ptx::pack2<BF16>(e[6], e[7]);
+    *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.dq) + q_off + c) = out;
+  }
+}
+
 // GQA split: dK, dV = cast(dk_acc, dv_acc), n8 groups of 8 elements each (same layouts)
 template <bool BF16>
 __global__ void __launch_bounds__(256)

@@ -28,6 +28,7 @@
 // and K, warp 10 TMA of V.
 #pragma once
 #include "fa2_fwd_sm100.cuh"
+#include "sm100_pair.cuh"
 
 namespace fa2 {
 
@@ -39,72 +40,6 @@ namespace fa2 {
 #endif
 constexpr int kFwdPairEmuPairs = FA2_FWD_PAIR_EMU;
 
-namespace pair {
-
-FA2_DEVICE uint32_t cta_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-FA2_DEVICE uint32_t cluster_id() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
-  return r;
-}
-FA2_DEVICE uint32_t num_clusters() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
-  return r;
-}
-FA2_DEVICE void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// arrive on the mbarrier at the same shared-memory offset in CTA `cta` of the cluster
-FA2_DEVICE void arrive_remote(uint64_t* bar, uint32_t cta) {
-  asm volatile(
-      "{\n\t.reg .b32 ra;\n\t"
-      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
-      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}"
-      :: "r"(ptx::smem_u32(bar)), "r"(cta) : "memory");
-}
-// wait on a local mbarrier whose arrivals come from the whole cluster
-FA2_DEVICE void wait_cluster(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = ptx::smem_u32(bar);
-  uint32_t ok = 0;
-  while (!ok) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok) : "r"(a), "r"(parity) : "memory");
-  }
-}
-// arrive (once) on `bar` in both CTAs of the pair when this thread's tcgen05 ops complete
-FA2_DEVICE void commit_both(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
-      :: "r"(ptx::smem_u32(bar)), "h"(static_cast<uint16_t>(0x3)) : "memory");
-}
-FA2_DEVICE void mma_ss2(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
-      :: "r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate) : "memory");
-}
-// TMA 3-D load into this CTA's SMEM whose completion bytes land on the leader's mbarrier
-// at the same offset (peer bit of the shared::cluster address cleared)
-FA2_DEVICE void tma_load_pair(void* smem_dst, const CUtensorMap* d, uint64_t* bar, int c0, int c1, int c2,
-                              uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3, %4}], [%5], %6;"
-      :: "r"(ptx::smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(d)), "r"(c0), "r"(c1), "r"(c2),
-         "r"(ptx::smem_u32(bar) & 0xFEFFFFFFu), "l"(policy)
-      : "memory");
-}
-
-}  // namespace pair
 
 struct FwdPairSmem {
   static constexpr int D = 128;

@@ -24,3 +24,6 @@ print("mma: p_ready->seen", avg(1, 4), " dV+dP issue", avg(4, 5), " S(x+1) issue
       " ->dst_ready seen", avg(6, 7), " dK+dQ issue", avg(7, 8), " dQ issued -> next p_ready seen", avg(8, 4, 1))
 print("dQ warps: dq_full seen->dq_empty", avg(9, 10), " dq_empty->rounds issued", avg(10, 16),
       " rounds issued->next dq_full seen", avg(16, 9, 1), " dQ issued(mma)->dq_full seen", avg(8, 9))
+print("P sub-phases: s_full->exps done", avg(0, 15), " exps->p_ready", avg(15, 1))
+print("dS sub-phases: dp_full->math done", avg(2, 11), " ->tmem st+sts issued", avg(11, 12), " ->wait st", avg(12, 13),
+      " ->fence.proxy", avg(13, 14), " ->arrive", avg(14, 3))
