@@ -1,10 +1,16 @@
 """Benchmark of the B200 FlashAttention-2 hot path (fwd + bwd step).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--sweep] [--extras]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config ps128|ps64|gpt|lc] [--sweep] [--extras]
 
-Under torchrun (N > 1) each rank runs the same per-GPU workload (weak scaling
-over batch x heads, no collective in the data path); the step time is the max
-over ranks.  Rank 0 prints ONE JSON line.
+Multi-GPU: `--gpus N` outside torchrun re-launches itself under
+torch.distributed.run with N ranks.  Rank 0 draws the seeded global inputs,
+NCCL-scatters contiguous (b,h) shards (the units are independent), every
+rank runs fwd+bwd on its shard with no collective in the step, and O, L, dQ, dK, dV
+are gathered back to rank 0 and checked bitwise against one unsharded run, all
+outside the timed region.  The step time is the max over ranks.  ps128 / ps64 scale
+weakly (each GPU keeps the paper's 16k tokens); gpt and lc split a fixed global
+batch (strong).  Rank 0 prints ONE JSON line.
 
 Workload (BASELINE.json configs[2], "paper fwd+bwd benchmark"): hidden 2048,
 d = 128 (H = 16), N = 8192, batch = 16k / N = 2, bf16, non-causal; synthetic
@@ -107,9 +113,43 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# distributed plumbing
+# distributed plumbing (the (b,h) units are independent, P:162-165,
+# P:457-464; NCCL only moves inputs and results, outside the timed region)
 # ---------------------------------------------------------------------------
-def dist_setup(gpus: int):
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_if_needed(gpus: int) -> None:
+    """`bench.py --gpus N` outside torchrun re-executes itself under
+    torch.distributed.run with N ranks (127.0.0.1 rendezvous) and exits with its
+    code; fails (exit 2) if fewer than N GPUs are visible or if an existing launch
+    disagrees with --gpus."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is not None:
+        if int(world) != gpus:
+            sys.stderr.write(f"bench.py: --gpus {gpus} but WORLD_SIZE={world}\n")
+            sys.exit(2)
+        return
+    if gpus <= 1:
+        return
+    import subprocess
+    import torch
+    n = torch.cuda.device_count()
+    if n < gpus:
+        sys.stderr.write(f"bench.py: --gpus {gpus} needs {gpus} CUDA devices, found {n}\n")
+        sys.exit(2)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
+def dist_setup():
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -149,6 +189,55 @@ def shard_units(n_units: int, rank: int, world: int):
     return start, start + base + (1 if rank < rem else 0)
 
 
+def scatter_units(x, n_units: int, tail, dtype, device, rank: int, world: int, src: int = 0):
+    """Rank `src` holds x = [n_units, *tail] (contiguous; the [B,H,...] layout with
+    b*h flattened); every rank returns its contiguous shard [u1 - u0, *tail] on
+    `device`.  Point-to-point sends from `src` (NCCL over NVLink, or gloo in the
+    CPU tests); empty shards are not sent."""
+    import torch
+    u0, u1 = shard_units(n_units, rank, world)
+    if world == 1:
+        return x[u0:u1]
+    import torch.distributed as dist
+    if rank == src:
+        reqs = []
+        for r in range(world):
+            a, b = shard_units(n_units, r, world)
+            if r != src and b > a:
+                reqs.append(dist.isend(x[a:b].contiguous(), dst=r))
+        for rq in reqs:
+            rq.wait()
+        return x[u0:u1].clone()
+    buf = torch.empty((u1 - u0, *tail), dtype=dtype, device=device)
+    if u1 > u0:
+        dist.recv(buf, src=src)
+    return buf
+
+
+def gather_units(x, n_units: int, rank: int, world: int, dst: int = 0):
+    """Inverse of scatter_units: rank `dst` returns the [n_units, *tail] tensor with
+    every rank's shard at its unit offsets; other ranks return None."""
+    import torch
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    tail = tuple(x.shape[1:])
+    if rank == dst:
+        out = torch.empty((n_units, *tail), dtype=x.dtype, device=x.device)
+        u0, u1 = shard_units(n_units, rank, world)
+        out[u0:u1].copy_(x)
+        for r in range(world):
+            a, b = shard_units(n_units, r, world)
+            if r != dst and b > a:
+                buf = torch.empty((b - a, *tail), dtype=x.dtype, device=x.device)
+                dist.recv(buf, src=r)
+                out[a:b].copy_(buf)
+        return out
+    if x.shape[0] > 0:
+        dist.send(x.contiguous(), dst=dst)
+    return None
+
+
 # ---------------------------------------------------------------------------
 # CPU oracle timing (cpu_baseline and --impl reference)
 # ---------------------------------------------------------------------------
@@ -160,12 +249,12 @@ def blas_threads():
         return None
 
 
-def oracle_head_step(N, d, causal, seed):
+def oracle_head_step(N, d, causal, seed, dtype="bf16"):
     """One bounded sample: fwd + bwd of ONE (b,h) head of the workload through
     the fp64 oracle, on the same dtype-rounded N(0,1) inputs.  Returns seconds."""
     import workloads as W
     from oracle import ref_attention as R
-    q, k, v, do = W.qkv(1, 1, N, d, "bf16", seed=seed)
+    q, k, v, do = W.qkv(1, 1, N, d, dtype, seed=seed)
     f = lambda t: t[0, 0].double().numpy()
     qq, kk, vv, dd = f(q), f(k), f(v), f(do)
     sc = 1.0 / math.sqrt(d)
@@ -175,18 +264,65 @@ def oracle_head_step(N, d, causal, seed):
     return time.perf_counter() - t0
 
 
+ORACLE_MAX_N = 8192   # the oracle materialises N x N fp64 matrices: 0.5 GiB each at 8k
+
+
 def cpu_baseline(cfg, budget_s=20.0):
-    N, d, causal = cfg["N"], cfg["d"], cfg["causal"]
+    N, d, causal = min(cfg["N"], ORACLE_MAX_N), cfg["d"], cfg["causal"]
     fl = flops(1, 1, N, d, causal, "fwd_bwd")
     times = []
     t_start = time.perf_counter()
     while not times or (time.perf_counter() - t_start < budget_s and len(times) < 5):
-        times.append(oracle_head_step(N, d, causal, seed=len(times)))
+        times.append(oracle_head_step(N, d, causal, seed=len(times), dtype=cfg["dtype"]))
     t = statistics.median(times)
     return {"value": fl / t / 1e12, "unit": "TFLOP/s", "cores": blas_threads() or os.cpu_count(),
             "kind": "oracle",
-            "sample": f"fp64 numpy oracle, fwd+bwd of one (b,h) head at N={N}, d={d}, causal={causal} "
-                      f"({len(times)} runs, median {t:.2f} s); the full step is {cfg['B'] * cfg['H']} such heads"}
+            "sample": f"fp64 numpy oracle, fwd+bwd of one (b,h) head at N={N}, d={d}, causal={causal}, "
+                      f"{cfg['dtype']}-rounded inputs ({len(times)} runs, median {t:.2f} s); the full step is "
+                      f"{cfg['B'] * cfg['H']} heads at N={cfg['N']}"
+                      + ("" if N == cfg["N"] else f" (sampled at N={N}: the oracle's N^2 memory bounds it)")}
+
+
+# ---------------------------------------------------------------------------
+# workloads (BASELINE.json configs; SURVEY §8 row names)
+# ---------------------------------------------------------------------------
+CONFIGS = {
+    # name: (BASELINE index, label, d, H, N, B (None: 16384 / N), causal, dtype, scaling)
+    "ps128": (2, "paper fwd+bwd benchmark: hidden 2048, d=128 (H=16), batch=16k/N", 128, 16, 8192, None, False,
+              "bf16", "weak"),
+    "ps64": (1, "paper fwd benchmark shape: hidden 2048, d=64 (H=32), batch=16k/N", 64, 32, 8192, None, False,
+             "bf16", "weak"),
+    "gpt": (3, "GPT-3 2.7B attention shape (H=20, d=128), 8k context, B=8", 128, 20, 8192, 8, True, "bf16",
+            "strong"),
+    "lc": (4, "long-context stress: B=1, H=16, d=128", 128, 16, 65536, 1, True, "fp16", "strong"),
+}
+
+
+def resolve_config(args):
+    idx, label, d, H, N, B, causal, dtype, scaling = CONFIGS[args.config]
+    N = args.seqlen or N
+    d = args.head_dim or d
+    H = args.heads or H
+    B = args.batch or B or max(1, 16384 // N)
+    causal = causal if args.causal is None else bool(args.causal)
+    dtype = args.dtype or dtype
+    if args.strong:
+        scaling = "strong"
+    if args.weak:
+        scaling = "weak"
+    return dict(name=args.config, index=idx, label=label, B=B, H=H, N=N, d=d, causal=causal, dtype=dtype,
+                scaling=scaling)
+
+
+def kernel_names(cfg):
+    """Which of the library's kernels the square fixed-length path launches (the
+    selection rules of fa2_api.cu): the CTA-pair forward serves non-causal d = 128;
+    the CTA-pair backward only when FA2_BWD_PAIR=1 is set (opt-in)."""
+    pair_fwd = not cfg["causal"] and cfg["d"] == 128
+    pair_bwd = os.environ.get("FA2_BWD_PAIR") == "1" and cfg["d"] == 128
+    return {"fwd": "fa2_fwd_pair_kernel" if pair_fwd else "fa2_fwd_kernel",
+            "bwd_main": "fa2_bwd_pair_kernel" if pair_bwd else ("fa2_bwd128_kernel" if cfg["d"] == 128 else
+                                                                 "fa2_bwd_kernel")}
 
 
 # ---------------------------------------------------------------------------
@@ -196,27 +332,40 @@ def run_ours(args, world, rank, local):
     import torch
     import paper_2307_08691_b200 as fa2
 
-    cfg = dict(B=args.batch, H=args.heads, N=args.seqlen, d=args.head_dim, causal=bool(args.causal))
-    B, H, N, d, causal = cfg["B"], cfg["H"], cfg["N"], cfg["d"], cfg["causal"]
-    if args.strong:
-        # strong scaling: the global B*H units are split across ranks (contiguous shards)
-        u0, u1 = shard_units(B * H, rank, world)
-        B, H = 1, u1 - u0
-        cfg.update(shard=[u0, u1])
+    cfg = resolve_config(args)
+    d, N, causal = cfg["d"], cfg["N"], cfg["causal"]
+    tdt = {"bf16": torch.bfloat16, "fp16": torch.float16}[cfg["dtype"]]
+    # the global job: weak scaling grows the batch with the world, strong splits a fixed one
+    B_glob = cfg["B"] * world if cfg["scaling"] == "weak" else cfg["B"]
+    H = cfg["H"]
+    n_units = B_glob * H
+    u0, u1 = shard_units(n_units, rank, world)
+    U = u1 - u0
     dev = torch.device("cuda", local if world > 1 else 0)
-    g = torch.Generator(device=dev)
-    g.manual_seed(1000 + rank)
-    mk = lambda: torch.randn(B, H, N, d, device=dev, dtype=torch.bfloat16, generator=g)
-    q, k, v, do = mk(), mk(), mk(), mk()
+
+    # rank 0 draws the seeded global inputs on its GPU and scatters contiguous (b,h) shards
+    glob = None
+    if rank == 0:
+        g = torch.Generator(device=dev)
+        g.manual_seed(1000 + cfg["index"])
+        glob = [torch.randn(n_units, N, d, device=dev, dtype=tdt, generator=g) for _ in range(4)]
+    torch.cuda.synchronize()
+    barrier(world)
+    q, k, v, do = (scatter_units(glob[i] if glob else None, n_units, (N, d), tdt, dev, rank, world)
+                   .view(1, U, N, d) for i in range(4))
+    torch.cuda.synchronize()
+    barrier(world)
     o = torch.empty_like(q)
-    lse = torch.empty(B, H, N, device=dev, dtype=torch.float32)
+    lse = torch.empty(1, U, N, device=dev, dtype=torch.float32)
     dq, dk, dv = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
-    ws = torch.empty(fa2.backward_workspace_size(B, H, N, d), dtype=torch.uint8, device=dev)
+    ws = torch.empty(fa2.backward_workspace_size(1, max(U, 1), N, d), dtype=torch.uint8, device=dev)
     sc = 1.0 / math.sqrt(d)
     stream = torch.cuda.current_stream()
     launches = [0]
 
     def step():
+        if U == 0:
+            return
         fa2.forward(q, k, v, causal=causal, softmax_scale=sc, out=o, lse=lse)
         launches[0] += fa2.lib().fa2_last_launch_count()
         fa2.backward(q, k, v, o, lse, do, causal=causal, softmax_scale=sc, dq=dq, dk=dk, dv=dv, workspace=ws)
@@ -249,82 +398,143 @@ def run_ours(args, world, rank, local):
     barrier(world)
     ms_local = start.elapsed_time(end) / args.steps
     ms = max_over_ranks(ms_local, world)
-    k_ms = {"fwd": [], "bwd_pre": [], "bwd_main": [], "bwd_dq": []}
-    for es in evs:
-        k_ms["fwd"].append(es[0].elapsed_time(es[1]))
-        k_ms["bwd_pre"].append(es[2].elapsed_time(es[3]))
-        k_ms["bwd_main"].append(es[3].elapsed_time(es[4]))
-        k_ms["bwd_dq"].append(es[4].elapsed_time(es[5]))
-    k_avg = {kk: statistics.mean(vv) for kk, vv in k_ms.items()}
+    k_avg = {"fwd": 0.0, "bwd_pre": 0.0, "bwd_main": 0.0, "bwd_dq": 0.0}
+    if U > 0:
+        k_ms = {"fwd": [], "bwd_pre": [], "bwd_main": [], "bwd_dq": []}
+        for es in evs:
+            k_ms["fwd"].append(es[0].elapsed_time(es[1]))
+            k_ms["bwd_pre"].append(es[2].elapsed_time(es[3]))
+            k_ms["bwd_main"].append(es[3].elapsed_time(es[4]))
+            k_ms["bwd_dq"].append(es[4].elapsed_time(es[5]))
+        k_avg = {kk: statistics.mean(vv) for kk, vv in k_ms.items()}
 
-    fl_step = flops(B, H, N, d, causal, "fwd_bwd")
-    fl_job = flops(cfg["B"], cfg["H"], N, d, causal, "fwd_bwd") * (1 if args.strong else world)
+    fl_unit = flops(1, 1, N, d, causal, "fwd_bwd")
+    fl_job = fl_unit * n_units
     value = fl_job / (ms * 1e-3) / 1e12
     peaks = measured_peaks()
-    fl_bwd = flops(B, H, N, d, causal, "bwd")
-    fl_fwd = flops(B, H, N, d, causal, "fwd")
+    fl_bwd = flops(1, U, N, d, causal, "bwd")
+    fl_fwd = flops(1, U, N, d, causal, "fwd")
+    names = kernel_names(cfg)
     dominant = "bwd_main" if k_avg["bwd_main"] >= k_avg["fwd"] else "fwd"
     dom_fl = fl_bwd if dominant == "bwd_main" else fl_fwd
-    achieved = dom_fl / (k_avg[dominant] * 1e-3) / 1e12
+    achieved = dom_fl / (max(k_avg[dominant], 1e-9) * 1e-3) / 1e12
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and args.config == "ps128" and world == 1:
         try:
-            traffic = json.load(open(tp)).get(dominant)
+            tj = json.load(open(tp))
+            traffic = tj.get(names[dominant], tj.get(dominant))
         except Exception:
             traffic = None
-    bwd_name = "fa2_bwd128_kernel" if d == 128 else "fa2_bwd_kernel"
-    roofline = {"bound": "tensor", "kernel": bwd_name if dominant == "bwd_main" else "fa2_fwd_kernel",
+    roofline = {"bound": "tensor", "kernel": names[dominant],
                 "achieved": round(achieved, 1), "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
                 "frac": round(achieved / peaks["bf16_tflops"], 4), "traffic": traffic,
                 "peak_source": peaks["source"] + ", burst bf16 GEMM (the timed region runs at max SM clock, "
-                               "see clocks)",
+                               "see clocks; fp16 has the same nominal tensor rate)",
                 "algorithmic_flops_per_launch": dom_fl,
+                "kernels": names,
                 "kernel_ms": {kk: round(vv, 4) for kk, vv in k_avg.items()},
                 "kernel_share_of_step": {kk: round(vv / ms_local, 4) for kk, vv in k_avg.items()}}
-    passes = {"fwd_tflops": round(fl_fwd / (k_avg["fwd"] * 1e-3) / 1e12, 1),
-              "bwd_tflops": round(fl_bwd / ((k_avg["bwd_pre"] + k_avg["bwd_main"] + k_avg["bwd_dq"]) * 1e-3) / 1e12, 1),
-              "fwd_bwd_tflops": round(fl_step / (ms_local * 1e-3) / 1e12, 1)}
+    passes = None
+    if U > 0:
+        passes = {"fwd_tflops": round(fl_fwd / (k_avg["fwd"] * 1e-3) / 1e12, 1),
+                  "bwd_tflops": round(fl_bwd / ((k_avg["bwd_pre"] + k_avg["bwd_main"] + k_avg["bwd_dq"]) * 1e-3)
+                                      / 1e12, 1),
+                  "fwd_bwd_tflops": round(flops(1, U, N, d, causal, "fwd_bwd") / (ms_local * 1e-3) / 1e12, 1)}
+
+    # ---- sharding check (outside the timed region): gathered results vs one unsharded run ----
+    shard_check = None if args.no_check else check_sharded(fa2, cfg, glob, q, k, v, do, o, lse, ws, B_glob, H,
+                                                           n_units, rank, world, dev, sc)
 
     # ---- e2e: the same step through the host-buffer C-ABI entry point ----
-    e2e = None if args.no_e2e else run_e2e(fa2, dict(cfg, B=B, H=H), dev, world, args, fl_job)
+    e2e = None if args.no_e2e or U == 0 else run_e2e(fa2, dict(cfg, B=1, H=U), dev, world, args, fl_job, tdt)
 
+    scatter_bytes = 4 * (n_units - U if rank == 0 else 0) * N * d * q.element_size()
     out = {"metric": METRIC, "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
-           "scaling": "strong" if args.strong else "weak",
-           "vs_baseline": None, "dtype": "bf16", "data": "synthetic N(0,1), seeded",
-           "config": {"workload": f"paper fwd+bwd benchmark (BASELINE configs[2]): hidden 2048, d={d}, H={cfg['H']}, "
-                                  f"N={N}, batch={cfg['B']}, bf16, {'causal' if causal else 'non-causal'}; fwd+bwd per step",
-                      "B": cfg["B"], "H": cfg["H"], "N": N, "d": d, "causal": causal, "per_gpu": not args.strong,
-                      "l2": "inputs larger than L2 (q,k,v,o,dO = %d MiB per step > 126 MB); no flush" %
-                            (5 * B * H * N * d * 2 // 2 ** 20),
-                      "parallelism": f"batch x heads, {world} independent replica(s), no collective"},
+           "scaling": cfg["scaling"],
+           "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic N(0,1), seeded (rank 0 draws, NCCL scatter)",
+           "config": {"workload": f"BASELINE configs[{cfg['index']}] {cfg['label']}; N={N}, "
+                                  f"{'causal' if causal else 'non-causal'}, {cfg['dtype']}; fwd+bwd per step",
+                      "name": cfg["name"], "B_global": B_glob, "B_per_gpu": B_glob if world == 1 else None,
+                      "H": H, "N": N, "d": d, "causal": causal, "units_global": n_units,
+                      "units_per_rank": [shard_units(n_units, r, world)[1] - shard_units(n_units, r, world)[0]
+                                         for r in range(world)],
+                      "l2": "inputs larger than L2 (q,k,v,o,dO = %d MiB per step on rank 0 > 126 MB); no flush" %
+                            (5 * U * N * d * q.element_size() // 2 ** 20),
+                      "parallelism": f"batch x heads over {world} GPU(s): contiguous (b,h) shards, no collective "
+                                     f"in the step; NCCL scatter of q,k,v,dO and gather of o,lse,dq,dk,dv outside "
+                                     f"the timed region"},
            "pct_of_nominal_peak": round(100 * value / world / NOMINAL_PEAK_TFLOPS, 2),
            "passes": passes,
            "clocks": sampler.summary(),
            "gpu_launches": launches[0],
            "roofline": roofline,
+           "shard_check": shard_check,
+           "exchange": {"scatter_bytes_from_rank0": scatter_bytes, "timed": False},
            "e2e": e2e}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, budget_s=args.cpu_budget)
+    if rank == 0 and not args.no_tables:
+        out["region"] = run_region(fa2, dev)
+        out["short_n"] = run_short_n(fa2, dev, peaks)
     if args.sweep and rank == 0:
         out["sweep"] = run_sweep(fa2, dev)
     if args.extras and rank == 0:
         out["extras"] = run_extras(fa2, dev)
+    barrier(world)
     return out
 
 
-def run_e2e(fa2, cfg, dev, world, args, job_flops):
+def check_sharded(fa2, cfg, glob, q, k, v, do, o, lse, ws, B_glob, H, n_units, rank, world, dev, sc):
+    """SURVEY §8e bitwise check: gather every rank's forward (O, L) and deterministic
+    backward (dQ, dK, dV) to rank 0 and compare them with ONE unsharded run of the
+    global [B, H, N, d] problem on rank 0.  The forward is deterministic and each
+    (b,h) unit is computed independently of the others; the deterministic
+    backward fixes the dQ summation order per tile (R21), which does not
+    depend on how many units share the launch."""
+    import torch
+    N, d, causal = cfg["N"], cfg["d"], cfg["causal"]
+    U = q.shape[1]
+    if U > 0:
+        fa2.forward(q, k, v, causal=causal, softmax_scale=sc, out=o, lse=lse)
+        dq, dk, dv = fa2.backward(q, k, v, o, lse, do, causal=causal, softmax_scale=sc, workspace=ws,
+                                  deterministic=True)
+    else:
+        dq = dk = dv = torch.empty_like(q)
+    torch.cuda.synchronize()
+    gathered = [gather_units(t.view(U, *t.shape[2:]), n_units, rank, world) for t in (o, lse, dq, dk, dv)]
+    res = None
+    if rank == 0:
+        shp = (B_glob, H, N, d)
+        qg, kg, vg, dog = (t.view(shp) for t in glob)
+        og, lg = fa2.forward(qg, kg, vg, causal=causal, softmax_scale=sc)
+        ref = [og, lg, *fa2.backward(qg, kg, vg, og, lg, dog, causal=causal, softmax_scale=sc, deterministic=True)]
+        torch.cuda.synchronize()
+        same = {n: bool(torch.equal(a.reshape(-1), b.reshape(-1)))
+                for n, a, b in zip(("o", "lse", "dq", "dk", "dv"), gathered, ref)}
+        res = {"against": "one unsharded run of the global problem on rank 0",
+               "fwd_bitwise": same["o"] and same["lse"], "bwd_deterministic_bitwise": same["dq"] and same["dk"]
+               and same["dv"], "per_tensor": same}
+        del ref, og, lg
+    barrier(world)
+    return res
+
+
+def run_e2e(fa2, cfg, dev, world, args, job_flops, tdt):
+    """The same job through the public host-buffer entry point: every rank runs its
+    shard from pinned host memory (H2D of q,k,v,dO and D2H of o,lse,dq,dk,dv inside
+    the timed region); wall clock, max over ranks."""
     import torch
     B, H, N, d, causal = cfg["B"], cfg["H"], cfg["N"], cfg["d"], cfg["causal"]
     g = torch.Generator()
     g.manual_seed(7)
-    host = [torch.randn(B, H, N, d, generator=g).bfloat16().pin_memory() for _ in range(4)]
-    outs = {"o": torch.empty(B, H, N, d, dtype=torch.bfloat16).pin_memory(),
+    host = [torch.randn(B, H, N, d, generator=g).to(tdt).pin_memory() for _ in range(4)]
+    outs = {"o": torch.empty(B, H, N, d, dtype=tdt).pin_memory(),
             "lse": torch.empty(B, H, N, dtype=torch.float32).pin_memory(),
-            "dq": torch.empty(B, H, N, d, dtype=torch.bfloat16).pin_memory(),
-            "dk": torch.empty(B, H, N, d, dtype=torch.bfloat16).pin_memory(),
-            "dv": torch.empty(B, H, N, d, dtype=torch.bfloat16).pin_memory()}
+            "dq": torch.empty(B, H, N, d, dtype=tdt).pin_memory(),
+            "dk": torch.empty(B, H, N, d, dtype=tdt).pin_memory(),
+            "dv": torch.empty(B, H, N, d, dtype=tdt).pin_memory()}
     arena = torch.empty(fa2.step_arena_size(B, H, N, d), dtype=torch.uint8, device=dev)
     steps = max(3, min(args.steps, 10))
     for _ in range(2):
@@ -335,11 +545,76 @@ def run_e2e(fa2, cfg, dev, world, args, job_flops):
         fa2.attention_step_host(*host, outs, arena, causal)   # synchronises the stream before returning
     dt = (time.perf_counter() - t0) / steps
     dt = max_over_ranks(dt, world)
-    t_bytes = B * H * N * d * 2
+    t_bytes = B * H * N * d * host[0].element_size()
     return {"value": round(job_flops / dt / 1e12, 2), "unit": "TFLOP/s",
             "ms_per_step": round(dt * 1e3, 3), "h2d_bytes_per_step": 4 * t_bytes,
             "d2h_bytes_per_step": 4 * t_bytes + B * H * N * 4,
             "api": "fa2_attention_step_host (pinned host buffers in/out, wall clock incl. copies)"}
+
+
+def _pass_times(fa2, dev, B, H, N, d, causal, reps=10):
+    import torch
+    mk = lambda: torch.randn(B, H, N, d, device=dev, dtype=torch.bfloat16)
+    q, k, v, do = mk(), mk(), mk(), mk()
+    o, lse = fa2.forward(q, k, v, causal=causal)
+    ws = torch.empty(fa2.backward_workspace_size(B, H, N, d), dtype=torch.uint8, device=dev)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
+    t_f = _tm(lambda: fa2.forward(q, k, v, causal=causal, out=o, lse=lse), reps)
+    t_b = _tm(lambda: fa2.backward(q, k, v, o, lse, do, causal=causal, dq=dq, dk=dk, dv=dv, workspace=ws), reps)
+    return t_f, t_b
+
+
+def run_region(fa2, dev):
+    """The north_star target region, timed in every default run: d = 128 (H = 16),
+    N in {4k, 8k, 16k}, B = 16k / N, bf16, causal and not (P:613-625).  Targets:
+    forward >= 60% and fwd+bwd >= 45% of the 2.25 PF dense bf16 peak.  Device
+    events around back-to-back launches on resident inputs (64 MiB per tensor, >
+    L2).  causal_speedup = non-causal time / causal time at the same shape (the
+    paper's block skipping claims 1.7-1.8x)."""
+    rows = []
+    for N in (4096, 8192, 16384):
+        B, H, d = 16384 // N, 16, 128
+        t = {}
+        for causal in (False, True):
+            t_f, t_b = _pass_times(fa2, dev, B, H, N, d, causal)
+            t[causal] = (t_f, t_b)
+            f = {p: flops(B, H, N, d, causal, p) for p in ("fwd", "bwd", "fwd_bwd")}
+            r = {"N": N, "B": B, "H": H, "d": d, "causal": causal,
+                 "fwd_tflops": round(f["fwd"] / t_f / 1e9, 1), "bwd_tflops": round(f["bwd"] / t_b / 1e9, 1),
+                 "fwd_bwd_tflops": round(f["fwd_bwd"] / (t_f + t_b) / 1e9, 1)}
+            r["fwd_pct"] = round(100 * r["fwd_tflops"] / NOMINAL_PEAK_TFLOPS, 1)
+            r["fwd_bwd_pct"] = round(100 * r["fwd_bwd_tflops"] / NOMINAL_PEAK_TFLOPS, 1)
+            r["meets_fwd_60"] = r["fwd_pct"] >= 60.0
+            r["meets_fwd_bwd_45"] = r["fwd_bwd_pct"] >= 45.0
+            rows.append(r)
+        (f0, b0), (f1, b1) = t[False], t[True]
+        rows[-1]["causal_speedup"] = {"fwd": round(f0 / f1, 3), "bwd": round(b0 / b1, 3),
+                                      "fwd_bwd": round((f0 + b0) / (f1 + b1), 3), "paper": "1.7-1.8x (P:382-383)"}
+    return rows
+
+
+def run_short_n(fa2, dev, peaks):
+    """Short sequences, where HBM rather than the tensor core bounds the pass (SURVEY
+    §8d roofline): achieved GB/s of the ALGORITHMIC bytes per head -- forward
+    8 N d + 4 N (read Q, K, V; write O, L), backward 16 N d + 4 N (read Q, K, V, O, dO,
+    L; write dQ, dK, dV), 2-byte elements -- against the measured HBM copy bandwidth."""
+    rows = []
+    for d, H in ((64, 32), (128, 16)):
+        for N in (512, 1024):
+            B = 16384 // N
+            for causal in (False, True):
+                t_f, t_b = _pass_times(fa2, dev, B, H, N, d, causal)
+                by_f = B * H * (8 * N * d + 4 * N)
+                by_b = B * H * (16 * N * d + 4 * N)
+                r = {"N": N, "B": B, "H": H, "d": d, "causal": causal,
+                     "fwd_us": round(t_f * 1e3, 1), "bwd_us": round(t_b * 1e3, 1),
+                     "fwd_tflops": round(flops(B, H, N, d, causal, "fwd") / t_f / 1e9, 1),
+                     "bwd_tflops": round(flops(B, H, N, d, causal, "bwd") / t_b / 1e9, 1),
+                     "fwd_hbm_gbs": round(by_f / t_f / 1e6, 1), "bwd_hbm_gbs": round(by_b / t_b / 1e6, 1)}
+                r["fwd_hbm_frac"] = round(r["fwd_hbm_gbs"] / peaks["hbm_gbs"], 3)
+                r["bwd_hbm_frac"] = round(r["bwd_hbm_gbs"] / peaks["hbm_gbs"], 3)
+                rows.append(r)
+    return rows
 
 
 def run_sweep(fa2, dev):
@@ -480,54 +755,70 @@ def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return None
-    N, d, causal = args.seqlen, args.head_dim, bool(args.causal)
+    cfg = resolve_config(args)
+    N, d, causal = min(cfg["N"], ORACLE_MAX_N), cfg["d"], cfg["causal"]
     for _ in range(args.warmup):
-        oracle_head_step(N, d, causal, seed=0)
-    ts = [oracle_head_step(N, d, causal, seed=i + 1) for i in range(args.steps)]
+        oracle_head_step(N, d, causal, seed=0, dtype=cfg["dtype"])
+    ts = [oracle_head_step(N, d, causal, seed=i + 1, dtype=cfg["dtype"]) for i in range(args.steps)]
     t = statistics.mean(ts)
     value = flops(1, 1, N, d, causal, "fwd_bwd") / t / 1e12
     cores = blas_threads() or os.cpu_count()
+    B_glob = cfg["B"] * world if cfg["scaling"] == "weak" else cfg["B"]
     sample = (f"fp64 numpy oracle (oracle/ref_attention.py), each step = fwd+bwd of one (b,h) head of the workload "
-              f"(N={N}, d={d}, causal={causal}); full step = {args.batch * args.heads} heads")
+              f"(N={N}, d={d}, causal={causal}, {cfg['dtype']}-rounded inputs); full step = {B_glob * cfg['H']} "
+              f"heads at N={cfg['N']}")
     return {"metric": METRIC, "value": round(value, 6), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(t * 1e3, 2), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic N(0,1), seeded", "impl": "reference",
-            "config": {"workload": f"paper fwd+bwd benchmark (BASELINE configs[2]): hidden 2048, d={d}, "
-                                   f"H={args.heads}, N={N}, batch={args.batch}, bf16-rounded inputs; "
-                                   f"one head per step (bounded sample)",
-                       "B": args.batch, "H": args.heads, "N": N, "d": d, "causal": causal},
+            "warmup": args.warmup, "ms_per_step": round(t * 1e3, 2), "higher_is_better": True,
+            "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic N(0,1), seeded",
+            "impl": "reference",
+            "config": {"workload": f"BASELINE configs[{cfg['index']}] {cfg['label']}; N={cfg['N']}, "
+                                   f"{'causal' if causal else 'non-causal'}, {cfg['dtype']}-rounded inputs; one head "
+                                   f"per step (bounded sample)",
+                       "name": cfg["name"], "B_global": B_glob, "H": cfg["H"], "N": cfg["N"], "d": d,
+                       "causal": causal},
             "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": round(value, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
-def main():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--seqlen", type=int, default=8192)
-    ap.add_argument("--batch", type=int, default=None)
-    ap.add_argument("--heads", type=int, default=16)
-    ap.add_argument("--head-dim", type=int, default=128)
-    ap.add_argument("--causal", type=int, default=0)
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="ps128",
+                    help="ps128 (default, BASELINE configs[2], weak scaling), ps64 (configs[1]), gpt (configs[3], "
+                         "strong scaling of 160 units), lc (configs[4], fp16 causal, strong scaling of 16 units)")
+    ap.add_argument("--seqlen", type=int, default=None)
+    ap.add_argument("--batch", type=int, default=None, help="per-GPU batch (weak) or global batch (strong)")
+    ap.add_argument("--heads", type=int, default=None)
+    ap.add_argument("--head-dim", type=int, default=None)
+    ap.add_argument("--causal", type=int, default=None)
+    ap.add_argument("--dtype", choices=["bf16", "fp16"], default=None)
+    ap.add_argument("--strong", action="store_true", help="split the global B*H over ranks")
+    ap.add_argument("--weak", action="store_true", help="give every rank the configured batch")
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--extras", action="store_true", help="also time GQA, deterministic bwd, N_q != N_k, varlen")
-    ap.add_argument("--strong", action="store_true", help="split the global B*H over ranks instead of replicating")
+    ap.add_argument("--no-tables", action="store_true", help="skip the target-region and short-N tables")
+    ap.add_argument("--no-check", action="store_true", help="skip the gathered-vs-unsharded bitwise check")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (ncu launch lists)")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
-    args = ap.parse_args()
-    if args.batch is None:
-        args.batch = max(1, 16384 // args.seqlen)
+    args = ap.parse_args(argv)
     args.warmup = max(3, args.warmup)
+    return args
+
+
+def main():
+    args = parse_args()
     if args.impl == "reference":
         out = run_reference(args)
         if out is not None:
             print(json.dumps(out), flush=True)
         return
-    world, rank, local = dist_setup(args.gpus)
+    relaunch_if_needed(args.gpus)
+    world, rank, local = dist_setup()
     out = run_ours(args, world, rank, local)
     if rank == 0:
         print(json.dumps(out), flush=True)

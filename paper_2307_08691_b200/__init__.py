@@ -119,10 +119,32 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
 
 
-def _need(t, like, name, heads=None):
-    shape = tuple(like.shape) if heads is None else (like.shape[0], heads) + tuple(like.shape[2:])
-    if tuple(t.shape) != shape or t.dtype != like.dtype or not t.is_contiguous() or t.device != like.device:
-        raise FA2Error(1, f"{name} must be a contiguous {shape} {like.dtype} tensor on {like.device}")
+def _need(t, shape, dtype, device, name):
+    """Every buffer handed to the library: a contiguous tensor of the expected shape,
+    dtype and device (the C layer checks only NULL and 16-byte alignment)."""
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise FA2Error(1, f"{name} must be a torch.Tensor")
+    shape = tuple(int(x) for x in shape)
+    if (tuple(t.shape) != shape or t.dtype != dtype or not t.is_contiguous() or t.device != device):
+        raise FA2Error(1, f"{name} must be a contiguous {shape} {dtype} tensor on {device} "
+                          f"(got {tuple(t.shape)} {t.dtype} on {t.device}, contiguous={t.is_contiguous()})")
+
+
+def _need_cuda(t, name):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise FA2Error(1, f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise FA2Error(1, f"{name} must be contiguous")
+
+
+def _need_workspace(ws, nbytes, device, name="workspace"):
+    import torch
+    if not isinstance(ws, torch.Tensor) or ws.device != device or not ws.is_contiguous():
+        raise FA2Error(1, f"{name} must be a contiguous tensor on {device}")
+    if ws.numel() * ws.element_size() < nbytes:
+        raise FA2Error(3, f"{name} holds {ws.numel() * ws.element_size()} bytes, needs {nbytes}")
 
 
 def _kv_heads(q, k):
@@ -132,13 +154,17 @@ def _kv_heads(q, k):
     return hkv
 
 
-def _kv_check(q, k, v):
-    """k, v: [B, H_kv, N_k, d] with H_kv | H; returns (H_kv, N_k)."""
-    Hkv = _kv_heads(q, k)
-    if k.dim() != 4 or k.shape[0] != q.shape[0] or k.shape[3] != q.shape[3]:
+def _kv_check(q, k, v, dtype=None):
+    """q: contiguous [B, H, N_q, d] CUDA tensor; k, v: [B, H_kv, N_k, d] with H_kv | H,
+    q's dtype (or `dtype`) and device.  Returns (H_kv, N_k)."""
+    import torch
+    _need_cuda(q, "q")
+    if not isinstance(k, torch.Tensor) or k.dim() != 4 or k.shape[0] != q.shape[0] or k.shape[3] != q.shape[3]:
         raise FA2Error(1, f"k must be [B, H_kv, N_k, d] matching q {tuple(q.shape)}")
-    _need(k, k, "k")
-    _need(v, k, "v")
+    Hkv = _kv_heads(q, k)
+    dt = q.dtype if dtype is None else dtype
+    _need(k, k.shape, dt, q.device, "k")
+    _need(v, k.shape, dt, q.device, "v")
     return Hkv, k.shape[2]
 
 
@@ -150,11 +176,12 @@ def forward(q, k, v, causal: bool = False, softmax_scale: float | None = None, o
     import torch
     B, H, N, d = _shape(q)
     Hkv, Nk = _kv_check(q, k, v)
-    if not q.is_contiguous():
-        raise FA2Error(1, "q must be contiguous")
+    _dtype_code(q)
     scale = 1.0 / math.sqrt(d) if softmax_scale is None else float(softmax_scale)
     o = torch.empty_like(q) if out is None else out
     L = torch.empty((B, H, N), dtype=torch.float32, device=q.device) if lse is None else lse
+    _need(o, q.shape, q.dtype, q.device, "out")
+    _need(L, (B, H, N), torch.float32, q.device, "lse")
     if Nk == N:
         _check(lib().fa2_forward_gqa(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(L), B, H, Hkv, N, d, int(bool(causal)),
                                      scale, _dtype_code(q), ctypes.c_void_p(_stream(stream))))
@@ -177,15 +204,21 @@ def backward(q, k, v, o, lse, do, causal: bool = False, softmax_scale: float | N
     import torch
     B, H, N, d = _shape(q)
     Hkv, Nk = _kv_check(q, k, v)
+    _dtype_code(q)
     for t, n in ((o, "o"), (do, "do")):
-        _need(t, q, n)
+        _need(t, q.shape, q.dtype, q.device, n)
+    _need(lse, (B, H, N), torch.float32, q.device, "lse")
     scale = 1.0 / math.sqrt(d) if softmax_scale is None else float(softmax_scale)
     dq = torch.empty_like(q) if dq is None else dq
     dk = torch.empty_like(k) if dk is None else dk
     dv = torch.empty_like(v) if dv is None else dv
+    _need(dq, q.shape, q.dtype, q.device, "dq")
+    _need(dk, k.shape, k.dtype, q.device, "dk")
+    _need(dv, k.shape, k.dtype, q.device, "dv")
     wsz = backward_workspace_size(B, H, N, d)
     if workspace is None:
         workspace = torch.empty(wsz, dtype=torch.uint8, device=q.device)
+    _need_workspace(workspace, wsz, q.device)
     args = (_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(workspace),
             workspace.numel() * workspace.element_size())
     st = ctypes.c_void_p(_stream(stream))
@@ -204,15 +237,16 @@ def forward_fp8(q, k, v, descale_q: float = 1.0, descale_k: float = 1.0, descale
     CUDA tensors representing descale_x * x.  Returns (o [B,H,N,128] bf16, lse [B,H,N] fp32)."""
     import torch
     B, H, N, d = _shape(q)
-    for t, n in ((q, "q"), (k, "k"), (v, "v")):
-        if t.dtype != torch.float8_e4m3fn:
-            raise FA2Error(1, f"{n} must be torch.float8_e4m3fn")
-    Hkv, Nk = _kv_check(q, k, v)
-    if Nk != N or not q.is_contiguous():
-        raise FA2Error(1, "FP8 forward: contiguous q, and k/v with N_k == N_q")
+    if q.dtype != torch.float8_e4m3fn:
+        raise FA2Error(1, "q must be torch.float8_e4m3fn")
+    Hkv, Nk = _kv_check(q, k, v, dtype=torch.float8_e4m3fn)
+    if Nk != N:
+        raise FA2Error(1, "FP8 forward: k/v with N_k == N_q")
     scale = 1.0 / math.sqrt(d) if softmax_scale is None else float(softmax_scale)
     o = torch.empty((B, H, N, d), dtype=torch.bfloat16, device=q.device) if out is None else out
     L = torch.empty((B, H, N), dtype=torch.float32, device=q.device) if lse is None else lse
+    _need(o, (B, H, N, d), torch.bfloat16, q.device, "out")
+    _need(L, (B, H, N), torch.float32, q.device, "lse")
     _check(lib().fa2_forward_fp8(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(L), B, H, Hkv, N, d, int(bool(causal)), scale,
                                  float(descale_q), float(descale_k), float(descale_v), ctypes.c_void_p(_stream(stream))))
     return o, L
@@ -225,9 +259,10 @@ def _varlen_check(q, k, v, cu_q, cu_k):
     Hkv = k.shape[1]
     if Hkv < 1 or q.shape[1] % Hkv:
         raise FA2Error(1, f"key/value heads ({Hkv}) must divide query heads ({q.shape[1]})")
-    _need(q, q, "q")
-    _need(k, k, "k")
-    _need(v, k, "v")
+    _need_cuda(q, "q")
+    _dtype_code(q)
+    _need(k, k.shape, q.dtype, q.device, "k")
+    _need(v, k.shape, q.dtype, q.device, "v")
     for c, n in ((cu_q, "cu_seqlens_q"), (cu_k, "cu_seqlens_k")):
         if c.dtype != torch.int32 or c.dim() != 1 or not c.is_contiguous() or c.device != q.device:
             raise FA2Error(1, f"{n} must be a contiguous int32 tensor on {q.device}")
@@ -247,6 +282,8 @@ def forward_varlen(q, k, v, cu_seqlens_q, cu_seqlens_k, max_seqlen_q: int, max_s
     scale = 1.0 / math.sqrt(d) if softmax_scale is None else float(softmax_scale)
     o = torch.empty_like(q) if out is None else out
     L = torch.empty((H, Tq), dtype=torch.float32, device=q.device) if lse is None else lse
+    _need(o, q.shape, q.dtype, q.device, "out")
+    _need(L, (H, Tq), torch.float32, q.device, "lse")
     _check(lib().fa2_forward_varlen(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(L), _ptr(cu_seqlens_q),
                                     _ptr(cu_seqlens_k), B, H, Hkv, Tq, k.shape[0], int(max_seqlen_q),
                                     int(max_seqlen_k), d, int(bool(causal)), scale, _dtype_code(q),
@@ -266,13 +303,19 @@ def backward_varlen(q, k, v, o, lse, do, cu_seqlens_q, cu_seqlens_k, max_seqlen_
     B, Hkv = _varlen_check(q, k, v, cu_seqlens_q, cu_seqlens_k)
     Tq, H, d = q.shape
     for t, n in ((o, "o"), (do, "do")):
-        _need(t, q, n)
+        _need(t, q.shape, q.dtype, q.device, n)
+    _need(lse, (H, Tq), torch.float32, q.device, "lse")
     scale = 1.0 / math.sqrt(d) if softmax_scale is None else float(softmax_scale)
     dq = torch.empty_like(q) if dq is None else dq
     dk = torch.empty_like(k) if dk is None else dk
     dv = torch.empty_like(v) if dv is None else dv
+    _need(dq, q.shape, q.dtype, q.device, "dq")
+    _need(dk, k.shape, k.dtype, q.device, "dk")
+    _need(dv, k.shape, k.dtype, q.device, "dv")
+    wsz = backward_varlen_workspace_size(B, H, Tq, d)
     if workspace is None:
-        workspace = torch.empty(backward_varlen_workspace_size(B, H, Tq, d), dtype=torch.uint8, device=q.device)
+        workspace = torch.empty(wsz, dtype=torch.uint8, device=q.device)
+    _need_workspace(workspace, wsz, q.device)
     _check(lib().fa2_backward_varlen(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk),
                                      _ptr(dv), _ptr(cu_seqlens_q), _ptr(cu_seqlens_k), _ptr(workspace),
                                      workspace.numel() * workspace.element_size(), B, H, Hkv, Tq, k.shape[0],
@@ -285,7 +328,9 @@ def backward_preprocess(o, do, stream=None):
     """D = rowsum(dO o O), [B,H,N] fp32."""
     import torch
     B, H, N, d = _shape(o)
-    _need(do, o, "do")
+    _need_cuda(o, "o")
+    _dtype_code(o)
+    _need(do, o.shape, o.dtype, o.device, "do")
     out = torch.empty((B, H, N), dtype=torch.float32, device=o.device)
     _check(lib().fa2_backward_preprocess(_ptr(o), _ptr(do), _ptr(out), B, H, N, d, _dtype_code(o),
                                          ctypes.c_void_p(_stream(stream))))
@@ -300,7 +345,21 @@ def attention_step_host(q_h, k_h, v_h, do_h, outs, arena, causal: bool, softmax_
                         stream=None):
     """One end-to-end fwd+bwd step through HOST (pinned) tensors.  `outs` is a
     dict with optional host tensors o, lse, dq, dk, dv to receive results."""
+    import torch
     B, H, N, d = _shape(q_h)
+    _dtype_code(q_h)
+    cpu = torch.device("cpu")
+    for t, n in ((q_h, "q"), (k_h, "k"), (v_h, "v"), (do_h, "do")):
+        _need(t, q_h.shape, q_h.dtype, cpu, n + " (host)")
+    for n, t in outs.items():
+        if n not in ("o", "lse", "dq", "dk", "dv"):
+            raise FA2Error(1, f"unknown output {n!r}")
+        if t is not None:
+            _need(t, (B, H, N) if n == "lse" else q_h.shape, torch.float32 if n == "lse" else q_h.dtype, cpu,
+                  n + " (host)")
+    if not isinstance(arena, torch.Tensor) or not arena.is_cuda:
+        raise FA2Error(1, "arena must be a CUDA tensor")
+    _need_workspace(arena, step_arena_size(B, H, N, d), arena.device, "arena")
     scale = 1.0 / math.sqrt(d) if softmax_scale is None else float(softmax_scale)
     g = outs.get
     _check(lib().fa2_attention_step_host(_ptr(q_h), _ptr(k_h), _ptr(v_h), _ptr(do_h), _ptr(g("o")),

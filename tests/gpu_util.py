@@ -31,12 +31,21 @@ def max_abs(a, b) -> float:
     return float(np.max(np.abs(a - b)))
 
 
-def grad_ok(g_gpu: torch.Tensor, g_ref: np.ndarray, dtype: str, floor: float = 0.0):
-    """Per-tensor rule (R15): max-abs error <= c * max(max|g_ref|, floor).
-    `floor` (2^-8 of the largest of the three gradients) only binds where the
-    exact gradient is ~0 (e.g. dQ = 0 at N = 1)."""
+def grad_ok(g_gpu: torch.Tensor, g_ref: np.ndarray, dtype: str, floor: float = 0.0, degenerate: bool = False):
+    """Per-tensor rule (R15): max-abs error <= c * max|g_ref|.
+
+    `floor` (2^-8 of the largest of the three gradients, `grad_floor`) replaces
+    max|g_ref| only where the exact gradient vanishes (e.g. dQ = dK = 0 at N = 1,
+    dQ = 0 for identical keys): the caller must declare such a case with
+    `degenerate=True`, and a non-degenerate reference below the floor fails."""
     err = max_abs(g_gpu, g_ref)
-    lim = TOL[dtype]["grad"] * max(float(np.max(np.abs(g_ref))), floor)
+    ref_max = float(np.max(np.abs(g_ref))) if g_ref.size else 0.0
+    if ref_max >= floor:
+        lim = TOL[dtype]["grad"] * ref_max
+    elif degenerate:
+        lim = TOL[dtype]["grad"] * floor
+    else:
+        return False, err, f"reference max {ref_max} below the floor {floor} in a case not declared degenerate"
     return err <= lim, err, lim
 
 
