@@ -25,8 +25,14 @@
  *   of fa2_backward and must not be modified in between.
  * Streams: `stream` is a cudaStream_t (0 = legacy default stream).  Calls are
  *   asynchronous with respect to the host; no host synchronisation happens
- *   inside the device-pointer entry points.  The library keeps no global mutable
- *   state besides a per-thread error-detail string, so calls are reentrant.
+ *   inside the device-pointer entry points.  Host-side state: a per-thread
+ *   error-detail string, launch count and timing/trace hooks; per-device caches
+ *   (co-resident cluster counts) and a shape-keyed cache of the balanced causal
+ *   schedules, both mutex-guarded and immutable once published (schedules are
+ *   shared_ptr-owned, so eviction never frees one in use); the copy/compute
+ *   streams of fa2_attention_step_host are per thread and per device.  No device
+ *   memory is allocated and no device-side state persists between calls, so
+ *   calls are reentrant and may run concurrently on different streams.
  * Errors: argument errors are detected before anything is launched and are
  *   returned synchronously (nothing is launched).  Launch failures return
  *   FA2_ERR_CUDA; fa2_last_error_detail() describes the last failure of the

@@ -139,12 +139,13 @@ def _need_cuda(t, name):
         raise FA2Error(1, f"{name} must be contiguous")
 
 
-def _need_workspace(ws, nbytes, device, name="workspace"):
+def _need_workspace(ws, device, name="workspace"):
+    """Scratch buffers: contiguous, on the device.  Their size is checked by the C
+    layer, which knows the minimum (e.g. the backward workspace without the GQA
+    split's extra accumulators) and returns FA2_ERR_WORKSPACE when it is short."""
     import torch
     if not isinstance(ws, torch.Tensor) or ws.device != device or not ws.is_contiguous():
         raise FA2Error(1, f"{name} must be a contiguous tensor on {device}")
-    if ws.numel() * ws.element_size() < nbytes:
-        raise FA2Error(3, f"{name} holds {ws.numel() * ws.element_size()} bytes, needs {nbytes}")
 
 
 def _kv_heads(q, k):
@@ -218,7 +219,7 @@ def backward(q, k, v, o, lse, do, causal: bool = False, softmax_scale: float | N
     wsz = backward_workspace_size(B, H, N, d)
     if workspace is None:
         workspace = torch.empty(wsz, dtype=torch.uint8, device=q.device)
-    _need_workspace(workspace, wsz, q.device)
+    _need_workspace(workspace, q.device)
     args = (_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(workspace),
             workspace.numel() * workspace.element_size())
     st = ctypes.c_void_p(_stream(stream))
@@ -315,7 +316,7 @@ def backward_varlen(q, k, v, o, lse, do, cu_seqlens_q, cu_seqlens_k, max_seqlen_
     wsz = backward_varlen_workspace_size(B, H, Tq, d)
     if workspace is None:
         workspace = torch.empty(wsz, dtype=torch.uint8, device=q.device)
-    _need_workspace(workspace, wsz, q.device)
+    _need_workspace(workspace, q.device)
     _check(lib().fa2_backward_varlen(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do), _ptr(dq), _ptr(dk),
                                      _ptr(dv), _ptr(cu_seqlens_q), _ptr(cu_seqlens_k), _ptr(workspace),
                                      workspace.numel() * workspace.element_size(), B, H, Hkv, Tq, k.shape[0],
@@ -359,7 +360,7 @@ def attention_step_host(q_h, k_h, v_h, do_h, outs, arena, causal: bool, softmax_
                   n + " (host)")
     if not isinstance(arena, torch.Tensor) or not arena.is_cuda:
         raise FA2Error(1, "arena must be a CUDA tensor")
-    _need_workspace(arena, step_arena_size(B, H, N, d), arena.device, "arena")
+    _need_workspace(arena, arena.device, "arena")
     scale = 1.0 / math.sqrt(d) if softmax_scale is None else float(softmax_scale)
     g = outs.get
     _check(lib().fa2_attention_step_host(_ptr(q_h), _ptr(k_h), _ptr(v_h), _ptr(do_h), _ptr(g("o")),

@@ -450,14 +450,18 @@ fa2_status_t forward_fp8_impl(const void* q, const void* k, const void* v, void*
                 : launch_fwd<128, true, false, false, true>(mq, mk, mv, p, sms, st);
 }
 
-// Copy streams and events of fa2_attention_step_host, created once per host thread.
+// Copy streams and events of fa2_attention_step_host, created once per host thread and
+// device (streams and events belong to the device that was current when they were made).
 struct StepStreams {
   static constexpr int kChunks = 16;
   cudaStream_t in = nullptr, out = nullptr;
   cudaEvent_t start = nullptr, in_done[kChunks] = {}, comp_done[kChunks] = {};
 };
 StepStreams& step_streams() {
-  thread_local StepStreams ss;
+  thread_local std::map<int, StepStreams> per_dev;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  StepStreams& ss = per_dev[dev];
   if (ss.in == nullptr) {
     StepStreams t;
     bool ok = cudaStreamCreateWithFlags(&t.in, cudaStreamNonBlocking) == cudaSuccess &&

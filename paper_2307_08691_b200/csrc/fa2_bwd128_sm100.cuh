@@ -31,7 +31,7 @@
 // dQ^T reduce-added straight from registers (red.global.add.v4.f32) into a chunked dQ_acc
 // layout ([q/4][d][4] per 128-row tile) instead of SMEM staging + TMA bulk reduce-adds
 #ifndef FA2_BWD_DQ_LSU
-#define FA2_BWD_DQ_LSU 1
+#define FA2_BWD_DQ_LSU 0
 #endif
 #ifndef FA2_BWD_RED_PACE
 #define FA2_BWD_RED_PACE 0

@@ -18,10 +18,11 @@
 //     applied to dK and dQ (dS carries it, R1).
 //   fa2_dq_convert     : dQ = cast(dQ_acc).
 //
-// Orientation: key rows are TMEM lanes (M = 128).  For d = 128 the query block
-// is B_r = 64 and dQ is produced transposed (dQ^T = K^T dS^T, M = d = 128); for
-// d = 64, B_r = 128 and dQ = dS K (M = B_r = 128).  Both keep every MMA at
-// M = 128 and the TMEM budget at 448 of 512 columns.
+// Orientation: key rows are TMEM lanes (M = 128), query blocks of B_r = 128 rows.
+// This file holds the d = 64 kernel (dQ = dS K, M = B_r = 128, TMEM S^T | dP^T | dV
+// | dK | dQ | P^T); d = 128 runs fa2_bwd128_kernel (fa2_bwd128_sm100.cuh, dQ^T =
+// K^T dS^T over the dP^T columns) or, opt-in, the CTA-pair fa2_bwd_pair_kernel
+// (fa2_bwd2_sm100.cuh).
 //
 // Warp roles (512 threads): warps 0-7 two compute warpgroups (each owns half of
 // the query columns of P^T / dS^T); warps 8-11 dQ readout + reduce-add; warp 12
