@@ -316,10 +316,10 @@ def resolve_config(args):
 
 def kernel_names(cfg):
     """Which of the library's kernels the square fixed-length path launches (the
-    selection rules of fa2_api.cu): the CTA-pair forward serves non-causal d = 128;
-    the CTA-pair backward only when FA2_BWD_PAIR=1 is set (opt-in)."""
+    selection rules of fa2_api.cu): the CTA-pair forward serves non-causal d = 128, the
+    CTA-pair backward every d = 128 call (unless FA2_BWD_PAIR=0 is set)."""
     pair_fwd = not cfg["causal"] and cfg["d"] == 128
-    pair_bwd = os.environ.get("FA2_BWD_PAIR") == "1" and cfg["d"] == 128
+    pair_bwd = os.environ.get("FA2_BWD_PAIR") != "0" and cfg["d"] == 128
     return {"fwd": "fa2_fwd_pair_kernel" if pair_fwd else "fa2_fwd_kernel",
             "bwd_main": "fa2_bwd_pair_kernel" if pair_bwd else ("fa2_bwd128_kernel" if cfg["d"] == 128 else
                                                                  "fa2_bwd_kernel")}

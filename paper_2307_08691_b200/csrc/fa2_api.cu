@@ -739,9 +739,10 @@ fa2_status_t backward_impl(const void* q, const void* k, const void* v, const vo
   p.acc_rows = wl.rows;
   p.tile_off = rp.tile_off;
   const bool bf16 = dtype == FA2_BF16;
-  // the CTA-pair kernel is opt-in (FA2_BWD_PAIR=1 in the environment): measured slower than the
-  // one-SM kernel on B200, kept as a tested alternative
-  static const bool pair_env = [] { const char* e = std::getenv("FA2_BWD_PAIR"); return e && e[0] == '1'; }();
+  // the CTA-pair kernel serves the square fixed-length arrival-order d = 128
+  // path; FA2_BWD_PAIR=0 in the environment selects the one-SM kernel instead (A/B runs and
+  // the one-SM kernel's parity test)
+  static const bool pair_env = [] { const char* e = std::getenv("FA2_BWD_PAIR"); return !(e && e[0] == '0'); }();
   const bool pair = FA2_BWD_PAIR && pair_env && g.d == 128 && !g.packed && g.Nq == g.Nk && !deterministic && hsplit == 1;
   if (pair) {
     CUtensorMap mq64, mdo64;

@@ -2,16 +2,13 @@
 // tcgen05 cta_group::2): the d = 128, square fixed-length, arrival-order path.
 //
 // Why a pair.  On one SM (fa2_bwd128_sm100.cuh) every 128 x 128 tile
-// sends 64 KB of fp32 dQ partials to L2, and the chip's L2 reduction rate (~6 TB/s,
-// ~20 B/clk/SM) then needs >= ~3100 cycles per tile against a 2560-cycle MMA floor; the
-// staging of those partials also costs 128 KB of the SM's 128 B/clk shared-memory
-// bandwidth per tile.  Here a work tile is a 256-row key block split over the pair
-// (CTA r owns key rows [256 nb2 + 128 r, +128)), and dQ_i = dS_i K_j contracts over all
-// 256 keys in ONE M = 128 cta_group::2 MMA whose output rows are split between the CTAs
-// (CTA r: query rows [64 r, 64 r + 64) of the tile, all of d).  Each CTA then reduce-adds
-// 32 KB per tile instead of 64 KB; the price is 16 KB of dS exchanged through DSMEM.
-// The B operands of S^T, dP^T, dV and dK are split between the CTAs too (each SM reads
-// half of them), so the SMEM -> tensor-core traffic per tile drops by a quarter.
+// sends 64 KB of fp32 dQ partials to L2, and the chip's L2 fp32 reduction rate (~5.9 TB/s,
+// ~20 B/clk/SM; tools/micro/tmaio.cu) then needs >= ~3300 cycles per tile against a
+// 2560-cycle MMA floor.  Here a work tile is a 256-row key block split over the pair (CTA r
+// owns key rows [256 nb2 + 128 r, +128)), and dQ_i = dS_i K_j contracts over all 256 keys
+// in ONE M = 128 cta_group::2 MMA whose output rows are split between the CTAs (CTA r:
+// query rows [64 r, 64 r + 64) of the tile, all of d).  Each CTA then reduce-adds 32 KB per
+// tile instead of 64 KB; the price is 16 KB of dS sent to the peer CTA per tile.
 //
 // Per query tile i (128 rows) and query head (all heads of the GQA group),
 // every MMA issued by the leader CTA (rank 0):
@@ -24,37 +21,48 @@
 // dQ lands in each CTA's TMEM as 64 rows x 128 d folded onto 128 lanes x 64 columns
 // (lanes 0-63: d [0,64), lanes 64-127: d [64,128), lane % 64 = query row).
 //
-// TMEM (512 columns per CTA): S^T [0,128) | dP^T [128,256) | dV [256,384) | dK [384,512);
-// P^T / dS^T overwrite S^T / dP^T in place (packed pairs), dQ overwrites dP^T [128,192)
-// after dK has read dS^T.  MMA issue order per query tile as in the one-SM kernel:
-//   dV(i), dP^T(i) [dQ(i-1) read out], S^T(i+1), dK(i) + dQ(i) [dS(i) ready].
+// TMEM (512 columns per CTA): S^T [0,128) | dP^T [128,256) | dV [256,384) | dK [384,512).
+// P^T overwrites S^T [0,64) (packed pairs), dS^T overwrites dP^T [128,192), dQ lands in
+// [192,256) (dP^T columns the dS phase has consumed).
+//
+// The dS exchange and the dQ reduce-add run on the TMA engine, not the LSU (st.async /
+// red.global through the LSU stall the compute warps' own shared-memory traffic behind
+// them): the warpgroup holding the peer's query half stages its 16 KB in shared memory and
+// one thread bulk-copies it into the peer's A slot (completion bytes on the peer's
+// dsx_full); the dQ warps stage 8 KB rounds and bulk reduce-add them.  The dS buffer is
+// single: dQ(x) is issued right after dK(x), before anything of step x + 1 needs it.
+// MMA issue order (steady state, step x):
+//   dK(x) [dS^T(x) in TMEM], dQ(x) [dS(x) in both CTAs' A slots], dV(x+1) [P^T(x+1)],
+//   dP^T(x+1) [dQ(x) read out of TMEM], S^T(x+2)
+// so the compute warps derive P^T(x+1) while dK(x) / dQ(x) run, and dS^T(x+1) is the only
+// phase the chain waits for.
 //
 // Shared memory per CTA (1024-B aligned boxes of 128-B swizzled rows):
 //   K   32 KB  own key rows, d halves 0 | 1               (A of S^T, K-major)
 //   V   32 KB  own key rows                               (A of dP^T)
 //   Kd  32 KB  K rows of CTA 0 | CTA 1, own d half        (B of dQ, MN-major)
-//   QS  2 x 16 KB  own 64 query rows, d halves 0 | 1     (B of S^T; 2-stage ring)
+//   QS  16 KB  own 64 query rows, d halves 0 | 1          (B of S^T)
 //   QK  16 KB  128 query rows, own d half                 (B of dK, MN-major)
 //   DOP 16 KB  own 64 dO rows, d halves 0 | 1             (B of dP^T)
 //   DOV 16 KB  128 dO rows, own d half                    (B of dV)
-//   DS  32 KB  dS of the own query half: keys of CTA 0 | CTA 1 (A of dQ, MN-major);
-//              the compute warpgroup of query half h writes its rows into CTA h
-//   DQ  8 KB   2 x 4 KB fp32 staging of the dQ reduce-add
+//   DS  32 KB  dS of the own query half: keys of CTA 0 | CTA 1 (A of dQ, MN-major)
+//   XS  16 KB  staging of the dS rows the peer needs (bulk-copied into its DS slot)
+//   DQ  16 KB  2 x 8 KB fp32 staging of the dQ reduce-add (one per d half)
 //   VEC 2 KB   L_i * log2(e), D_i (2 stages)
 //
 // dQ_acc layout (workspace, fp32): inside every 128-row tile of the padded rows, element
-// (q, c) at float ((q / 64) * 32 + c / 4) * 256 + (q % 64) * 4 + c % 4, so each red.v4 of a
-// dQ warp (32 consecutive rows, 4 columns) covers 512 contiguous bytes; fa2_dq_convert_pair
-// casts it back.
+// (q, c) at float ((q / 64) * 32 + c / 4) * 256 + (q % 64) * 4 + c % 4: each CTA's 64 rows
+// are one contiguous 32 KB range, a d half of them 16 KB, and the staging rounds copy
+// verbatim; fa2_dq_convert_pair casts it back.
 //
 // Barriers the leader's MMA warp waits on live in the leader: TMA loads of both CTAs
 // complete on them (cta_group::2 TMA), warps of both CTAs arrive on them remotely.
-// Barriers released by MMAs (s_full, dp_full, dq_full, dkv_full, *_empty) are signalled
-// in both CTAs by multicast tcgen05.commit.  L_i / D_i are per-CTA (local barriers).
+// Barriers released by MMAs (s_full, dp_full, dq_full, dkv_full, ds_free, *_empty) are
+// signalled in both CTAs by multicast tcgen05.commit.  L_i / D_i are per-CTA (local).
 //
 // Warp roles (512 threads per CTA): warps 0-7 compute (P^T, dS^T; warpgroup w owns query
 // columns [64 w, 64 w + 64)), warps 8-11 dQ read-out + reduce-add, warp 12 MMA issuer
-// (leader only), warp 13 TMA producer, warps 14-15 idle.
+// (leader only), warp 13 TMA producer, warp 14 dS-exchange bookkeeping, warp 15 idle.
 #pragma once
 #include "fa2_bwd_sm100.cuh"
 #include "sm100_pair.cuh"
@@ -63,28 +71,24 @@
 #ifndef FA2_BWD_PAIR_EMU
 #define FA2_BWD_PAIR_EMU 4
 #endif
-// stages of the own-query-rows Q ring (B operand of S^T)
-#ifndef FA2_BWD_PAIR_QSTAGES
-#define FA2_BWD_PAIR_QSTAGES 1
-#endif
 
 namespace fa2 {
 
 struct BwdPairSmem {
   static constexpr int BOX128 = 128 * 128;      // 128 rows x 128 B
   static constexpr int BOX64 = 64 * 128;        // 64 rows x 128 B
-  static constexpr int QSTAGES = FA2_BWD_PAIR_QSTAGES;
+  static constexpr int DQ_BUF = 8192;           // one dQ reduce round: 8 KB fp32
   static constexpr int OFF_K = 0;
   static constexpr int OFF_V = OFF_K + 2 * BOX128;
   static constexpr int OFF_KD = OFF_V + 2 * BOX128;
   static constexpr int OFF_QS = OFF_KD + 2 * BOX128;
-  static constexpr int QS_STAGE = 2 * BOX64;
-  static constexpr int OFF_QK = OFF_QS + QSTAGES * QS_STAGE;
+  static constexpr int OFF_QK = OFF_QS + 2 * BOX64;
   static constexpr int OFF_DOP = OFF_QK + BOX128;
   static constexpr int OFF_DOV = OFF_DOP + 2 * BOX64;
-  static constexpr int OFF_DS = OFF_DOV + BOX128;      // [2 buffers] A0 | A1 (dQ's A operand)
-  static constexpr int DS_BUF = 2 * BOX128;
-  static constexpr int OFF_VEC = OFF_DS + 2 * DS_BUF;  // [2][2][128] floats: L2, D
+  static constexpr int OFF_DS = OFF_DOV + BOX128;      // A0 | A1 (dQ's A operand)
+  static constexpr int OFF_XS = OFF_DS + 2 * BOX128;   // outgoing dS rows (staging)
+  static constexpr int OFF_DQ = OFF_XS + BOX128;       // [2] dQ staging, one per d half
+  static constexpr int OFF_VEC = OFF_DQ + 2 * DQ_BUF;  // [2][2][128] floats: L2, D
   static constexpr int OFF_BAR = OFF_VEC + 2 * 2 * 128 * 4;
   static constexpr int NBAR = 32;
   static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
@@ -119,7 +123,6 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
                     const BwdParams p, const __grid_constant__ SchedT<CAUSAL> sched) {
   using L = BwdPairSmem;
   constexpr int D = 128, BM = 128;
-  constexpr uint32_t QST = L::QSTAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if (ptx::smem_u32(smem) & 1023u) __trap();   // SW128 tiles and descriptors need 1024-B alignment
@@ -131,34 +134,39 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
   uint8_t* sDOP = smem + L::OFF_DOP;
   uint8_t* sDOV = smem + L::OFF_DOV;
   uint8_t* sDS = smem + L::OFF_DS;
+  uint8_t* sXS = smem + L::OFF_XS;
+  uint8_t* sDQ = smem + L::OFF_DQ;
   float* sVec = reinterpret_cast<float*>(smem + L::OFF_VEC);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   // leader-side (the MMA warp waits; arrivals / tx from both CTAs)
   uint64_t* kv_full = bars + 0;
-  uint64_t* q_full = bars + 1;      // [2]
-  uint64_t* qk_full = bars + 3;
-  uint64_t* dop_full = bars + 4;
-  uint64_t* dov_full = bars + 5;
-  uint64_t* p_ready = bars + 6;     // 16 arrivals: 8 compute warps x 2 CTAs
-  uint64_t* ds_ready = bars + 7;    // 16
-  uint64_t* dq_empty = bars + 8;    // 8: 4 dQ warps x 2 CTAs
-  uint64_t* dkv_empty = bars + 9;   // 16
+  uint64_t* q_full = bars + 1;
+  uint64_t* qk_full = bars + 2;
+  uint64_t* dop_full = bars + 3;
+  uint64_t* dov_full = bars + 4;
+  uint64_t* p_ready = bars + 5;     // 16 arrivals: 8 compute warps x 2 CTAs
+  uint64_t* ds_ready = bars + 6;    // 16
+  uint64_t* dq_empty = bars + 7;    // 8: 4 dQ warps x 2 CTAs
+  uint64_t* dkv_empty = bars + 8;   // 16
+  uint64_t* dsx_ready = bars + 9;   // CTA 1's dsx_full completed (relayed by its warp 14)
   // released by the MMAs (multicast commit: both CTAs)
   uint64_t* kv_empty = bars + 10;
-  uint64_t* q_empty = bars + 11;    // [2]
-  uint64_t* qk_empty = bars + 13;
-  uint64_t* dop_empty = bars + 14;
-  uint64_t* dov_empty = bars + 15;
-  uint64_t* s_full = bars + 16;
-  uint64_t* dp_full = bars + 17;
-  uint64_t* dq_full = bars + 18;
-  uint64_t* dkv_full = bars + 19;
+  uint64_t* q_empty = bars + 11;
+  uint64_t* qk_empty = bars + 12;
+  uint64_t* dop_empty = bars + 13;
+  uint64_t* dov_empty = bars + 14;
+  uint64_t* s_full = bars + 15;
+  uint64_t* dp_full = bars + 16;
+  uint64_t* dq_full = bars + 17;
+  uint64_t* dkv_full = bars + 18;
+  uint64_t* ds_free = bars + 19;    // dQ(x) complete: both CTAs' A slots may be rewritten
   // local
   uint64_t* vec_full = bars + 20;   // [2]
   uint64_t* vec_empty = bars + 22;  // [2]
-  uint64_t* dsx_full = bars + 24;   // [2] local: the peer's dS half of buffer b has landed here (tx bytes)
-  uint64_t* dsx_ready = bars + 26;  // [2] leader: CTA 1's dsx_full[b] completed (relayed by its warp 14)
-  uint64_t* dq_done = bars + 28;    // [2] dQ of the last step that used dS buffer b has completed
+  uint64_t* dsx_full = bars + 24;   // the peer's dS rows have landed in this CTA's A slot (tx bytes)
+  uint64_t* xs_full = bars + 25;    // 4: the staging warpgroup's rows are in XS
+  uint64_t* xs_empty = bars + 26;   // 1: the bulk copy has read XS
+  uint64_t* s_consumed = bars + 27; // (leader) 8: warpgroup 1 of both CTAs has loaded S^T cols [64,128)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::OFF_TMEM);
 
   const int warp = threadIdx.x / 32;
@@ -168,15 +176,7 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(kv_full, 1);
-    for (int s = 0; s < 2; ++s) {
-      ptx::mbar_init(&dsx_full[s], 1);
-      ptx::mbar_init(&dsx_ready[s], 1);
-      ptx::mbar_init(&dq_done[s], 1);
-      ptx::mbar_init(&q_full[s], 1);
-      ptx::mbar_init(&q_empty[s], 1);
-      ptx::mbar_init(&vec_full[s], 1);
-      ptx::mbar_init(&vec_empty[s], 8);
-    }
+    ptx::mbar_init(q_full, 1);
     ptx::mbar_init(qk_full, 1);
     ptx::mbar_init(dop_full, 1);
     ptx::mbar_init(dov_full, 1);
@@ -184,7 +184,9 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
     ptx::mbar_init(ds_ready, 16);
     ptx::mbar_init(dq_empty, 8);
     ptx::mbar_init(dkv_empty, 16);
+    ptx::mbar_init(dsx_ready, 1);
     ptx::mbar_init(kv_empty, 1);
+    ptx::mbar_init(q_empty, 1);
     ptx::mbar_init(qk_empty, 1);
     ptx::mbar_init(dop_empty, 1);
     ptx::mbar_init(dov_empty, 1);
@@ -192,6 +194,15 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
     ptx::mbar_init(dp_full, 1);
     ptx::mbar_init(dq_full, 1);
     ptx::mbar_init(dkv_full, 1);
+    ptx::mbar_init(ds_free, 1);
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(&vec_full[s], 1);
+      ptx::mbar_init(&vec_empty[s], 8);
+    }
+    ptx::mbar_init(dsx_full, 1);
+    ptx::mbar_init(xs_full, 4);
+    ptx::mbar_init(xs_empty, 1);
+    ptx::mbar_init(s_consumed, 8);
     ptx::fence_mbar_init();
   }
   if (warp == 13 && lane == 0) {
@@ -205,7 +216,7 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
   pair::cluster_sync();   // barriers initialised and TMEM allocated in both CTAs
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  constexpr uint32_t T_S = 0, T_DP = 128, T_DV = 256, T_DK = 384, T_DQ = 64;
+  constexpr uint32_t T_S = 0, T_DQ = 64, T_DP = 128, T_DV = 256, T_DK = 384;
   const int N = p.geom.Nq;
 
   if (warp < 8) {
@@ -216,16 +227,13 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
     const uint32_t lane_base = static_cast<uint32_t>((warp % 4) * 32) << 16;
     const uint32_t sVec_a = ptx::smem_u32(sVec);
     const int c0 = wg * 64;                             // this warpgroup's 64 query columns
-    // dS row r, query columns [c0, c0 + 64) (128-B swizzled MN-major rows) -> key slot A_rank of
-    // the CTA whose dQ rows they are: the own query half (wg == rank) with plain stores, the
-    // other half straight into the peer's shared memory with st.async, whose bytes complete on
-    // the peer's dsx_full (no fence or wait on this side)
+    // dS row r, query columns [c0, c0 + 64) (128-B swizzled MN-major rows) belong to the CTA
+    // whose dQ rows they are: the own query half (wg == rank) goes into this CTA's A slot
+    // A_rank, the other half is staged in XS and bulk-copied into the peer's A slot A_rank
     const bool own_half = static_cast<uint32_t>(wg) == rank;
-    const uint32_t ds_row = ptx::smem_u32(sDS) + rank * L::BOX128 + (r / 8) * 1024 + (r % 8) * 128;
-    const uint32_t peer = rank ^ 1u;
-    const uint32_t ds_row_peer = pair::map_cta(ds_row, peer);
-    const uint32_t x_bar = pair::map_cta(ptx::smem_u32(dsx_full), peer);   // + 8 * buffer
-    const uint32_t qbar = 2 + (warp % 4);   // named barrier of the two warps sharing these TMEM lanes
+    const uint32_t row_off = (r / 8) * 1024 + (r % 8) * 128;
+    const uint32_t ds_row = own_half ? ptx::smem_u32(sDS) + rank * L::BOX128 + row_off : ptx::smem_u32(sXS) + row_off;
+    const uint32_t pbar = 2 + (warp % 4);   // named barrier of the two warps sharing these TMEM lanes
     const float sl2 = p.scale_log2;
     uint32_t g = 0;
     int it = 0;
@@ -255,6 +263,11 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
             uint32_t sv[32];
             ptx::tmem_ld_x32(tmem + lane_base + T_S + c0 + ch * 32, sv);
             ptx::tmem_wait_ld();
+            if (ch == 1 && wg == 1) {   // S^T cols [64,128) are in registers: dQ(x-1) may land there
+              ptx::tc_fence_before();
+              __syncwarp();
+              if (lane == 0) pair::arrive_remote(s_consumed, 0);
+            }
 #pragma unroll
             for (int e4 = 0; e4 < 8; ++e4) {
               const float4 l4 = ptx::lds_v4f(vL2 + (ch * 32 + e4 * 4) * 4);
@@ -287,13 +300,12 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
         {
           // packed P^T, contiguous: query columns [0,64) at TMEM cols [0,32), [64,128) at [32,64)
           // (A operand of dV); warpgroup 1 overwrites S^T columns warpgroup 0 reads, so it waits
-          // for its partner warp (same lanes) to have loaded them.  Cols [64,128) are then free
-          // for dQ.
+          // for its partner warp (same lanes) to have loaded them
           uint32_t pk[32];
 #pragma unroll
           for (int e = 0; e < 32; ++e) pk[e] = ptx::pack2<BF16>(pf[2 * e], pf[2 * e + 1]);
-          if (wg == 0) ptx::named_bar_arrive(qbar, 64);
-          else ptx::named_bar_sync(qbar, 64);
+          if (wg == 0) ptx::named_bar_arrive(pbar, 64);
+          else ptx::named_bar_sync(pbar, 64);
           ptx::tmem_st_x32(tmem + lane_base + T_S + wg * 32, pk);
         }
         ptx::tmem_wait_st();
@@ -325,29 +337,28 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
           }
         }
         if (threadIdx.x == 0) FA2_BTRACE(11, g);
-        ptx::tmem_st_x32(tmem + lane_base + T_DP + c0, dk);   // A operand of dK
-        // dS buffer g % 2 was last read by dQ two steps ago: wait for it (usually long done)
-        const uint32_t db = g & 1;
-        if (g >= 2) ptx::mbar_wait(&dq_done[db], ((g >> 1) - 1) & 1);
+        // packed dS^T of this warpgroup's 64 query columns over the first 32 of its own dP^T
+        // columns (A operand of dK)
+        ptx::tmem_st_x32(tmem + lane_base + T_DP + c0, dk);
+        // dS rows -> shared memory (A operand of dQ): the own A slot is rewritten once dQ of
+        // the previous step has completed; the staging buffer once warp 15's bulk copy of the
+        // previous step has read it
         if (own_half) {
-#pragma unroll
-          for (int q8 = 0; q8 < 8; ++q8)
-            ptx::sts_v4(ds_row + db * L::DS_BUF + ((q8 ^ (r % 8)) * 16), dk[4 * q8], dk[4 * q8 + 1], dk[4 * q8 + 2],
-                        dk[4 * q8 + 3]);
+          if (g > 0) ptx::mbar_wait(ds_free, (g - 1) & 1);
         } else {
-#pragma unroll
-          for (int q8 = 0; q8 < 8; ++q8)
-            pair::st_async_v4(ds_row_peer + db * L::DS_BUF + ((q8 ^ (r % 8)) * 16), dk[4 * q8], dk[4 * q8 + 1],
-                              dk[4 * q8 + 2], dk[4 * q8 + 3], x_bar + db * 8);
+          if (g > 0) ptx::mbar_wait(xs_empty, (g - 1) & 1);
         }
         if (threadIdx.x == 0) FA2_BTRACE(12, g);
+#pragma unroll
+        for (int q8 = 0; q8 < 8; ++q8)
+          ptx::sts_v4(ds_row + ((q8 ^ (r % 8)) * 16), dk[4 * q8], dk[4 * q8 + 1], dk[4 * q8 + 2], dk[4 * q8 + 3]);
+        ptx::fence_proxy_async_smem();
         ptx::tmem_wait_st();
         if (threadIdx.x == 0) FA2_BTRACE(13, g);
-        ptx::fence_proxy_async_smem();
-        if (threadIdx.x == 0) FA2_BTRACE(14, g);
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) {
+          if (!own_half) ptx::mbar_arrive(xs_full);
           pair::arrive_remote(ds_ready, 0);
           ptx::mbar_arrive(&vec_empty[slot]);
         }
@@ -381,15 +392,19 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
       if (lane == 0) pair::arrive_remote(dkv_empty, 0);
     }
   } else if (warp < 12) {
-    // ====================== dQ read-out + fp32 reduce-add ======================
-    // straight from registers (red.global.add.v4.f32): a warp's 32 lanes hold 32 consecutive
-    // query rows, so with the [d/4][64 rows][4] accumulator layout every red.v4 of a warp covers
-    // 512 contiguous bytes; no shared-memory staging, no barriers
+    // ====================== dQ read-out + fp32 bulk reduce-add ======================
+    // lane L holds query row L % 64 of this CTA's half and d half L / 64 (64 columns); the two
+    // warps of a d half stage their 16 KB in two 8 KB rounds ([c/4][64 rows][4] floats, the
+    // accumulator's own layout) and one of them bulk reduce-adds each round
     ptx::setmaxnreg_inc<152>();
     const int quarter = warp % 4;
     const int row = (quarter % 2) * 32 + lane;          // query row within this CTA's 64
     const int dh = quarter / 2;                          // d half held by this lane
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
+    const bool issuer = (quarter % 2 == 0) && lane == 0;
+    const uint32_t hbar = 11 + dh;                       // the 64 threads of this d half
+    uint8_t* const stage = sDQ + dh * L::DQ_BUF;
+    const uint32_t stage_a = ptx::smem_u32(stage) + row * 16;
     const bool leader = (threadIdx.x == 256);
     uint32_t g = 0;
     for (int n_ = 0, t; (t = pair::sched_tile_pair(sched, n_, p.num_tiles, pair_id, npairs)) >= 0; ++n_) {
@@ -398,9 +413,9 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
       for (int x = 0; x < nx; ++x, ++g) {
         const int i = w.i0 + x % w.nqt;
         const int hq = w.kvh * p.group + x / w.nqt;
-        // this CTA's 32 KB of the tile (query rows [64 rank, +64)), this lane's d half and row
+        // this CTA's 32 KB of the tile (query rows [64 rank, +64)), this d half's 16 KB
         float* const acc = p.dq_acc + ((static_cast<long long>(w.b) * p.H + hq) * p.acc_hs + static_cast<long long>(i) * BM) * D +
-                           (rank * 32 + dh * 16) * 256 + row * 4;
+                           (rank * 32 + dh * 16) * 256;
         ptx::mbar_wait(dq_full, g & 1);
         if (leader) FA2_BTRACE(9, g);
         ptx::tc_fence_after();
@@ -413,149 +428,161 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
         if (lane == 0) pair::arrive_remote(dq_empty, 0);
         if (leader) FA2_BTRACE(10, g);
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          ptx::red_add_v4_f32(acc + j * 256, __uint_as_float(v[4 * j]) * p.scale, __uint_as_float(v[4 * j + 1]) * p.scale,
-                              __uint_as_float(v[4 * j + 2]) * p.scale, __uint_as_float(v[4 * j + 3]) * p.scale);
+        for (int rd = 0; rd < 2; ++rd) {
+          if (issuer) ptx::bulk_wait_read<0>();          // the staging buffer's last round was read
+          ptx::named_bar_sync(hbar, 64);
+#pragma unroll
+          for (int j4 = 0; j4 < 8; ++j4) {
+            const int j = rd * 32 + j4 * 4;
+            ptx::sts_v4(stage_a + j4 * 1024, __float_as_uint(__uint_as_float(v[j]) * p.scale),
+                        __float_as_uint(__uint_as_float(v[j + 1]) * p.scale),
+                        __float_as_uint(__uint_as_float(v[j + 2]) * p.scale),
+                        __float_as_uint(__uint_as_float(v[j + 3]) * p.scale));
+          }
+          ptx::fence_proxy_async_smem();
+          ptx::named_bar_sync(hbar, 64);
+          if (issuer) {
+            ptx::bulk_reduce_add_f32(acc + rd * 2048, stage, L::DQ_BUF);
+            ptx::bulk_commit();
+          }
+        }
         if (leader) FA2_BTRACE(16, g);
       }
     }
+    if (issuer) ptx::bulk_wait<0>();
   } else if (warp == 12) {
     // ================== MMA issuer (leader CTA): whole warp, one elected lane ==================
-    ptx::setmaxnreg_dec<48>();
+    ptx::setmaxnreg_dec<56>();   // 12 x 152 + 4 x 56 = 2048 registers per lane slot
     if (rank == 0) {
       constexpr uint32_t IDESC_S = ptx::idesc_f16(BF16, 256, 128, false, false);   // S^T, dP^T
       constexpr uint32_t IDESC_G = ptx::idesc_f16(BF16, 256, D, false, true);      // dV, dK
       constexpr uint32_t IDESC_Q = ptx::idesc_f16(BF16, 128, D, true, true);       // dQ
-      const uint64_t dK_k = ptx::sw128_desc(ptx::smem_u32(sK), 16, 1024);
-      const uint64_t dV_k = ptx::sw128_desc(ptx::smem_u32(sV), 16, 1024);
-      const uint64_t dQS_k = ptx::sw128_desc(ptx::smem_u32(sQS), 16, 1024);
-      const uint64_t dDOP_k = ptx::sw128_desc(ptx::smem_u32(sDOP), 16, 1024);
-      const uint64_t dDOV_mn = ptx::sw128_desc(ptx::smem_u32(sDOV), L::BOX128, 1024);
-      const uint64_t dQK_mn = ptx::sw128_desc(ptx::smem_u32(sQK), L::BOX128, 1024);
-      const uint64_t dDS_mn = ptx::sw128_desc(ptx::smem_u32(sDS), L::BOX128, 1024);
-      const uint64_t dKD_mn = ptx::sw128_desc(ptx::smem_u32(sKd), L::BOX128, 1024);
-      auto mma_s = [&](uint32_t slot) {   // S^T = K Q^T: K = d, 4 steps per 64-column box
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t offa = (k / 4) * L::BOX128 + (k % 4) * 32;
-          const uint32_t offb = slot * L::QS_STAGE + (k / 4) * L::BOX64 + (k % 4) * 32;
-          pair::mma_ss2(tmem + T_S, dK_k + (offa >> 4), dQS_k + (offb >> 4), IDESC_S, k > 0 ? 1u : 0u);
-        }
-      };
-      auto mma_dp = [&]() {   // dP^T = V dO^T
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t offa = (k / 4) * L::BOX128 + (k % 4) * 32;
-          const uint32_t offb = (k / 4) * L::BOX64 + (k % 4) * 32;
-          pair::mma_ss2(tmem + T_DP, dV_k + (offa >> 4), dDOP_k + (offb >> 4), IDESC_S, k > 0 ? 1u : 0u);
-        }
-      };
-      // dQ(y) = dS K over the pair's 256 keys into S^T cols [64,128), once both CTAs' A slots
-      // hold step y's dS (own half stored locally, the peer's half landed by st.async)
-      auto issue_dq = [&](uint32_t y) {
-        const uint32_t db = y & 1, ph = (y >> 1) & 1;
-        ptx::mbar_wait(&dsx_full[db], ph);                 // CTA 1's half landed here
-        pair::wait_cluster_acquire(&dsx_ready[db], ph);   // CTA 0's half landed in CTA 1
-        ptx::fence_proxy_async_smem();
+      // descriptors are rebuilt from the 32-bit shared-window base at every issue (a few
+      // integer ops) instead of keeping eight 64-bit values live in this 56-register warp
+      const uint32_t sb = ptx::smem_u32(smem);
+      auto kmaj = [&](int off) { return ptx::sw128_desc(sb + off, 16, 1024); };
+      auto mnmaj = [&](int off) { return ptx::sw128_desc(sb + off, L::BOX128, 1024); };
+      // each issue step: wait (whole warp), fence, one elected lane issues + commits
+      auto issue_s = [&]() {   // S^T = K Q^T: K = d, 4 steps per 64-column box
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
 #pragma unroll
-          for (int k = 0; k < 256 / 16; ++k) {
-            const uint32_t off = (db * L::DS_BUF + (k / 8) * L::BOX128 + (k % 8) * 2048) >> 4;
-            const uint32_t offb = ((k / 8) * L::BOX128 + (k % 8) * 2048) >> 4;
-            pair::mma_ss2(tmem + T_DQ, dDS_mn + off, dKD_mn + offb, IDESC_Q, k > 0 ? 1u : 0u);
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t offa = (k / 4) * L::BOX128 + (k % 4) * 32;
+            const uint32_t offb = (k / 4) * L::BOX64 + (k % 4) * 32;
+            pair::mma_ss2(tmem + T_S, kmaj(L::OFF_K) + (offa >> 4), kmaj(L::OFF_QS) + (offb >> 4), IDESC_S, k > 0 ? 1u : 0u);
           }
-          pair::commit_both(dq_full);
-          pair::commit_both(&dq_done[db]);
+          pair::commit_both(s_full);
+          pair::commit_both(q_empty);
         }
         __syncwarp();
       };
-      // Issue order for query step x (steady state):
-      //   dV(x) [P^T(x)], dQ(x-1) [dS(x-1) exchanged; S^T cols [64,128) read by P(x)],
-      //   S^T(x+1) [dQ(x-1) read out], dK(x) [dS^T(x)], dP^T(x+1) [dK(x) read dS^T(x), in order]
-      // so dP^T(x+1) never waits for the dQ read-out or the exchange.
+      auto issue_dp = [&]() {   // dP^T = V dO^T
+        ptx::tc_fence_after();
+        if (ptx::elect_one()) {
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t offa = (k / 4) * L::BOX128 + (k % 4) * 32;
+            const uint32_t offb = (k / 4) * L::BOX64 + (k % 4) * 32;
+            pair::mma_ss2(tmem + T_DP, kmaj(L::OFF_V) + (offa >> 4), kmaj(L::OFF_DOP) + (offb >> 4), IDESC_S, k > 0 ? 1u : 0u);
+          }
+          pair::commit_both(dp_full);
+          pair::commit_both(dop_empty);
+        }
+        __syncwarp();
+      };
+      auto issue_dv = [&](bool acc) {   // dV += P^T dO (A: packed P^T at TMEM cols [0,64))
+        ptx::tc_fence_after();
+        if (ptx::elect_one()) {
+#pragma unroll
+          for (int k = 0; k < BM / 16; ++k)
+            pair::mma_ts2(tmem + T_DV, tmem + T_S + k * 8, mnmaj(L::OFF_DOV) + ((k * 2048) >> 4), IDESC_G, (acc || k > 0) ? 1u : 0u);
+          pair::commit_both(dov_empty);
+        }
+        __syncwarp();
+      };
+      auto issue_dk = [&](bool acc) {   // dK += dS^T Q (A: packed dS^T at TMEM cols [128,160) | [192,224))
+        ptx::tc_fence_after();
+        if (ptx::elect_one()) {
+#pragma unroll
+          for (int k = 0; k < BM / 16; ++k)
+            pair::mma_ts2(tmem + T_DK, tmem + T_DP + (k / 4) * 64 + (k % 4) * 8, mnmaj(L::OFF_QK) + ((k * 2048) >> 4), IDESC_G,
+                          (acc || k > 0) ? 1u : 0u);
+          pair::commit_both(qk_empty);
+        }
+        __syncwarp();
+      };
+      // dQ = dS K over the pair's 256 keys into S^T cols [64,128), once the dS rows of both
+      // query halves sit in both CTAs' A slots
+      auto issue_dq = [&](uint32_t y) {
+        ptx::mbar_wait(dsx_full, y & 1);                   // CTA 1's rows landed here
+        pair::wait_cluster(dsx_ready, y & 1);              // CTA 0's rows landed in CTA 1
+        ptx::tc_fence_after();
+        if (ptx::elect_one()) {
+#pragma unroll 1   // rolled: sixteen hoisted 64-bit descriptor pairs would not fit the warp's registers
+          for (int k = 0; k < 256 / 16; ++k) {
+            const uint32_t off = ((k / 8) * L::BOX128 + (k % 8) * 2048) >> 4;
+            pair::mma_ss2(tmem + T_DQ, mnmaj(L::OFF_DS) + off, mnmaj(L::OFF_KD) + off, IDESC_Q, k > 0 ? 1u : 0u);
+          }
+          pair::commit_both(dq_full);
+          pair::commit_both(ds_free);
+        }
+        __syncwarp();
+      };
+      // Issue order, step x (steady state):
+      //   dK(x) [dS^T(x)], dP^T(x+1) [dK(x) read dS^T(x), in order],
+      //   dQ(x) [dS(x) in both CTAs' A slots; P(x+1) has loaded S^T cols [64,128)],
+      //   dV(x+1) [P^T(x+1)], S^T(x+2) [dQ(x) read out]
+      // dQ(x) completes well before the compute warps rewrite the (single) A slots with
+      // dS(x+1), and the exchange of dS(x) overlaps dK(x) / dP^T(x+1) and P(x+1).
       uint32_t g = 0;
       int it = 0;
       for (int n_ = 0, t; (t = pair::sched_tile_pair(sched, n_, p.num_tiles, pair_id, npairs)) >= 0; ++n_, ++it) {
         const PairTile w = pair_tile(p, CAUSAL, t);
         const uint32_t n = static_cast<uint32_t>(w.nqt * p.group);
-        const uint32_t g0 = g;
+        const uint32_t g0 = g, end = g0 + n;
+        // prologue: S^T(g0), dP^T(g0), dV(g0), S^T(g0+1)
         ptx::mbar_wait(kv_full, it & 1);
-        ptx::mbar_wait(&q_full[g0 % QST], (g0 / QST) & 1);
+        ptx::mbar_wait(q_full, g0 & 1);
         if (g0 > 0) pair::wait_cluster(dq_empty, (g0 - 1) & 1);   // previous tile's last dQ read out
-        ptx::tc_fence_after();
-        if (ptx::elect_one()) {
-          mma_s(g0 % QST);
-          pair::commit_both(s_full);
-          pair::commit_both(&q_empty[g0 % QST]);
-        }
-        __syncwarp();
+        issue_s();
         ptx::mbar_wait(dop_full, g0 & 1);
-        ptx::tc_fence_after();
-        if (ptx::elect_one()) {
-          mma_dp();
-          pair::commit_both(dp_full);
-          pair::commit_both(dop_empty);
+        issue_dp();
+        if (it > 0) pair::wait_cluster(dkv_empty, (it - 1) & 1);  // previous dK / dV drained
+        ptx::mbar_wait(dov_full, g0 & 1);
+        pair::wait_cluster(p_ready, g0 & 1);
+        issue_dv(false);
+        if (g0 + 1 < end) {
+          ptx::mbar_wait(q_full, (g0 + 1) & 1);
+          issue_s();
         }
-        __syncwarp();
-        if (it > 0) pair::wait_cluster(dkv_empty, (it - 1) & 1);   // previous dK / dV drained
-        for (uint32_t x = g0; x < g0 + n; ++x) {
-          const bool first = (x == g0);
-          // dV += P^T dO  (A: packed P^T, query columns [0,128) at TMEM cols [0,64))
-          ptx::mbar_wait(dov_full, x & 1);
-          pair::wait_cluster(p_ready, x & 1);
-          FA2_BTRACE(4, x);
-          ptx::tc_fence_after();
-          if (ptx::elect_one()) {
-#pragma unroll
-            for (int k = 0; k < BM / 16; ++k)
-              pair::mma_ts2(tmem + T_DV, tmem + T_S + k * 8, dDOV_mn + ((k * 2048) >> 4), IDESC_G, (!first || k > 0) ? 1u : 0u);
-            pair::commit_both(dov_empty);
-          }
-          __syncwarp();
-          if (!first) issue_dq(x - 1);
-          FA2_BTRACE(5, x);
-          // S^T of the next query tile (its P^T columns were just consumed by dV, in order)
-          if (x + 1 < g0 + n) {
-            ptx::mbar_wait(&q_full[(x + 1) % QST], ((x + 1) / QST) & 1);
-            if (!first) pair::wait_cluster(dq_empty, (x - 1) & 1);
-            ptx::tc_fence_after();
-            if (ptx::elect_one()) {
-              mma_s((x + 1) % QST);
-              pair::commit_both(s_full);
-              pair::commit_both(&q_empty[(x + 1) % QST]);
-            }
-            __syncwarp();
-            FA2_BTRACE(6, x);
-          }
-          // dK += dS^T Q
+        for (uint32_t x = g0; x < end; ++x) {
           pair::wait_cluster(ds_ready, x & 1);
           FA2_BTRACE(7, x);
           ptx::mbar_wait(qk_full, x & 1);
-          ptx::tc_fence_after();
-          if (ptx::elect_one()) {
-#pragma unroll
-            for (int k = 0; k < BM / 16; ++k)
-              pair::mma_ts2(tmem + T_DK, tmem + T_DP + (k / 4) * 64 + (k % 4) * 8, dQK_mn + ((k * 2048) >> 4), IDESC_G,
-                            (!first || k > 0) ? 1u : 0u);
-            pair::commit_both(qk_empty);
-          }
-          __syncwarp();
-          // dP^T of the next query tile (dK just read dS^T(x) out of these columns, in order)
-          if (x + 1 < g0 + n) {
+          issue_dk(x > g0);
+          if (x + 1 < end) {
             ptx::mbar_wait(dop_full, (x + 1) & 1);
-            ptx::tc_fence_after();
-            if (ptx::elect_one()) {
-              mma_dp();
-              pair::commit_both(dp_full);
-              pair::commit_both(dop_empty);
-            }
-            __syncwarp();
+            issue_dp();
+            pair::wait_cluster(s_consumed, (x + 1) & 1);
           }
           FA2_BTRACE(8, x);
+          issue_dq(x);
+          FA2_BTRACE(5, x);
+          if (x + 1 < end) {
+            ptx::mbar_wait(dov_full, (x + 1) & 1);
+            pair::wait_cluster(p_ready, (x + 1) & 1);
+            FA2_BTRACE(4, x + 1);
+            issue_dv(true);
+            if (x + 2 < end) {
+              ptx::mbar_wait(q_full, (x + 2) & 1);
+              pair::wait_cluster(dq_empty, x & 1);                 // dQ(x) read out of [64,128)
+              issue_s();
+            }
+            FA2_BTRACE(6, x + 1);
+          }
         }
-        issue_dq(g0 + n - 1);
-        g = g0 + n;
+        g = end;
         if (ptx::elect_one()) {
           pair::commit_both(dkv_full);
           pair::commit_both(kv_empty);
@@ -565,7 +592,7 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
     }
   } else if (warp == 13) {
     // ============================ TMA producer (both CTAs) ============================
-    ptx::setmaxnreg_dec<48>();
+    ptx::setmaxnreg_dec<56>();
     if (lane == 0) {
       const float* gD = p.dvec;
       const float* gL2 = p.dvec + p.acc_rows;
@@ -597,13 +624,11 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
           const long long voff = static_cast<long long>(bhq) * p.acc_hs + static_cast<long long>(i) * BM;
           ptx::bulk_load_1d(sVec + slot * 2 * BM, gL2 + voff, BM * 4, &vec_full[slot]);
           ptx::bulk_load_1d(sVec + slot * 2 * BM + BM, gD + voff, BM * 4, &vec_full[slot]);
-          // Q_i rows of this CTA's query half, all d (QST-stage ring; released after S^T(i))
-          const uint32_t qs = g % QST;
-          if (g >= QST) ptx::mbar_wait(&q_empty[qs], ((g / QST) - 1) & 1);
-          if (rank == 0) ptx::mbar_arrive_expect_tx(&q_full[qs], 2 * L::QS_STAGE);
+          // Q_i rows of this CTA's query half, all d (released after S^T(i))
+          if (g >= 1) ptx::mbar_wait(q_empty, (g - 1) & 1);
+          if (rank == 0) ptx::mbar_arrive_expect_tx(q_full, 2 * 2 * L::BOX64);
           for (int s = 0; s < 2; ++s)
-            pair::tma_load_pair(sQS + qs * L::QS_STAGE + s * L::BOX64, &tm_q64, &q_full[qs], s * 64,
-                                i * BM + ro * 64, bhq, pol_q);
+            pair::tma_load_pair(sQS + s * L::BOX64, &tm_q64, q_full, s * 64, i * BM + ro * 64, bhq, pol_q);
           // dO_i rows of this CTA's query half, all d (released after dP^T(i))
           if (g >= 1) ptx::mbar_wait(dop_empty, (g - 1) & 1);
           if (rank == 0) ptx::mbar_arrive_expect_tx(dop_full, 2 * 2 * L::BOX64);
@@ -622,28 +647,49 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
     }
   } else if (warp == 14) {
     // ============ dS exchange bookkeeping (both CTAs) ============
-    // each step the peer's compute warps bulk-copy 4 x 4 KB into this CTA's A slot, completing
-    // on dsx_full; CTA 1 relays its completion to the leader (whose MMA cannot wait on a
-    // remote barrier)
-    ptx::setmaxnreg_dec<48>();
+    // each step the peer bulk-copies 16 KB into this CTA's A slot, completing on dsx_full;
+    // CTA 1 relays its completion to the leader (whose MMA warp waits on local barriers)
+    ptx::setmaxnreg_dec<56>();
     if (lane == 0) {
       uint32_t g = 0;
       for (int n_ = 0, t; (t = pair::sched_tile_pair(sched, n_, p.num_tiles, pair_id, npairs)) >= 0; ++n_) {
         const PairTile w = pair_tile(p, CAUSAL, t);
         const int nx = w.nqt * p.group;
         for (int x = 0; x < nx; ++x, ++g) {
-          const uint32_t db = g & 1;
-          ptx::mbar_arrive_expect_tx(&dsx_full[db], L::BOX128);
-          ptx::mbar_wait(&dsx_full[db], (g >> 1) & 1);
-          if (rank == 1) {
-            ptx::fence_proxy_async_smem();   // st.async (generic) writes -> visible to the tensor core
-            pair::arrive_remote_release(&dsx_ready[db], 0);
-          }
+          ptx::mbar_arrive_expect_tx(dsx_full, L::BOX128);
+          ptx::mbar_wait(dsx_full, g & 1);
+          FA2_BTRACE(20, g);
+          if (rank == 1) pair::arrive_remote(dsx_ready, 0);
         }
       }
     }
   } else {
-    ptx::setmaxnreg_dec<48>();
+    // ============ warp 15: dS exchange issuer (both CTAs) ============
+    // bulk-copies the staged rows (own keys, the peer's query half) into the peer's A slot
+    // A_rank once the peer's dQ of the previous step has released it (ds_free, multicast)
+    ptx::setmaxnreg_dec<56>();
+    if (lane == 0) {
+      const uint32_t peer = rank ^ 1u;
+      const uint32_t peer_slot = pair::map_cta(ptx::smem_u32(sDS) + rank * L::BOX128, peer);
+      const uint32_t peer_bar = pair::map_cta(ptx::smem_u32(dsx_full), peer);
+      uint32_t g = 0;
+      for (int n_ = 0, t; (t = pair::sched_tile_pair(sched, n_, p.num_tiles, pair_id, npairs)) >= 0; ++n_) {
+        const PairTile w = pair_tile(p, CAUSAL, t);
+        const int nx = w.nqt * p.group;
+        for (int x = 0; x < nx; ++x, ++g) {
+          ptx::mbar_wait(xs_full, g & 1);
+          FA2_BTRACE(17, g);
+          if (g > 0) ptx::mbar_wait(ds_free, (g - 1) & 1);
+          FA2_BTRACE(18, g);
+          pair::bulk_copy_to_cta(peer_slot, sXS, L::BOX128, peer_bar);
+          ptx::bulk_commit();
+          ptx::bulk_wait_read<0>();
+          FA2_BTRACE(19, g);
+          ptx::mbar_arrive(xs_empty);
+        }
+      }
+      ptx::bulk_wait<0>();
+    }
   }
   __syncwarp();
   ptx::tc_fence_before();

@@ -13,6 +13,7 @@ import torch
 import paper_2307_08691_b200 as fa2
 import workloads as W
 from oracle import ref_attention as R
+from tests.fp8_bound import fp8_pv_error_bound
 from tests.gpu_util import TOL, half_ulp, scale_for
 
 pytestmark = pytest.mark.gpu
@@ -34,7 +35,7 @@ def _check(o, lse, q8, k8, v8, dq, dk, dv, sc, causal):
     og = o.double().cpu().numpy()
     for b in range(B):
         for h in range(H):
-            bound = R.fp8_pv_error_bound(qd[b, h], kd[b, h // group], vd[b, h // group], sc, causal)
+            bound = fp8_pv_error_bound(qd[b, h], kd[b, h // group], vd[b, h // group], sc, causal)
             p, _, _ = R.softmax_rows(R.scores(qd[b, h], kd[b, h // group], sc, causal))
             slack = 2.0 ** -11 * (p @ np.abs(vd[b, h // group]))
             err = np.abs(og[b, h] - o_ref[b, h]) - half_ulp(o_ref[b, h], "bf16")

@@ -15,6 +15,7 @@ import pytest
 
 from oracle import flops as F
 from oracle import ref_attention as R
+from tests.fp8_bound import fp8_pv_error_bound
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))
 
@@ -665,7 +666,7 @@ def test_fp8_bound_matches_brute_force_and_holds(causal):
     n, d = 11, 4
     q, k, v = r.normal(size=(3, n, d))
     sc = 0.9
-    bound = R.fp8_pv_error_bound(q, k, v, sc, causal)
+    bound = fp8_pv_error_bound(q, k, v, sc, causal)
     # brute force of the formula
     for i in range(n):
         vis = [j for j in range(n) if not (causal and j > i)]

@@ -19,7 +19,8 @@ FULL = [  # name, B, H, N, d, causal, dtype, check backward
     ("PS64_N512", 32, 32, 512, 64, False, "bf16", True),         # configs[1] smallest N
     ("GPT_N8192_causal", 8, 20, 8192, 128, True, "bf16", True),  # configs[3]
     ("LC_N32768_causal", 1, 16, 32768, 128, True, "fp16", True), # configs[4]
-    ("LC_N65536_causal", 1, 16, 65536, 128, True, "fp16", False),
+    ("LC_N65536_causal", 1, 16, 65536, 128, True, "fp16", True), # configs[4] largest N (8192 tiles: schedule cap)
+    ("PS128_N8192_fp16", 2, 16, 8192, 128, False, "fp16", True), # bench workload in fp16 (CTA-pair forward)
 ]
 
 
@@ -60,9 +61,8 @@ def test_full_size_sampled(case):
         sm = R.backward_sampled_head(f64(q[b, h]), f64(k[b, h]), f64(v[b, h]), f64(do[b, h]), sc, causal,
                                      dq_rows=rows, dkv_cols=cols, rows_per_chunk=1024)
         got = {"dq": dq[b, h, rows], "dk": dk[b, h, cols], "dv": dv[b, h, cols]}
-        floor = 2.0 ** -8 * max(float(np.max(np.abs(sm[x]))) for x in ("dq", "dk", "dv"))
-        for x in ("dq", "dk", "dv"):
+        for x in ("dq", "dk", "dv"):   # no case here is degenerate: plain rule R15, no floor
             ref = sm[x]
             err = float(np.max(np.abs(got[x].double().cpu().numpy() - ref)))
-            lim = TOL[dtype]["grad"] * max(float(np.max(np.abs(ref))), floor)
+            lim = TOL[dtype]["grad"] * float(np.max(np.abs(ref)))
             assert err <= lim, (name, x, err, lim)

@@ -249,3 +249,20 @@ def test_binding_rejects_bad_buffers():
         fa2.attention_step_host(q, k, v, do, {}, arena, False)                # device tensors as host inputs
     with pytest.raises(fa2.FA2Error):
         fa2.attention_step_host(hq, hk, hv, hdo, {}, arena[:100], False)      # arena too small
+
+
+def test_one_sm_d128_backward_kernel_parity():
+    """The square d = 128 backward runs on the CTA-pair kernel by default; the one-SM
+    kernel (fa2_bwd128_kernel) still serves varlen, N_q != N_k, deterministic and split-GQA
+    calls.  Run the backward parity cases once more with FA2_BWD_PAIR=0 (read at library
+    load, hence a subprocess) so both kernels stay checked on the square shapes."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FA2_BWD_PAIR="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", os.path.join(root, "tests", "test_parity_gpu.py"),
+                        "-k", "test_backward_parity or test_gqa_parity"], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout

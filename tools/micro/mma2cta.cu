@@ -70,6 +70,76 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k(unsigned l
   }
 }
 
+// The pair backward's dQ shape: M = 128 (64 query rows per CTA), N = d = 128 (64 per CTA),
+// K = 256 keys in 16 steps; A (dS) and B (K) MN-major, 128-B swizzled boxes of 128 rows.
+template <int M>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) kq(unsigned long long* cyc, int reps) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  for (int i = threadIdx.x; i < (96 * 1024) / 16; i += blockDim.x) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  const uint32_t rank = cluster_rank();
+  if (threadIdx.x == 0) { ptx::mbar_init(&bar, 1); ptx::fence_mbar_init(); }
+  if (threadIdx.x < 32)
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" :: "r"(ptx::smem_u32(&slot)), "r"(512));
+  ptx::fence_proxy_async_smem();
+  ptx::tc_fence_before();
+  cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem = slot;
+  unsigned long long t0 = clock64();
+  if (rank == 0 && threadIdx.x < 32) {
+    const uint32_t a = ptx::smem_u32(smem), b = a + 32768;
+    const uint64_t dA = ptx::sw128_desc(a, 16384, 1024), dB = ptx::sw128_desc(b, 16384, 1024);
+    constexpr uint32_t ID = ptx::idesc_f16(true, M, 128, true, true);
+    if (ptx::elect_one()) {
+      for (int r = 0; r < reps; ++r) {
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+          const uint32_t off = ((kk / 8) * 16384 + (kk % 8) * 2048) >> 4;
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                       :: "r"(tmem), "l"(dA + off), "l"(dB + off), "r"(ID), "r"(1u) : "memory");
+        }
+      }
+      asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                   :: "r"(ptx::smem_u32(&bar)), "h"((uint16_t)0x3) : "memory");
+    }
+    __syncwarp();
+  }
+  if (threadIdx.x == 0) {
+    ptx::mbar_wait(&bar, 0);
+    cyc[blockIdx.x] = clock64() - t0;
+  }
+  ptx::tc_fence_before();
+  cluster_sync();
+  if (threadIdx.x < 32) {
+    ptx::tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::);
+  }
+}
+
+template <int M>
+void runq(unsigned long long* cyc) {
+  const int reps = 512, smem = 96 * 1024 + 1024;
+  cudaFuncSetAttribute(kq<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  for (int grid : {2, 148}) {
+    kq<M><<<grid, 128, smem>>>(cyc, reps);
+    kq<M><<<grid, 128, smem>>>(cyc, reps);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) { printf("kq M=%d grid %d: %s\n", M, grid, cudaGetErrorString(e)); return; }
+    unsigned long long h[148];
+    cudaMemcpy(h, cyc, 8 * grid, cudaMemcpyDeviceToHost);
+    double mx = 0;
+    for (int i = 0; i < grid; ++i) mx = mx > h[i] ? mx : h[i];
+    const double per = mx / (reps * 16.0);
+    printf("cta_group::2 M%d N128 MN-major A,B (dQ shape) grid %3d: %.1f cycles per K=16 MMA (full-rate floor %d)\n", M,
+           grid, per, M * 128 / 256);
+  }
+}
+
 template <int N>
 void run(unsigned long long* cyc) {
   const int reps = 512, smem = 96 * 1024 + 1024;
@@ -94,5 +164,7 @@ int main() {
   run<128>(cyc);
   run<64>(cyc);
   run<256>(cyc);
+  runq<128>(cyc);
+  runq<256>(cyc);
   return 0;
 }

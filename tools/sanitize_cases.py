@@ -1,5 +1,6 @@
 """Small forward/backward cases over every code path (fixed, GQA split, deterministic,
-N_q != N_k, varlen with empty sequences, FP8) for compute-sanitizer runs."""
+N_q != N_k, varlen with empty sequences, FP8, the CTA-pair forward and backward) for
+compute-sanitizer runs."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -27,6 +28,12 @@ for d in (64, 128):
     q3, k3, v3, do3 = (mk(1, 3, 1500, d) for _ in range(4))
     o3, l3 = fa2.forward(q3, k3, v3, causal=True)
     fa2.backward(q3, k3, v3, o3, l3, do3, causal=True)
+    # square MHA shapes: the CTA-pair forward (non-causal d = 128) and the CTA-pair backward
+    # (d = 128, causal and not), ragged (700 = 2 pair key blocks + a 188-row tail)
+    for causal in (False, True):
+        q4, k4, v4, do4 = (mk(1, 2, 700, d) for _ in range(4))
+        o4, l4 = fa2.forward(q4, k4, v4, causal=causal)
+        fa2.backward(q4, k4, v4, o4, l4, do4, causal=causal)
     if d == 128:
         q8, k8, v8 = (mk(1, 2, 300, 128).to(torch.float8_e4m3fn) for _ in range(3))
         fa2.forward_fp8(q8, k8, v8, causal=True)
