@@ -171,7 +171,7 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
           for (int c = 0; c < 128; ++c)
             if (c0 + c >= N) s[c] = -INFINITY;
         }
-        float mx = s[0];
+        float mx = s[0];   // (a tree of 3-input maxima measured 1.7% slower here)
 #pragma unroll
         for (int c = 1; c < 128; ++c) mx = fmaxf(mx, s[c]);
         if (tr) FA2_TRACE(1, wg, j);

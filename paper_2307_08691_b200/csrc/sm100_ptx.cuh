@@ -302,6 +302,32 @@ __host__ __device__ constexpr uint32_t idesc_f16(bool bf16, int M, int N, bool a
 // ----------------------------------------------------------------------------
 // Numeric helpers
 // ----------------------------------------------------------------------------
+// 3-input max (FMNMX3 on sm_100a)
+FA2_DEVICE float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// Max of N (>= 2) values as a tree of 3-input maxima: depth ~log3 N instead of a serial
+// chain of N/2 dependent FMNMX3 (the row max of the softmax, one thread per row).
+template <int N>
+FA2_DEVICE float tree_max(const float* v) {
+  if constexpr (N == 1) {
+    return v[0];
+  } else if constexpr (N == 2) {
+    return fmaxf(v[0], v[1]);
+  } else if constexpr (N == 3) {
+    return fmax3(v[0], v[1], v[2]);
+  } else {
+    constexpr int M = (N + 2) / 3;
+    float t[M];
+#pragma unroll
+    for (int i = 0; i < N / 3; ++i) t[i] = fmax3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+    if constexpr (N % 3 == 1) t[M - 1] = v[N - 1];
+    if constexpr (N % 3 == 2) t[M - 1] = fmaxf(v[N - 2], v[N - 1]);
+    return tree_max<M>(t);
+  }
+}
 FA2_DEVICE float ex2(float x) { float y; asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 FA2_DEVICE float lg2(float x) { float y; asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 
