@@ -539,9 +539,10 @@ fa2::RowParams row_params(const Geom& g, const WsLayout& w, const void* o, const
 }
 
 fa2_status_t preprocess_impl(const fa2::RowParams& rp, int d, fa2_dtype_t dtype, cudaStream_t st) {
-  // one warp per padded workspace row; 8 rows per 256-thread block (32-bit row arithmetic in the kernels)
+  // d / 8 threads per padded workspace row, 256-thread blocks
   if (rp.acc_rows >= (1LL << 31)) return fail(FA2_ERR_INVALID_ARG, "problem too large: %lld padded query rows", rp.acc_rows);
-  const long long grid = (rp.acc_rows + 7) / 8;
+  const long long grid = (rp.acc_rows * (d / 8) + 255) / 256;
+  if (grid >= (1LL << 31)) return fail(FA2_ERR_INVALID_ARG, "problem too large: %lld padded query rows", rp.acc_rows);
   const bool bf16 = dtype == FA2_BF16;
   if (d == 64) {
     if (bf16) fa2::fa2_bwd_preprocess<64, true><<<static_cast<int>(grid), 256, 0, st>>>(rp);

@@ -262,31 +262,31 @@ __global__ void __launch_bounds__(1024) fa2_tile_prefix(const int* __restrict__ 
 // ---------------------------------------------------------------------------
 template <int D, bool BF16>
 __global__ void __launch_bounds__(256) fa2_bwd_preprocess(const RowParams p) {
-  const long long R = static_cast<long long>(blockIdx.x) * 8 + threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  if (R >= p.acc_rows) return;
+  // D / 8 threads per padded workspace row, 16-byte loads of O and dO (8 elements each), the
+  // row sum reduced over the row's lanes: enough bytes in flight per SM for HBM (one warp
+  // per row with 4-8 byte loads ran at ~2.7 TB/s)
+  constexpr int TPR = D / 8;
+  const long long gt = static_cast<long long>(blockIdx.x) * 256 + threadIdx.x;
+  const long long R = gt / TPR;
+  const int sub = static_cast<int>(gt % TPR);
+  const bool in = R < p.acc_rows;
   long long q_off = 0, l_off = 0;
-  const bool real = acc_row_ref(p, R, q_off, l_off);
-  constexpr int PER = D / 32;  // elements per lane (2 or 4)
+  const bool real = in && acc_row_ref(p, R, q_off, l_off);
   float acc = 0.f;
   if (real) {
-    const long long base = q_off + lane * PER;
-    if constexpr (PER == 4) {
-      const uint2 a = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(p.o) + base);
-      const uint2 c = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(p.dout) + base);
-      const float2 a0 = ptx::unpack2<BF16>(a.x), a1 = ptx::unpack2<BF16>(a.y);
-      const float2 c0 = ptx::unpack2<BF16>(c.x), c1 = ptx::unpack2<BF16>(c.y);
-      acc = a0.x * c0.x + a0.y * c0.y + a1.x * c1.x + a1.y * c1.y;
-    } else {
-      const uint32_t a = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint16_t*>(p.o) + base);
-      const uint32_t c = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint16_t*>(p.dout) + base);
-      const float2 a0 = ptx::unpack2<BF16>(a), c0 = ptx::unpack2<BF16>(c);
-      acc = a0.x * c0.x + a0.y * c0.y;
-    }
+    const uint4 a = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(p.o) + q_off + sub * 8);
+    const uint4 c = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(p.dout) + q_off + sub * 8);
+    const uint32_t av[4] = {a.x, a.y, a.z, a.w}, cv[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    for (int e = 0; e < 4; ++e) {
+      const float2 x = ptx::unpack2<BF16>(av[e]), y = ptx::unpack2<BF16>(cv[e]);
+      acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
+    }
   }
-  if (lane == 0) {
+#pragma unroll
+  for (int off = TPR / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (!in) return;
+  if (sub == 0) {
     p.dvec[R] = acc;
     if (p.lse2 != nullptr) {
       const float l = real ? p.lse[l_off] : INFINITY;
@@ -295,8 +295,9 @@ __global__ void __launch_bounds__(256) fa2_bwd_preprocess(const RowParams p) {
     if (p.dq_sem != nullptr && R % 128 == 0) p.dq_sem[R / 128] = 0;
   }
   if (p.dq_acc != nullptr) {
-    float4* z = reinterpret_cast<float4*>(p.dq_acc + R * D);
-    for (int c = lane; c < D / 4; c += 32) z[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4* z = reinterpret_cast<float4*>(p.dq_acc + R * D + sub * 8);
+    z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
 }
 

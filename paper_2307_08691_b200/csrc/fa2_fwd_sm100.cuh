@@ -23,14 +23,14 @@
 //   warps 4-7   softmax WG 1: rows of Q1
 //   warp  8     MMA issuer (one elected thread)
 //   warp  9     TMA producer of Q and K, warp 10 TMA producer of V (one thread each)
-//   warp  11    idle (HB: MMA issuer of sub-tile 1)
+//   warp  11    idle
 //
 // TMEM columns: S0 [0,128), S1 [128,256), O0 [256,256+D), O1 [256+D,256+2D);
 // P~_i (16-bit) is written over the first 64 columns of S_i (d = 64: own columns).
 //
-// Compile-time alternatives, measured on B200 and off by default:
-// FA2_FWD_RS=2 (two warps per row, row max exchanged through SMEM) and FA2_FWD_HB=1
-// (B_c = 64, double-buffered P~, one MMA issuer per sub-tile).
+// Alternatives measured on B200 and removed: two warps per row with the
+// row max exchanged through SMEM; B_c = 64 with double-buffered P~ and one MMA issuer per
+// sub-tile.
 #pragma once
 #include <cuda_fp16.h>
 #include <cuda_bf16.h>
@@ -50,29 +50,11 @@ namespace fa2 {
 #define FA2_FWD_EMU_PAIRS_D64 6
 #endif
 constexpr int kFwdEmuPairs = FA2_FWD_EMU_PAIRS;
-// Row split (bf16/fp16, d = 128): each 128-row sub-tile's softmax runs on 8 warps, two
-// per TMEM lane quarter, each owning 64 of the 128 columns of its rows (row max
-// exchanged through shared memory).  One warp per SMSP per sub-tile reaches only ~2/3
-// of the MUFU.EX2 rate (tools/micro/mufu2.cu); two reach ~90%.
-#ifndef FA2_FWD_RS
-#define FA2_FWD_RS 1
-#endif
-#ifndef FA2_FWD_RS64
-#define FA2_FWD_RS64 1
-#endif
-// 64-key blocks (bf16/fp16, d = 128): B_c = 64 gives every sub-tile its own P~ columns
-// (TMEM: O0 O1 [0,256) | S0 S1 [256,384) | P~ 2 x 2 buffers [384,512)), so S_{j+1} is issued as
-// soon as the softmax has read S_j and the softmax -> P~V -> S chain disappears.  The
-// TMA stages stay 128 key rows (two blocks each).
-#ifndef FA2_FWD_HB
-#define FA2_FWD_HB 0
-#endif
 template <int D, bool FP8> struct FwdCfg {
-  static constexpr int RS = (D == 128 && !FP8) ? FA2_FWD_RS : (D == 64 ? FA2_FWD_RS64 : 1);   // warps per row quarter
-  static constexpr int SM_WARPS = 8 * RS;                          // softmax warps (both sub-tiles)
-  static constexpr int THREADS = SM_WARPS * 32 + 128;              // + MMA, TMA, 2 idle
-  static constexpr int REG_SM = RS == 2 ? 104 : 224;               // setmaxnreg per warpgroup
-  static constexpr int REG_OTHER = RS == 2 ? 64 : 56;   // RS = 2: 104*512 + 64*128 == 96*640 (the launch allocation)
+  static constexpr int SM_WARPS = 8;                   // softmax warps (both sub-tiles)
+  static constexpr int THREADS = SM_WARPS * 32 + 128;  // + MMA, 2 TMA, 1 idle
+  static constexpr int REG_SM = 224;                   // setmaxnreg: 224*256 + 56*128 == 168*384
+  static constexpr int REG_OTHER = 56;
 };
 constexpr int kFwdEmuPairsD64 = FA2_FWD_EMU_PAIRS_D64;
 
@@ -116,9 +98,7 @@ struct FwdSmem {
   // barriers: q_full[2] q_empty[2] k_full[S] k_empty[S] v_full[S] v_empty[S] s_full[2] p_full[2][2] o_done[2][2] o_empty[2]
   static constexpr int NBAR = 2 + 2 + 4 * STAGES + 2 + 4 + 4 + 2 + 2;   // + s_consumed[2]
   static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
-  // row-split exchange: max[2 parities][2 sub-tiles][2 halves][128 rows], l[2][2][128]
-  static constexpr int OFF_RED = OFF_TMEM + 16;
-  static constexpr int BYTES = OFF_RED + (2 * 2 * 2 * 128 + 2 * 2 * 128) * 4;
+  static constexpr int BYTES = OFF_TMEM + 16;
   static constexpr int ALLOC = BYTES + 1024;   // slack for 1024-B alignment
 };
 
@@ -133,25 +113,17 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   static_assert(!FP8 || (D == 128 && BF16), "FP8 forward: d = 128, bf16 output");
   using L = FwdSmem<D, FP8 ? 1 : 2>;
   using CFG = FwdCfg<D, FP8>;
-  constexpr int RS = CFG::RS;
-  constexpr int COLS = (((D == 128) && !FP8 && FA2_FWD_HB) ? 64 : 128) / RS;   // S columns per softmax thread
-  constexpr int W_MMA = CFG::SM_WARPS, W_TMA = CFG::SM_WARPS + 1, W_MMA2 = CFG::SM_WARPS + 3;
+  constexpr int COLS = 128;   // S columns per softmax thread (one thread = one row)
+  constexpr int W_MMA = CFG::SM_WARPS, W_TMA = CFG::SM_WARPS + 1;
   constexpr int STAGES = L::STAGES;
   constexpr int NSUB = D * (FP8 ? 1 : 2) / 128;   // 128-B swizzle boxes per tile row
-  constexpr bool HB = (D == 128) && !FP8 && FA2_FWD_HB;   // 64-key blocks
-  constexpr int BN = HB ? 64 : 128;                          // B_c: keys per block
-  constexpr bool SEP_P = (D == 64) || HB;   // P~ in its own TMEM columns
+  constexpr int BN = 128;                  // B_c: keys per block
+  constexpr bool SEP_P = (D == 64);        // P~ in its own TMEM columns
   // TMEM columns of S_i, O_i and (SEP_P) P~_i
-  constexpr uint32_t TS0 = HB ? 2 * D : 0, TS_STEP = BN;
-  constexpr uint32_t TO0 = HB ? 0 : 256;
-  constexpr uint32_t TP0 = HB ? 2 * D + 2 * BN : 256 + 2 * D, TP_STEP = BN / 2;
-  // HB: two P~ buffers per sub-tile (P~ of block j in buffer j % 2), so the softmax of
-  // block j+1 never waits for P~V of block j.  p_full[i][b] / o_done[i][b] hand buffer b
-  // over (written / read); P~V number n of sub-tile i (counted over all tiles) uses
-  // b = n % NPB, so no barrier runs more than one phase ahead of its waiter.
-  constexpr int NPB = HB ? 2 : 1;
-  auto od_bar = [&](uint64_t* od, int i, uint32_t n) { return &od[2 * i + (NPB == 2 ? (n & 1) : 0)]; };
-  auto od_par = [&](uint32_t n) -> uint32_t { return NPB == 2 ? ((n >> 1) & 1) : (n & 1); };
+  constexpr uint32_t TS_STEP = BN, TO0 = 256, TP0 = 256 + 2 * D, TP_STEP = BN / 2;
+  // p_full[i] / o_done[i] hand sub-tile i's P~ over (written / read by P~V number n)
+  auto od_bar = [&](uint64_t* od, int i, uint32_t) { return &od[2 * i]; };
+  auto od_par = [&](uint32_t n) -> uint32_t { return n & 1; };
   // FP8 (P~ over the first 32 columns of S_i): S_{j+1} in two N = 64 halves -- columns
   // 64-127 as soon as the softmax has read S_j (they are not under P~), columns 0-63 after
   // P~V_j -- so half of the next S overlaps the softmax instead of following P~V (+5-11%).
@@ -189,18 +161,18 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       ptx::mbar_init(&q_full[i], 1);
       ptx::mbar_init(&q_empty[i], 1);
       ptx::mbar_init(&s_full[i], 1);
-      ptx::mbar_init(&p_full[2 * i], 4 * RS);
-      ptx::mbar_init(&p_full[2 * i + 1], 4 * RS);
+      ptx::mbar_init(&p_full[2 * i], 4);
+      ptx::mbar_init(&p_full[2 * i + 1], 4);
       ptx::mbar_init(&o_done[2 * i], 1);
       ptx::mbar_init(&o_done[2 * i + 1], 1);
-      ptx::mbar_init(&o_empty[i], 4 * RS);
-      ptx::mbar_init(&s_consumed[i], 4 * RS);
+      ptx::mbar_init(&o_empty[i], 4);
+      ptx::mbar_init(&s_consumed[i], 4);
     }
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&k_full[s], 1);
-      ptx::mbar_init(&k_empty[s], HB ? 2 : 1);
+      ptx::mbar_init(&k_empty[s], 1);
       ptx::mbar_init(&v_full[s], 1);
-      ptx::mbar_init(&v_empty[s], HB ? 2 : 1);
+      ptx::mbar_init(&v_empty[s], 1);
     }
     ptx::fence_mbar_init();
   }
@@ -240,23 +212,16 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 
   if (warp < CFG::SM_WARPS) {
     // ======================= softmax warpgroups =======================
-    // RS = 1: 224*256 + 56*128 == 168*384;  RS = 2: 104*512 + 64*128 == 96*640
-    ptx::setmaxnreg_inc<CFG::REG_SM>();
-    const int wg = warp / (4 * RS);          // sub-tile index
-    const int hf = (warp / 4) % RS;          // column half (RS = 2)
+    ptx::setmaxnreg_inc<CFG::REG_SM>();     // 224*256 + 56*128 == 168*384
+    const int wg = warp / 4;                 // sub-tile index
     const int quad = warp % 4;               // TMEM lane quarter
     const int row = quad * 32 + lane;        // TMEM lane == row within sub-tile
-    const bool lead = hf == 0;               // writes L, zero rows
     const uint32_t lane_base = static_cast<uint32_t>(quad * 32) << 16;
-    const uint32_t tS = tmem + lane_base + TS0 + wg * TS_STEP + hf * COLS;
-    // P~_i: over the first 64 columns of S_i (B_c = 128, d = 128), or its own columns
-    // (d = 64, or B_c = 64: frees S_i for S_{j+1} as soon as it has been read)
-    const uint32_t tP0 = SEP_P ? (tmem + lane_base + TP0 + wg * NPB * TP_STEP + hf * COLS / 2)
-                               : (tmem + lane_base + TS0 + wg * TS_STEP + hf * COLS / 2);
-    const uint32_t tO = tmem + lane_base + TO0 + wg * D + hf * (D / RS);
-    float* red_max = reinterpret_cast<float*>(smem + L::OFF_RED);          // [2][2][2][128]
-    float* red_l = red_max + 2 * 2 * 2 * 128;                              // [2][2][128]
-    const uint32_t bar_id = 1 + wg * 4 + quad;   // named barrier of the two warps sharing these rows
+    const uint32_t tS = tmem + lane_base + wg * TS_STEP;
+    // P~_i: over the first 64 columns of S_i (d = 128), or its own columns (d = 64: frees
+    // S_i for S_{j+1} as soon as it has been read)
+    const uint32_t tP0 = SEP_P ? (tmem + lane_base + TP0 + wg * TP_STEP) : (tmem + lane_base + wg * TS_STEP);
+    const uint32_t tO = tmem + lane_base + TO0 + wg * D;
     uint32_t s_count = 0;   // completed waits on s_full[wg]
     uint32_t pv_count = 0;  // PV MMAs issued so far for this sub-tile (all tiles)
     const float sl2 = p.scale_log2;
@@ -271,11 +236,10 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         // rows that see no key (R23): O = 0, L = -inf; no MMA work was scheduled
         if (grow < sq.nq) {
           uint4* dst = reinterpret_cast<uint4*>(
-              reinterpret_cast<uint8_t*>(p.o) + (sq.bc * p.o_bs + (bh % p.H) * p.o_hs + (sq.q0 + grow) * p.o_rs) * 2) +
-              hf * (D / RS / 8);
+              reinterpret_cast<uint8_t*>(p.o) + (sq.bc * p.o_bs + (bh % p.H) * p.o_hs + (sq.q0 + grow) * p.o_rs) * 2);
 #pragma unroll
-          for (int e = 0; e < D / RS / 8; ++e) dst[e] = make_uint4(0u, 0u, 0u, 0u);
-          if (lead) p.lse[sq.bc * p.l_bs + (bh % p.H) * p.l_hs + sq.q0 + grow] = -INFINITY;
+          for (int e = 0; e < D / 8; ++e) dst[e] = make_uint4(0u, 0u, 0u, 0u);
+          p.lse[sq.bc * p.l_bs + (bh % p.H) * p.l_hs + sq.q0 + grow] = -INFINITY;
         }
         continue;
       }
@@ -283,9 +247,8 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       float l_sum = 0.f;
       for (int j = 0; j < nb; ++j) {
         ptx::mbar_wait(&s_full[wg], s_count & 1);
-        const int par = s_count & 1;
         ++s_count;
-        if (threadIdx.x % (128 * RS) == 0 && n == 0) FA2_TRACE(0, wg, j);
+        if (threadIdx.x % 128 == 0 && n == 0) FA2_TRACE(0, wg, j);
         ptx::tc_fence_after();
         uint32_t su[COLS];
 #pragma unroll
@@ -306,7 +269,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           const int lim = CAUSAL ? min(sq.nk - 1, grow + sq.off) : (sq.nk - 1);
 #pragma unroll
           for (int c = 0; c < COLS; ++c)
-            if (c0 + hf * COLS + c > lim) s[c] = -INFINITY;
+            if (c0 + c > lim) s[c] = -INFINITY;
         }
         // row max: a tree of 3-input maxima at d = 128 (+1.5% causal bf16, +3.5% FP8 on B200),
         // the serial FMNMX3 chain at d = 64 (the tree's temporaries cost it 10%)
@@ -318,15 +281,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
 #pragma unroll
           for (int c = 1; c < COLS; ++c) mx = fmaxf(mx, s[c]);
         }
-        if constexpr (RS == 2) {
-          // the row's other half lives in the partner warp (same lanes, other columns)
-          float* mine = red_max + ((par * 2 + wg) * 2 + hf) * 128;
-          float* other = red_max + ((par * 2 + wg) * 2 + (hf ^ 1)) * 128;
-          mine[row] = mx;
-          ptx::named_bar_sync(bar_id, 64);
-          mx = fmaxf(mx, other[row]);
-        }
-        if (threadIdx.x % (128 * RS) == 0 && n == 0) FA2_TRACE(1, wg, j);
+        if (threadIdx.x % 128 == 0 && n == 0) FA2_TRACE(1, wg, j);
         const float m_new = fmaxf(m_used, mx * sl2);
         const bool rescale = (m_new - m_used) > 8.0f;   // also true when m_used == -inf and m_new finite
         float alpha = 1.f;
@@ -339,18 +294,17 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         float2 rs2 = make_float2(0.f, 0.f);
         // exponent x = s * scale * log2(e) - m (FFMA2), P~ = 2^x.  On unmasked blocks
         // EMU of every 16 column pairs use the FMA-pipe polynomial, the rest MUFU.EX2.
-        // SEP_P: the P buffer is free once the previous P~V MMA of this sub-tile completed
-        // (HB: the buffer this block writes was last read by P~V number pv_count - 2).  The
+        // SEP_P: the P buffer is free once the previous P~V MMA of this sub-tile completed.  The
         // exponentials do not need it: they are computed into registers first and the wait
         // comes right before the first TMEM store, so they overlap that P~V (d = 64: the exp
         // phase was 2270 cycles per block with the wait in front, ~MUFU-bound 1300 after)
         auto wait_p_free = [&]() {
           if constexpr (SEP_P) {
-            if (pv_count >= (uint32_t)NPB) ptx::mbar_wait(od_bar(o_done, wg, pv_count - NPB), od_par(pv_count - NPB));
+            if (pv_count >= 1) ptx::mbar_wait(od_bar(o_done, wg, pv_count - 1), od_par(pv_count - 1));
             ptx::tc_fence_after();
           }
         };
-        const uint32_t tP = tP0 + (pv_count % NPB) * TP_STEP;
+        const uint32_t tP = tP0;
         auto exp_block = [&](auto emu_tag) {
           constexpr int EMU = decltype(emu_tag)::value;
           uint32_t pk_all[COLS / 32][16];
@@ -389,14 +343,14 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         if (need_mask) exp_block(std::integral_constant<int, 0>{});
         else exp_block(std::integral_constant<int, D == 64 ? kFwdEmuPairsD64 : kFwdEmuPairs>{});
         l_sum = l_sum * alpha + (rs2.x + rs2.y);
-        if (threadIdx.x % (128 * RS) == 0 && n == 0) FA2_TRACE(2, wg, j);
+        if (threadIdx.x % 128 == 0 && n == 0) FA2_TRACE(2, wg, j);
         // Rescale the un-normalised O accumulator before P~_j V_j is added
         // (needs PV_{j-1} finished; it was issued before S_j, so it usually is).
         if (j > 0 && __any_sync(0xffffffffu, rescale)) {
           ptx::mbar_wait(od_bar(o_done, wg, pv_count - 1), od_par(pv_count - 1));
           ptx::tc_fence_after();
 #pragma unroll
-          for (int ch = 0; ch < D / RS / 32; ++ch) {
+          for (int ch = 0; ch < D / 32; ++ch) {
             uint32_t o[32];
             ptx::tmem_ld_x32(tO + ch * 32, o);
             ptx::tmem_wait_ld();
@@ -409,26 +363,19 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(od_bar(p_full, wg, pv_count));
-        if (threadIdx.x % (128 * RS) == 0 && n == 0) FA2_TRACE(3, wg, j);
+        if (threadIdx.x % 128 == 0 && n == 0) FA2_TRACE(3, wg, j);
         ++pv_count;
       }
       // ---- epilogue: O = O / l, L = m + log l (natural log) ----
       ptx::mbar_wait(od_bar(o_done, wg, pv_count - 1), od_par(pv_count - 1));
       ptx::tc_fence_after();
-      if constexpr (RS == 2) {   // l of the whole row: both halves' partial sums
-        float* mine = red_l + (wg * 2 + hf) * 128;
-        mine[row] = l_sum;
-        ptx::named_bar_sync(bar_id, 64);
-        l_sum += red_l[(wg * 2 + (hf ^ 1)) * 128 + row];
-        ptx::named_bar_sync(bar_id, 64);   // both read before the next tile's writes
-      }
       float inv_l = l_sum > 0.f ? 1.f / l_sum : 0.f;   // rows that saw no key: O = 0 (R23)
       if constexpr (FP8) inv_l *= p.o_descale;
       uint8_t* orow = reinterpret_cast<uint8_t*>(p.o) +
                       (GEN ? (sq.bc * p.o_bs + (bh % p.H) * p.o_hs + (sq.q0 + grow) * p.o_rs)
-                           : (static_cast<size_t>(bh) * sq.nq + grow) * D) * 2 + hf * (D / RS) * 2;
+                           : (static_cast<size_t>(bh) * sq.nq + grow) * D) * 2;
 #pragma unroll
-      for (int ch = 0; ch < D / RS / 32; ++ch) {
+      for (int ch = 0; ch < D / 32; ++ch) {
         uint32_t o[32];
         ptx::tmem_ld_x32(tO + ch * 32, o);
         ptx::tmem_wait_ld();
@@ -442,7 +389,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           for (int e = 0; e < 4; ++e) dst[e] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
         }
       }
-      if (grow < sq.nq && lead)
+      if (grow < sq.nq)
         p.lse[GEN ? sq.bc * p.l_bs + (bh % p.H) * p.l_hs + sq.q0 + grow : static_cast<size_t>(bh) * sq.nq + grow] = l_sum > 0.f ? (m_used + ptx::lg2(l_sum)) * 0.69314718055994531f : -INFINITY;
       ptx::tc_fence_before();
       __syncwarp();
@@ -450,13 +397,9 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     }
   } else {
     ptx::setmaxnreg_dec<CFG::REG_OTHER>();
-    if (warp == W_MMA || (HB && warp == W_MMA2)) {
+    if (warp == W_MMA) {
       // ================== MMA issuer: whole warp, one elected lane issues ==================
-      // HB: one issuer warp per sub-tile (me), so each sub-tile's S_{j+1} goes into the
-      // tensor pipe as soon as its own softmax has read S_j, independent of the other
-      // sub-tile's progress (a single in-order issuer serialises the two chains: 2380 ->
-      // 1785 cycles per 64-key block).  Otherwise one warp issues for both (me = 0).
-      const int me = warp == W_MMA ? 0 : 1;
+      const int me = 0;
       // (E4M3 has format code 0 in the kind::f8f6f4 descriptor, as F16 in kind::f16)
       constexpr uint32_t IDESC_S = ptx::idesc_f16(FP8 ? false : BF16, 128, 128, false, false);
       constexpr uint32_t IDESC_O = ptx::idesc_f16(FP8 ? false : BF16, 128, D, false, true);
@@ -469,7 +412,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       uint32_t p_count0 = 0, p_count1 = 0, o_uses0 = 0, o_uses1 = 0;
       int it = 0;
       constexpr uint32_t IDESC_S64 = ptx::idesc_f16(FP8 ? false : BF16, 128, 64, false, false);
-      auto mma_s = [&](int i, int slot, int sub = 0) {
+      auto mma_s = [&](int i, int slot) {
         // K steps of 32 bytes (16 bf16/fp16 or 32 E4M3 elements), 4 per 128-B swizzle box
 #pragma unroll
         for (int k = 0; k < D * (FP8 ? 1 : 2) / 32; ++k) {
@@ -477,9 +420,6 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           if constexpr (FP8)
             ptx::mma_ss_f8(tmem + i * 128, dQ + ((i * L::TILE + off) >> 4), dK + ((slot * L::TILE + off) >> 4),
                            IDESC_S, k > 0 ? 1u : 0u);
-          else if constexpr (HB)   // block sub of the stage: key rows [64 sub, 64 sub + 64) -> S_i (N = 64)
-            ptx::mma_ss(tmem + TS0 + i * TS_STEP, dQ + ((i * L::TILE + off) >> 4),
-                        dK + ((slot * L::TILE + off + sub * 64 * 128) >> 4), IDESC_S64, k > 0 ? 1u : 0u);
           else
             ptx::mma_ss(tmem + i * 128, dQ + ((i * L::TILE + off) >> 4), dK + ((slot * L::TILE + off) >> 4), IDESC_S,
                         k > 0 ? 1u : 0u);
@@ -499,7 +439,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
                         k > 0 ? 1u : 0u);
         }
       };
-      auto mma_pv = [&](int i, int slot, bool acc, int sub = 0, int pb = 0) {
+      auto mma_pv = [&](int i, int slot, bool acc) {
         // K = 128 keys: 8 steps of 16 (P~ 16-bit: 8 TMEM columns, V rows 16 x 128 B) or
         // 4 steps of 32 (P~ E4M3: 8 TMEM columns, V rows 32 x 128 B)
         if constexpr (FP8) {
@@ -510,18 +450,18 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         } else {
 #pragma unroll
           for (int k = 0; k < BN / 16; ++k)
-            ptx::mma_ts(tmem + TO0 + i * D, tmem + (SEP_P ? TP0 + (i * NPB + pb) * TP_STEP : i * 128) + k * 8,
-                        dV + ((slot * L::TILE + sub * 64 * 128 + k * 2048) >> 4), IDESC_O, (acc || k > 0) ? 1u : 0u);
+            ptx::mma_ts(tmem + TO0 + i * D, tmem + (SEP_P ? TP0 + i * TP_STEP : i * 128) + k * 8,
+                        dV + ((slot * L::TILE + k * 2048) >> 4), IDESC_O, (acc || k > 0) ? 1u : 0u);
         }
       };
       uint32_t s_iss01[2] = {0, 0};   // SEP_P: S MMAs issued per sub-tile (s_consumed phases)
       uint32_t p_cnt01[2] = {0, 0}, o_use01[2] = {0, 0};   // SEP_P: P~V MMAs / tiles per sub-tile
       uint32_t sc_count0 = 0, sc_count1 = 0;   // d = 128 SPLIT_S: s_consumed phases waited per sub-tile
       // d = 64: S_i into its buffer once softmax i has read the previous S_i
-      auto issue_s_sep = [&](int i, uint32_t& s_iss, int sub) {
+      auto issue_s_sep = [&](int i, uint32_t& s_iss) {
         if (s_iss > 0) ptx::mbar_wait(&s_consumed[i], (s_iss - 1) & 1);
         ptx::tc_fence_after();
-        if (ptx::elect_one()) { mma_s(i, kslot, sub); ptx::mma_commit(&s_full[i]); }
+        if (ptx::elect_one()) { mma_s(i, kslot); ptx::mma_commit(&s_full[i]); }
         __syncwarp();
         ++s_iss;
       };
@@ -532,39 +472,32 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         const int nb0 = n_blocks(sq, mb, 0), nb1 = n_blocks(sq, mb, 1);
         const int nkv = max(nb0, nb1);
         if constexpr (SEP_P) {
-          // sub-tiles [i0, i1] of this issuer; HB: every K/V stage is waited for and
-          // released by both issuers (k/v_empty count 2)
-          const int i0 = HB ? me : 0, i1 = HB ? me : 1;
+          const int i0 = 0, i1 = 1;
           uint32_t* s_iss = s_iss01;
           uint32_t* p_cnt = p_cnt01;
           uint32_t* o_use = o_use01;
           for (int i = i0; i <= i1; ++i) ptx::mbar_wait(&q_full[i], it & 1);
           // S_{j+1} is issued as soon as S_j has been read (P~ has its own buffer),
           // so the next block's scores are ready when the softmax finishes block j.
-          // HB: a TMA stage holds two 64-key blocks (sub = j & 1); it is waited for at its
-          // first block and released after its last one
           for (int j = -1; j < nkv; ++j) {
             if (j + 1 < nkv) {
-              const int jn = j + 1, subn = HB ? (jn & 1) : 0;
-              if (subn == 0) ptx::mbar_wait(&k_full[kslot], kphase);
+              const int jn = j + 1;
+              ptx::mbar_wait(&k_full[kslot], kphase);
               if (it == 0) FA2_TRACE(4, me, jn);
               for (int i = i0; i <= i1; ++i) {
                 const int nbi = i == 0 ? nb0 : nb1;
-                if (jn < nbi) issue_s_sep(i, s_iss[i], subn);
+                if (jn < nbi) issue_s_sep(i, s_iss[i]);
                 if (jn + 1 == nbi) {   // Q_i's last S: release Q_i for the next tile
                   if (ptx::elect_one()) ptx::mma_commit(&q_empty[i]);
                   __syncwarp();
                 }
               }
-              if (!HB || subn == 1 || jn + 1 == nkv) {
-                if (ptx::elect_one()) ptx::mma_commit(&k_empty[kslot]);
-                __syncwarp();
-                if (++kslot == STAGES) { kslot = 0; kphase ^= 1; }
-              }
+              if (ptx::elect_one()) ptx::mma_commit(&k_empty[kslot]);
+              __syncwarp();
+              if (++kslot == STAGES) { kslot = 0; kphase ^= 1; }
             }
             if (j < 0) continue;
-            const int sub = HB ? (j & 1) : 0;
-            if (sub == 0) ptx::mbar_wait(&v_full[vslot], vphase);
+            ptx::mbar_wait(&v_full[vslot], vphase);
             auto pv = [&](int i, int nbi) {
               if (j >= nbi) return;
               if (j == 0) {
@@ -574,16 +507,14 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
               const uint32_t n = p_cnt[i]++;
               ptx::mbar_wait(od_bar(p_full, i, n), od_par(n));
               ptx::tc_fence_after();
-              if (ptx::elect_one()) { mma_pv(i, vslot, j > 0, sub, n % NPB); ptx::mma_commit(od_bar(o_done, i, n)); }
+              if (ptx::elect_one()) { mma_pv(i, vslot, j > 0); ptx::mma_commit(od_bar(o_done, i, n)); }
               __syncwarp();
             };
             for (int i = i0; i <= i1; ++i) pv(i, i == 0 ? nb0 : nb1);
             if (it == 0) FA2_TRACE(5, me, j);
-            if (!HB || sub == 1 || j + 1 == nkv) {
-              if (ptx::elect_one()) ptx::mma_commit(&v_empty[vslot]);
-              __syncwarp();
-              if (++vslot == STAGES) { vslot = 0; vphase ^= 1; }
-            }
+            if (ptx::elect_one()) ptx::mma_commit(&v_empty[vslot]);
+            __syncwarp();
+            if (++vslot == STAGES) { vslot = 0; vphase ^= 1; }
           }
           if (ptx::elect_one())   // sub-tiles without key blocks release Q_i here
             for (int i = i0; i <= i1; ++i)
@@ -691,7 +622,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         Seq sq;
         decode(t, bh, mb, sq);
         const int nblk = max(n_blocks(sq, mb, 0), n_blocks(sq, mb, 1));
-        const int nkv = HB ? (nblk + 1) / 2 : nblk;   // 128-row K/V stages
+        const int nkv = nblk;   // 128-row K/V stages
         // key/value head of this query head: implicit index manipulation
         const int h = bh % p.H, kvh = h / p.group;
         if (is_k) {
