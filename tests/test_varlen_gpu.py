@@ -99,14 +99,16 @@ def test_varlen_parity(case, d, causal, dtype):
     _grads_ok((dq, dk, dv), (gq, gk, gv), dtype)
 
 
+@pytest.mark.parametrize("d", [64, 128])
 @pytest.mark.parametrize("causal", [False, True])
-def test_varlen_equal_lengths_match_fixed_layout(causal):
+def test_varlen_equal_lengths_match_fixed_layout(causal, d):
     """Equal lengths: the packed path computes what the [B,H,N,d] path does.  Causal:
-    the same kernel, forward bitwise.  Non-causal d=128: the fixed layout runs the
-    CTA-pair forward, whose exponential split (2 of 16 pairs on the FMA pipe instead of
-    4) rounds P~ differently, so forward to within a bf16 rounding step.  Backward up to
-    the dQ summation order (and the forward difference)."""
-    B, H, N, d = 3, 2, 300, 128
+    the same one-SM forward kernel, forward bitwise.  Non-causal d = 128: the fixed
+    layout runs the CTA-pair forward, whose exponential split (2 of 16 pairs on the FMA
+    pipe instead of 4) and key-block split over the pair round P~ differently, so forward
+    to within a bf16 rounding step (d = 64: same kernel, compared the same way).  Backward
+    up to the dQ summation order (and the forward difference)."""
+    B, H, N = 3, 2, 300
     q, k, v, do = W.qkv(B, H, N, d, "bf16", seed=320)
     qc, kc, vc, doc = q.cuda(), k.cuda(), v.cuda(), do.cuda()
     o, lse = fa2.forward(qc, kc, vc, causal=causal)
