@@ -73,8 +73,9 @@ FA2_API fa2_status_t fa2_forward(const void* q, const void* k, const void* v, vo
 
 /* Bytes of device scratch fa2_backward needs: the fp32 dQ accumulator
  * [B,H,N_pad,d], D [B,H,N_pad] and L*log2(e) [B,H,N_pad] (fp32), where N_pad is
- * N rounded up to a multiple of 128, plus [B,H,N_pad/128] int32 dQ-tile
- * counters (used by fa2_backward_deterministic), rounded up to 16 bytes -- the
+ * N rounded up to a multiple of 128, plus [B,H,N_pad/32] int32 dQ-tile
+ * counters (4 per 128-row tile, used by fa2_backward_deterministic), rounded up
+ * to 16 bytes -- the
  * minimum -- plus, 256-byte aligned, 2*B*H*N*d fp32 for the GQA load-balance
  * split (fp32 dK, dV partial sums when the query heads of a key/value group are
  * spread over several CTAs; used only when H_kv < H, not deterministic, and the
@@ -156,8 +157,9 @@ FA2_API fa2_status_t fa2_forward_fp8(const void* q, const void* k, const void* v
  * arguments.  Alg. 2 accumulates dQ_i += dS_ij K_j into HBM from every key block
  * j with atomic adds, so the fp32 summation order -- and
  * the last bits of dQ -- follow arrival order.  Here every dQ tile (query head,
- * 128-row query tile) takes its key blocks' contributions in one fixed order,
- * serialised by a counter per tile in the workspace; the arithmetic is otherwise
+ * 128-row query tile; in the CTA-pair d = 128 kernel each query half and d half
+ * of it) takes its key blocks' contributions in one fixed order, serialised by
+ * counters in the workspace; the arithmetic is otherwise
  * identical (dK, dV are accumulated on chip in a fixed order in both modes).
  * Slower than fa2_backward_gqa by the waits on those counters. */
 FA2_API fa2_status_t fa2_backward_deterministic(const void* q, const void* k, const void* v, const void* o,

@@ -482,7 +482,7 @@ size_t pad128(long long N) { return static_cast<size_t>((N + 127) / 128) * 128; 
 size_t round16(size_t b) { return (b + 15) / 16 * 16; }
 
 // Backward workspace (both layouts), in this order:
-//   dq_acc [rows, d] fp32 | D [rows] fp32 | L*log2e [rows] fp32 | counters [rows/128] int32 |
+//   dq_acc [rows, d] fp32 | D [rows] fp32 | L*log2e [rows] fp32 | counters [rows/32] int32 |
 //   tile_off [B+1] int32 (packed only)
 // rows = padded query rows: fixed B*H*N_pad; packed H * pad128(T_q + 127 B) (every sequence is
 // padded to whole 128-row tiles, fa2_bwd_sm100.cuh RowParams).
@@ -503,7 +503,7 @@ WsLayout ws_layout(const Geom& g) {
   w.dvec = w.dq + static_cast<size_t>(w.rows) * g.d * 4;
   w.lse2 = w.dvec + static_cast<size_t>(w.rows) * 4;
   w.sem = w.lse2 + static_cast<size_t>(w.rows) * 4;
-  w.tile = w.sem + round16(static_cast<size_t>(w.rows / 128) * 4);
+  w.tile = w.sem + round16(static_cast<size_t>(w.rows / 32) * 4);   // 4 counters per 128-row tile
   w.total = w.tile + (g.packed ? round16(static_cast<size_t>(g.B + 1) * 4) : 0);
   return w;
 }
@@ -632,10 +632,20 @@ fa2_status_t launch_bwd_pair(const fa2::BwdMaps& maps, const CUtensorMap& mq64, 
   p.num_n_blocks = (N + 255) / 256;
   p.num_tiles = (p.BH / p.group) * p.num_n_blocks;
   int npairs = std::min(p.num_tiles, std::min(sms / 2, max_active_pairs(kern, smem, fa2::kBwdThreads, sms)));
+  if (p.dq_sem != nullptr) {
+    // deterministic mode (fa2_bwd2_sm100.cuh pair_q_tile / pair_rank): the cyclic order needs an
+    // even number of query tiles and a head's key blocks side by side, i.e. a pair grid that is
+    // a multiple of them
+#ifndef FA2_DET_CYCLIC_PAIR
+#define FA2_DET_CYCLIC_PAIR 1
+#endif
+    p.det_cyclic = (FA2_DET_CYCLIC_PAIR && p.num_n_blocks <= npairs && ((N + 127) / 128) % 2 == 0) ? 1 : 0;
+    if (p.det_cyclic) npairs = (npairs / p.num_n_blocks) * p.num_n_blocks;
+  }
   fa2::SchedT<CAUSAL> sched;
   sched.n = 0;
   if constexpr (CAUSAL) {   // balanced pair-tile lists: key block nb2 sees nqb - 2 nb2 query tiles per head
-    if (FA2_SCHED && p.num_tiles <= fa2::kSchedMaxTiles && npairs <= fa2::kSchedMaxCtas) {
+    if (FA2_SCHED && p.dq_sem == nullptr && p.num_tiles <= fa2::kSchedMaxTiles && npairs <= fa2::kSchedMaxCtas) {
       const int nnb2 = p.num_n_blocks, group = p.group, nt = p.num_tiles;
       const SchedPtr sc = cached_sched(2, nt, nnb2, N, group, npairs, [&](std::vector<int>& work) {
         const int nqb = (N + 127) / 128;
@@ -744,7 +754,7 @@ fa2_status_t backward_impl(const void* q, const void* k, const void* v, const vo
   // path; FA2_BWD_PAIR=0 in the environment selects the one-SM kernel instead (A/B runs and
   // the one-SM kernel's parity test)
   static const bool pair_env = [] { const char* e = std::getenv("FA2_BWD_PAIR"); return !(e && e[0] == '0'); }();
-  const bool pair = FA2_BWD_PAIR && pair_env && g.d == 128 && !g.packed && g.Nq == g.Nk && !deterministic && hsplit == 1;
+  const bool pair = FA2_BWD_PAIR && pair_env && g.d == 128 && !g.packed && g.Nq == g.Nk && hsplit == 1;
   if (pair) {
     CUtensorMap mq64, mdo64;
     if ((s = make_rows_map(&mq64, q, dt, g, g.H, true, 2, 64)) != FA2_OK) return s;

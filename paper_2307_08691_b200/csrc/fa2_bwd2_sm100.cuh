@@ -107,12 +107,39 @@ FA2_DEVICE PairTile pair_tile(const BwdParams& p, bool causal, int t) {
   PairTile w;
   const int bh = t / p.num_n_blocks;
   w.nb2 = t % p.num_n_blocks;
+  // deterministic cyclic causal: alternate heavy / light key blocks between the grid's rounds
+  // (all key blocks of a head run in the same round, so this only permutes them over pairs)
+  if (causal && p.dq_sem != nullptr && p.det_cyclic && ((t / static_cast<int>(gridDim.x / 2)) & 1))
+    w.nb2 = p.num_n_blocks - 1 - w.nb2;
   w.b = bh / p.Hkv;
   w.kvh = bh % p.Hkv;
   const int nqb = (p.geom.Nq + 127) / 128;
   w.i0 = causal ? 2 * w.nb2 : 0;   // first query tile that sees key 256 nb2 (CTA 0's first key)
   w.nqt = nqb - w.i0;
   return w;
+}
+// Deterministic mode (R21, §6.4): every dQ half-tile (query head,
+// query tile i, query half r, d half) receives the pair key blocks' contributions in a fixed
+// order, enforced by its own counter (4 per 128-row tile).  Key blocks are 256 rows, query
+// tiles 128, so a head has T_r = 2 T_c2 query tiles.
+//   det_cyclic (T_r even and the head's key blocks fit the pair grid, which is then a
+//   multiple of them, so they run side by side):
+//     non-causal: step s visits query tile i = (2 nb2 + s) mod T_r; tile i is visited by
+//     key block nb2 at s = (i - 2 nb2) mod T_r, one of every other step, so rank = s / 2
+//     and the predecessor of (nb2, s) is (nb2 + 1, s - 2);
+//     causal: i = 2 nb2 + s (from the first tile that sees the block), rank = i / 2 - nb2
+//     (descending key blocks), predecessor (nb2 + 1, s - 2).
+//     The waits point to a neighbour's earlier step: no skew accumulates.
+//   otherwise: i = i0 + s, rank = nb2 (ascending key blocks: every wait points to a lower
+//   work tile, so progress is guaranteed).
+FA2_DEVICE int pair_q_tile(const BwdParams& p, bool causal, const PairTile& w, int s) {
+  if (causal || p.dq_sem == nullptr || !p.det_cyclic) return w.i0 + s;
+  const int nqb = w.nqt, i = 2 * w.nb2 + s;   // non-causal: every query tile, nqb even
+  return i < nqb ? i : i - nqb;
+}
+FA2_DEVICE int pair_rank(const BwdParams& p, bool causal, const PairTile& w, int i, int s) {
+  if (!p.det_cyclic) return w.nb2;
+  return causal ? (i >> 1) - w.nb2 : (s >> 1);
 }
 
 template <bool BF16, bool CAUSAL>
@@ -242,7 +269,7 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
       const int kv_row = w.nb2 * 256 + static_cast<int>(rank) * 128 + r;
       const int nx = w.nqt * p.group;
       for (int x = 0; x < nx; ++x, ++g) {
-        const int i = w.i0 + x % w.nqt;
+        const int i = pair_q_tile(p, CAUSAL, w, x % w.nqt);
         const uint32_t slot = g & 1;
         const uint32_t vL2 = sVec_a + slot * 2 * BM * 4 + c0 * 4, vD = vL2 + BM * 4;
         // mask: causal tiles crossing the diagonal and the ragged key tail (query rows past N
@@ -411,11 +438,15 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
       const PairTile w = pair_tile(p, CAUSAL, t);
       const int nx = w.nqt * p.group;
       for (int x = 0; x < nx; ++x, ++g) {
-        const int i = w.i0 + x % w.nqt;
+        const int i = pair_q_tile(p, CAUSAL, w, x % w.nqt);
         const int hq = w.kvh * p.group + x / w.nqt;
         // this CTA's 32 KB of the tile (query rows [64 rank, +64)), this d half's 16 KB
         float* const acc = p.dq_acc + ((static_cast<long long>(w.b) * p.H + hq) * p.acc_hs + static_cast<long long>(i) * BM) * D +
                            (rank * 32 + dh * 16) * 256;
+        // deterministic mode: this d half's counter of the dQ half-tile (see pair_rank)
+        int* const sem = p.dq_sem == nullptr ? nullptr
+            : p.dq_sem + (((static_cast<long long>(w.b) * p.H + hq) * p.acc_hs) / 128 + i) * 4 + rank * 2 + dh;
+        const int drank = pair_rank(p, CAUSAL, w, i, x % w.nqt);
         ptx::mbar_wait(dq_full, g & 1);
         if (leader) FA2_BTRACE(9, g);
         ptx::tc_fence_after();
@@ -427,6 +458,7 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
         __syncwarp();
         if (lane == 0) pair::arrive_remote(dq_empty, 0);
         if (leader) FA2_BTRACE(10, g);
+        if (sem != nullptr && issuer) dq_sem_wait(sem, drank);   // the previous contribution landed
 #pragma unroll
         for (int rd = 0; rd < 2; ++rd) {
           if (issuer) ptx::bulk_wait_read<0>();          // the staging buffer's last round was read
@@ -446,6 +478,9 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
             ptx::bulk_commit();
           }
         }
+        // complete, then rank + 1 (deferring the release to the next step measured slower:
+        // 773 -> 651 TFLOP/s non-causal, 676 -> 529 causal)
+        if (sem != nullptr && issuer) dq_sem_release(sem, drank);
         if (leader) FA2_BTRACE(16, g);
       }
     }
@@ -567,6 +602,9 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
             pair::wait_cluster(s_consumed, (x + 1) & 1);
           }
           FA2_BTRACE(8, x);
+          // dQ(x) lands where dQ(x-1) was: its read-out was waited for before S^T(x+1) --
+          // except at the tile's last step, where no S^T follows
+          if (x + 1 == end && x > g0) pair::wait_cluster(dq_empty, (x - 1) & 1);
           issue_dq(x);
           FA2_BTRACE(5, x);
           if (x + 1 < end) {
@@ -614,7 +652,7 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
         }
         const int nx = w.nqt * p.group;
         for (int x = 0; x < nx; ++x, ++g) {
-          const int i = w.i0 + x % w.nqt;
+          const int i = pair_q_tile(p, CAUSAL, w, x % w.nqt);
           const int hq = w.kvh * p.group + x / w.nqt;
           const int bhq = w.b * p.H + hq;
           const uint32_t slot = g & 1;

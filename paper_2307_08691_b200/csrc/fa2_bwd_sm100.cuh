@@ -159,7 +159,8 @@ FA2_DEVICE int bwd_q_tile(const BwdParams& p, bool causal, const BwdTile& w, int
 // tile in the ascending one, so the wait graph is acyclic and every CTA progresses.
 // (Finer-grained counters per part of a tile, with deferred releases, were measured
 // slower: tools/bench_det.py.)
-FA2_DEVICE int* dq_sem_ptr(const BwdParams& p, long long acc_row0, int i) { return p.dq_sem + acc_row0 / 128 + i; }
+// 4 counters per 128-row dQ tile (the CTA-pair kernel uses one per query half and d half)
+FA2_DEVICE int* dq_sem_ptr(const BwdParams& p, long long acc_row0, int i) { return p.dq_sem + (acc_row0 / 128 + i) * 4; }
 FA2_DEVICE int dq_rank(const BwdParams& p, int nb, int s) { return p.det_cyclic ? s : nb; }
 FA2_DEVICE void dq_sem_wait(const int* sem, int rank) {
   while (ptx::ld_acquire_gpu(sem) != rank) {
@@ -292,7 +293,7 @@ __global__ void __launch_bounds__(256) fa2_bwd_preprocess(const RowParams p) {
       const float l = real ? p.lse[l_off] : INFINITY;
       p.lse2[R] = l == -INFINITY ? INFINITY : l * 1.4426950408889634f;
     }
-    if (p.dq_sem != nullptr && R % 128 == 0) p.dq_sem[R / 128] = 0;
+    if (p.dq_sem != nullptr && R % 32 == 0) p.dq_sem[R / 32] = 0;   // 4 counters per 128-row tile
   }
   if (p.dq_acc != nullptr) {
     float4* z = reinterpret_cast<float4*>(p.dq_acc + R * D + sub * 8);

@@ -73,7 +73,7 @@ def test_forward_validation(L):
 def test_backward_validation(L):
     ws = L.fa2_backward_workspace_size(2, 3, 100, 64)
     npad = 128
-    sem = (2 * 3 * (npad // 128) * 4 + 15) // 16 * 16
+    sem = (2 * 3 * (npad // 32) * 4 + 15) // 16 * 16   # 4 counters per 128-row tile
     base = 2 * 3 * npad * 64 * 4 + 2 * 2 * 3 * npad * 4 + sem
     # + room for the GQA split's fp32 dK/dV accumulators (256-byte aligned)
     assert ws == (base + 255) // 256 * 256 + 2 * 3 * 100 * 64 * 8
@@ -166,7 +166,7 @@ def test_rectangular_and_varlen_validation(L):
     B, H, T, d = 3, 4, 1000, 64
     rows = H * (-(-(T + 127 * B) // 128) * 128)
     r16 = lambda x: (x + 15) // 16 * 16
-    want = rows * d * 4 + 2 * rows * 4 + r16(rows // 128 * 4) + r16((B + 1) * 4)
+    want = rows * d * 4 + 2 * rows * 4 + r16(rows // 32 * 4) + r16((B + 1) * 4)
     assert L.fa2_backward_varlen_workspace_size(B, H, T, d) == (want + 255) // 256 * 256 + T * H * d * 8
     ws = ctypes.c_void_p(1 << 20)
     bv = lambda nbytes, *a: L.fa2_backward_varlen(*p[:9], cu, cu, ws, nbytes, *a)

@@ -69,10 +69,12 @@ def test_deterministic_bitwise(causal, d):
         assert rel <= 2 ** -6, rel
 
 
-def test_deterministic_fallback_schedule():
-    """N = 149*128: 149 key blocks > 148 SMs -> the ascending-order schedule.  Bitwise
-    repeatable, and sampled dQ rows match the oracle."""
-    B, H, N, d = 1, 1, 149 * 128, 64
+@pytest.mark.parametrize("d", [64, 128])
+def test_deterministic_fallback_schedule(d):
+    """N = 149*128: 149 key blocks > 148 SMs (d = 64, one-SM kernel) and 75 key-block pairs
+    > 74 CTA pairs (d = 128, CTA-pair kernel) -> the ascending-order schedule.  Bitwise
+    repeatable, and sampled rows match the oracle."""
+    B, H, N = 1, 1, 149 * 128
     q, k, v, do = W.qkv(B, H, N, d, "bf16", seed=31)
     sc = scale_for(d)
     runs = _fwd_bwd(q, k, v, do, True, sc, True, reps=2)
@@ -83,9 +85,8 @@ def test_deterministic_fallback_schedule():
     f64 = lambda t: t.double().numpy()
     sm = R.backward_sampled_head(f64(q[0, 0]), f64(k[0, 0]), f64(v[0, 0]), f64(do[0, 0]), sc, True,
                                  dq_rows=rows, dkv_cols=rows, rows_per_chunk=1024)
-    floor = 2.0 ** -8 * max(float(np.max(np.abs(sm[x]))) for x in ("dq", "dk", "dv"))
     got = {"dq": dq[0, 0, rows], "dk": dk[0, 0, rows], "dv": dv[0, 0, rows]}
-    for x in ("dq", "dk", "dv"):
+    for x in ("dq", "dk", "dv"):   # not degenerate: plain rule R15
         err = float(np.max(np.abs(got[x].double().cpu().numpy() - sm[x])))
-        lim = TOL["bf16"]["grad"] * max(float(np.max(np.abs(sm[x]))), floor)
+        lim = TOL["bf16"]["grad"] * float(np.max(np.abs(sm[x])))
         assert err <= lim, (x, err, lim)
