@@ -285,16 +285,19 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
         const float2 sl2x2 = make_float2(sl2, sl2);
         auto p_block = [&](auto emu_tag) {
           constexpr int EMU = decltype(emu_tag)::value;
+          // both 32-column chunks of S^T in one round trip (tcgen05.wait::ld waits for all)
+          uint32_t sva[64];
+          ptx::tmem_ld_x32(tmem + lane_base + T_S + c0, sva);
+          ptx::tmem_ld_x32(tmem + lane_base + T_S + c0 + 32, sva + 32);
+          ptx::tmem_wait_ld();
+          if (wg == 1) {   // S^T cols [64,128) are in registers: dQ(x-1) may land there
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) pair::arrive_remote(s_consumed, 0);
+          }
 #pragma unroll
           for (int ch = 0; ch < 2; ++ch) {
-            uint32_t sv[32];
-            ptx::tmem_ld_x32(tmem + lane_base + T_S + c0 + ch * 32, sv);
-            ptx::tmem_wait_ld();
-            if (ch == 1 && wg == 1) {   // S^T cols [64,128) are in registers: dQ(x-1) may land there
-              ptx::tc_fence_before();
-              __syncwarp();
-              if (lane == 0) pair::arrive_remote(s_consumed, 0);
-            }
+            const uint32_t* sv = sva + ch * 32;
 #pragma unroll
             for (int e4 = 0; e4 < 8; ++e4) {
               const float4 l4 = ptx::lds_v4f(vL2 + (ch * 32 + e4 * 4) * 4);
