@@ -180,11 +180,14 @@ fa2_bwd128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constan
         const float2 sl2x2 = make_float2(p.scale_log2, p.scale_log2);
         auto p_block = [&](auto emu_tag) {
           constexpr int EMU = decltype(emu_tag)::value;
+          // both 32-column chunks of S^T in one TMEM round trip (tcgen05.wait::ld waits for all)
+          uint32_t sva[64];
+          ptx::tmem_ld_x32(tmem + lane_base + T_S + c0, sva);
+          ptx::tmem_ld_x32(tmem + lane_base + T_S + c0 + 32, sva + 32);
+          ptx::tmem_wait_ld();
 #pragma unroll
           for (int ch = 0; ch < 2; ++ch) {
-            uint32_t sv[32];
-            ptx::tmem_ld_x32(tmem + lane_base + T_S + c0 + ch * 32, sv);
-            ptx::tmem_wait_ld();
+            const uint32_t* sv = sva + ch * 32;
 #pragma unroll
             for (int e4 = 0; e4 < 8; ++e4) {
               const float4 l4 = ptx::lds_v4f(vL2 + (c0 + ch * 32 + e4 * 4) * 4);

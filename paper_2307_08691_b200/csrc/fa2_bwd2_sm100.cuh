@@ -554,7 +554,9 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
       // query halves sit in both CTAs' A slots
       auto issue_dq = [&](uint32_t y) {
         ptx::mbar_wait(dsx_full, y & 1);                   // CTA 1's rows landed here
+        FA2_BTRACE(21, y);
         pair::wait_cluster(dsx_ready, y & 1);              // CTA 0's rows landed in CTA 1
+        FA2_BTRACE(22, y);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
 #pragma unroll 1   // rolled: sixteen hoisted 64-bit descriptor pairs would not fit the warp's registers

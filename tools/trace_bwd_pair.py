@@ -29,3 +29,5 @@ print("dQ warps: dq_full seen -> read out", avg(9, 10), "| reduce issue", avg(10
 print("exchange (CTA 0 -> 1): ds_ready(x) -> xs_full seen", avg(3, 17), "| ds_free wait", avg(17, 18),
       "| copy read done", avg(18, 19), "| CTA 1 -> 0 landed (dsx_full seen) after copy issue", avg(18, 20),
       "| dQ issued after landing", avg(20, 5))
+print("mma in issue_dq: dsx_full seen after event 8", avg(8, 21), "| dsx_ready (relay) seen after dsx_full", avg(21, 22),
+      "| dQ MMAs issued after both", avg(22, 5))
