@@ -630,7 +630,7 @@ fa2_status_t launch_bwd_pair(const fa2::BwdMaps& maps, const CUtensorMap& mq64, 
   if (s != FA2_OK) return s;
   const int N = p.geom.Nq;
   p.num_n_blocks = (N + 255) / 256;
-  p.num_tiles = (p.BH / p.group) * p.num_n_blocks;
+  p.num_tiles = (p.BH / p.group) * p.hsplit * p.num_n_blocks;
   int npairs = std::min(p.num_tiles, std::min(sms / 2, max_active_pairs(kern, smem, fa2::kBwdThreads, sms)));
   if (p.dq_sem != nullptr) {
     // deterministic mode (fa2_bwd2_sm100.cuh pair_q_tile / pair_rank): the cyclic order needs an
@@ -646,10 +646,10 @@ fa2_status_t launch_bwd_pair(const fa2::BwdMaps& maps, const CUtensorMap& mq64, 
   sched.n = 0;
   if constexpr (CAUSAL) {   // balanced pair-tile lists: key block nb2 sees nqb - 2 nb2 query tiles per head
     if (FA2_SCHED && p.dq_sem == nullptr && p.num_tiles <= fa2::kSchedMaxTiles && npairs <= fa2::kSchedMaxCtas) {
-      const int nnb2 = p.num_n_blocks, group = p.group, nt = p.num_tiles;
-      const SchedPtr sc = cached_sched(2, nt, nnb2, N, group, npairs, [&](std::vector<int>& work) {
+      const int nnb2 = p.num_n_blocks, nh = p.group / p.hsplit, nt = p.num_tiles;
+      const SchedPtr sc = cached_sched(2, nt, nnb2, N, nh, npairs, [&](std::vector<int>& work) {
         const int nqb = (N + 127) / 128;
-        for (int t = 0; t < nt; ++t) work[t] = (nqb - 2 * (t % nnb2)) * group + 1;
+        for (int t = 0; t < nt; ++t) work[t] = (nqb - 2 * (t % nnb2)) * nh + 1;
       });
       mark(3, st);
       kern<<<2 * npairs, fa2::kBwdThreads, smem, st>>>(mq64, maps.q, maps.k, maps.v, mdo64, maps.dout, p, *sc);
@@ -676,12 +676,15 @@ int choose_hsplit(const Geom& g, bool causal, bool deterministic, int sms, size_
   dk_numel = (g.packed ? static_cast<long long>(g.Tk) : static_cast<long long>(g.B) * g.Nk) * g.Hkv * g.d;
   acc_off = (base + 255) / 256 * 256;
   if (group == 1 || deterministic || ws_bytes < acc_off + static_cast<size_t>(dk_numel) * 8) return 1;
-  const long long nkb = (g.Nk + 127) / 128, nqb = (g.Nq + 127) / 128;
+  // the CTA-pair kernel (square fixed-length d = 128) tiles keys by 256 on pairs of SMs
+  const bool pair_path = g.d == 128 && !g.packed && g.Nq == g.Nk;
+  const long long kb = pair_path ? 256 : 128, units = pair_path ? sms / 2 : sms;
+  const long long nkb = (g.Nk + kb - 1) / kb, nqb = (g.Nq + 127) / 128;
   const long long tiles1 = static_cast<long long>(g.B) * g.Hkv * nkb;
-  long long need = (2LL * sms + tiles1 - 1) / tiles1;
+  long long need = (2LL * units + tiles1 - 1) / tiles1;
   if (causal) {   // heaviest tile (key block 0: nqb query tiles x group/split heads) <= 1/4 of an SM's share
     const long long den = (nqb + 1) * g.B * g.Hkv;
-    need = std::max(need, (8LL * sms + den - 1) / den);
+    need = std::max(need, (8LL * units * (pair_path ? 2 : 1) + den - 1) / den);
   }
   for (int sp = 1; sp <= group; ++sp)
     if (group % sp == 0 && sp >= need) return sp;
@@ -754,7 +757,7 @@ fa2_status_t backward_impl(const void* q, const void* k, const void* v, const vo
   // path; FA2_BWD_PAIR=0 in the environment selects the one-SM kernel instead (A/B runs and
   // the one-SM kernel's parity test)
   static const bool pair_env = [] { const char* e = std::getenv("FA2_BWD_PAIR"); return !(e && e[0] == '0'); }();
-  const bool pair = FA2_BWD_PAIR && pair_env && g.d == 128 && !g.packed && g.Nq == g.Nk && hsplit == 1;
+  const bool pair = FA2_BWD_PAIR && pair_env && g.d == 128 && !g.packed && g.Nq == g.Nk;
   if (pair) {
     CUtensorMap mq64, mdo64;
     if ((s = make_rows_map(&mq64, q, dt, g, g.H, true, 2, 64)) != FA2_OK) return s;

@@ -99,13 +99,18 @@ struct BwdPairSmem {
 };
 
 // A pair work tile: key block nb2 (256 rows) of key/value head kvh of batch b, visited
-// with query tiles i0 .. nqb-1 of every query head of the group.
+// with query tiles i0 .. nqb-1 of query heads kvh*group + h0 .. + h0+nh-1 (the whole group
+// unless the GQA load balance splits it over hsplit tiles, BwdParams::hsplit).
 struct PairTile {
-  int b, kvh, nb2, i0, nqt;
+  int b, kvh, nb2, i0, nqt, h0, nh;
 };
 FA2_DEVICE PairTile pair_tile(const BwdParams& p, bool causal, int t) {
   PairTile w;
-  const int bh = t / p.num_n_blocks;
+  int bh = t / p.num_n_blocks;   // (b * Hkv + kvh) * hsplit + split
+  const int split = bh % p.hsplit;
+  bh /= p.hsplit;
+  w.nh = p.group / p.hsplit;
+  w.h0 = split * w.nh;
   w.nb2 = t % p.num_n_blocks;
   // deterministic cyclic causal: alternate heavy / light key blocks between the grid's rounds
   // (all key blocks of a head run in the same round, so this only permutes them over pairs)
@@ -267,7 +272,7 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
     for (int n_ = 0, t; (t = pair::sched_tile_pair(sched, n_, p.num_tiles, pair_id, npairs)) >= 0; ++n_, ++it) {
       const PairTile w = pair_tile(p, CAUSAL, t);
       const int kv_row = w.nb2 * 256 + static_cast<int>(rank) * 128 + r;
-      const int nx = w.nqt * p.group;
+      const int nx = w.nqt * w.nh;
       for (int x = 0; x < nx; ++x, ++g) {
         const int i = pair_q_tile(p, CAUSAL, w, x % w.nqt);
         const uint32_t slot = g & 1;
@@ -397,7 +402,25 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
       // ---- epilogue: dV_j (warpgroup 0), dK_j * scale (warpgroup 1) ----
       ptx::mbar_wait(dkv_full, it & 1);
       ptx::tc_fence_after();
-      {
+      if (p.hsplit > 1) {
+        // this tile covers part of the group's query heads: fp32 reduce-add of the partial
+        // dV / dK (fa2_dkv_convert casts the sums)
+        const uint32_t tsrc = tmem + lane_base + (wg == 0 ? T_DV : T_DK);
+        const float mul = wg == 0 ? 1.f : p.scale;
+        float* acc = (wg == 0 ? p.dv_acc : p.dk_acc) + (static_cast<long long>(w.b * p.Hkv + w.kvh) * N + kv_row) * D;
+#pragma unroll
+        for (int ch = 0; ch < D / 32; ++ch) {
+          uint32_t v[32];
+          ptx::tmem_ld_x32(tsrc + ch * 32, v);
+          ptx::tmem_wait_ld();
+          if (kv_row < N) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              ptx::red_add_v4_f32(acc + ch * 32 + 4 * e, __uint_as_float(v[4 * e]) * mul, __uint_as_float(v[4 * e + 1]) * mul,
+                                  __uint_as_float(v[4 * e + 2]) * mul, __uint_as_float(v[4 * e + 3]) * mul);
+          }
+        }
+      } else {
         const uint32_t tsrc = tmem + lane_base + (wg == 0 ? T_DV : T_DK);
         const float mul = wg == 0 ? 1.f : p.scale;
         uint8_t* dst = reinterpret_cast<uint8_t*>(wg == 0 ? p.dv : p.dk) +
@@ -439,10 +462,10 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
     uint32_t g = 0;
     for (int n_ = 0, t; (t = pair::sched_tile_pair(sched, n_, p.num_tiles, pair_id, npairs)) >= 0; ++n_) {
       const PairTile w = pair_tile(p, CAUSAL, t);
-      const int nx = w.nqt * p.group;
+      const int nx = w.nqt * w.nh;
       for (int x = 0; x < nx; ++x, ++g) {
         const int i = pair_q_tile(p, CAUSAL, w, x % w.nqt);
-        const int hq = w.kvh * p.group + x / w.nqt;
+        const int hq = w.kvh * p.group + w.h0 + x / w.nqt;
         // this CTA's 32 KB of the tile (query rows [64 rank, +64)), this d half's 16 KB
         float* const acc = p.dq_acc + ((static_cast<long long>(w.b) * p.H + hq) * p.acc_hs + static_cast<long long>(i) * BM) * D +
                            (rank * 32 + dh * 16) * 256;
@@ -579,7 +602,7 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
       int it = 0;
       for (int n_ = 0, t; (t = pair::sched_tile_pair(sched, n_, p.num_tiles, pair_id, npairs)) >= 0; ++n_, ++it) {
         const PairTile w = pair_tile(p, CAUSAL, t);
-        const uint32_t n = static_cast<uint32_t>(w.nqt * p.group);
+        const uint32_t n = static_cast<uint32_t>(w.nqt * w.nh);
         const uint32_t g0 = g, end = g0 + n;
         // prologue: S^T(g0), dP^T(g0), dV(g0), S^T(g0+1)
         ptx::mbar_wait(kv_full, it & 1);
@@ -655,10 +678,10 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
           pair::tma_load_pair(sV + s * L::BOX128, &tm_v, kv_full, s * 64, k0 + ro * 128, kvb, pol_kv);
           pair::tma_load_pair(sKd + s * L::BOX128, &tm_k, kv_full, ro * 64, k0 + s * 128, kvb, pol_kv);
         }
-        const int nx = w.nqt * p.group;
+        const int nx = w.nqt * w.nh;
         for (int x = 0; x < nx; ++x, ++g) {
           const int i = pair_q_tile(p, CAUSAL, w, x % w.nqt);
-          const int hq = w.kvh * p.group + x / w.nqt;
+          const int hq = w.kvh * p.group + w.h0 + x / w.nqt;
           const int bhq = w.b * p.H + hq;
           const uint32_t slot = g & 1;
           // L_i * log2(e), D_i: this CTA's own copy (local barrier)
@@ -697,7 +720,7 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
       uint32_t g = 0;
       for (int n_ = 0, t; (t = pair::sched_tile_pair(sched, n_, p.num_tiles, pair_id, npairs)) >= 0; ++n_) {
         const PairTile w = pair_tile(p, CAUSAL, t);
-        const int nx = w.nqt * p.group;
+        const int nx = w.nqt * w.nh;
         for (int x = 0; x < nx; ++x, ++g) {
           ptx::mbar_arrive_expect_tx(dsx_full, L::BOX128);
           ptx::mbar_wait(dsx_full, g & 1);
@@ -718,7 +741,7 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
       uint32_t g = 0;
       for (int n_ = 0, t; (t = pair::sched_tile_pair(sched, n_, p.num_tiles, pair_id, npairs)) >= 0; ++n_) {
         const PairTile w = pair_tile(p, CAUSAL, t);
-        const int nx = w.nqt * p.group;
+        const int nx = w.nqt * w.nh;
         for (int x = 0; x < nx; ++x, ++g) {
           ptx::mbar_wait(xs_full, g & 1);
           FA2_BTRACE(17, g);
