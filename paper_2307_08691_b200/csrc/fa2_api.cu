@@ -157,7 +157,7 @@ fa2_status_t make_rows_map(CUtensorMap* m, const void* base, CUtensorMapDataType
     const cuuint64_t t = static_cast<cuuint64_t>(std::max(1, is_q ? g.Tq : g.Tk));
     dims[0] = d; dims[1] = static_cast<cuuint64_t>(heads); dims[2] = t;
     strides[0] = d * eb; strides[1] = static_cast<cuuint64_t>(heads) * d * eb;
-    box[0] = box_cols; box[1] = 1; box[2] = 128;
+    box[0] = box_cols; box[1] = 1; box[2] = static_cast<cuuint32_t>(box_rows);
   }
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -619,17 +619,18 @@ fa2_status_t dispatch_bwd_causal(bool causal, const fa2::BwdMaps& maps, const fa
 #ifndef FA2_BWD_PAIR
 #define FA2_BWD_PAIR 1   // 0: the one-SM d = 128 backward kernel for every shape (A/B builds)
 #endif
-// CTA-pair backward (fa2_bwd2_sm100.cuh): d = 128, square fixed-length, arrival-order dQ.
-// p arrives with the 128-row tiling; the pair kernel tiles keys by 256.
-template <bool BF16, bool CAUSAL>
+// CTA-pair backward (fa2_bwd2_sm100.cuh): d = 128, every geometry (GEN: N_q != N_k and/or
+// packed variable-length), arrival-order or deterministic dQ.  p arrives with the 128-row
+// tiling; the pair kernel tiles keys by 256.
+template <bool BF16, bool CAUSAL, bool GEN>
 fa2_status_t launch_bwd_pair(const fa2::BwdMaps& maps, const CUtensorMap& mq64, const CUtensorMap& mdo64,
                              fa2::BwdParams p, int sms, cudaStream_t st) {
-  auto kern = fa2::fa2_bwd_pair_kernel<BF16, CAUSAL>;
+  auto kern = fa2::fa2_bwd_pair_kernel<BF16, CAUSAL, GEN>;
   constexpr int smem = fa2::BwdPairSmem::ALLOC;
   fa2_status_t s = set_smem(kern, smem);
   if (s != FA2_OK) return s;
   const int N = p.geom.Nq;
-  p.num_n_blocks = (N + 255) / 256;
+  p.num_n_blocks = (p.geom.Nk + 255) / 256;
   p.num_tiles = (p.BH / p.group) * p.hsplit * p.num_n_blocks;
   int npairs = std::min(p.num_tiles, std::min(sms / 2, max_active_pairs(kern, smem, fa2::kBwdThreads, sms)));
   if (p.dq_sem != nullptr) {
@@ -639,12 +640,12 @@ fa2_status_t launch_bwd_pair(const fa2::BwdMaps& maps, const CUtensorMap& mq64, 
 #ifndef FA2_DET_CYCLIC_PAIR
 #define FA2_DET_CYCLIC_PAIR 1
 #endif
-    p.det_cyclic = (FA2_DET_CYCLIC_PAIR && p.num_n_blocks <= npairs && ((N + 127) / 128) % 2 == 0) ? 1 : 0;
+    p.det_cyclic = (!GEN && FA2_DET_CYCLIC_PAIR && p.num_n_blocks <= npairs && ((N + 127) / 128) % 2 == 0) ? 1 : 0;
     if (p.det_cyclic) npairs = (npairs / p.num_n_blocks) * p.num_n_blocks;
   }
-  fa2::SchedT<CAUSAL> sched;
+  fa2::SchedT<CAUSAL && !GEN> sched;
   sched.n = 0;
-  if constexpr (CAUSAL) {   // balanced pair-tile lists: key block nb2 sees nqb - 2 nb2 query tiles per head
+  if constexpr (CAUSAL && !GEN) {   // balanced pair-tile lists: key block nb2 sees nqb - 2 nb2 query tiles per head
     if (FA2_SCHED && p.dq_sem == nullptr && p.num_tiles <= fa2::kSchedMaxTiles && npairs <= fa2::kSchedMaxCtas) {
       const int nnb2 = p.num_n_blocks, nh = p.group / p.hsplit, nt = p.num_tiles;
       const SchedPtr sc = cached_sched(2, nt, nnb2, N, nh, npairs, [&](std::vector<int>& work) {
@@ -677,7 +678,7 @@ int choose_hsplit(const Geom& g, bool causal, bool deterministic, int sms, size_
   acc_off = (base + 255) / 256 * 256;
   if (group == 1 || deterministic || ws_bytes < acc_off + static_cast<size_t>(dk_numel) * 8) return 1;
   // the CTA-pair kernel (square fixed-length d = 128) tiles keys by 256 on pairs of SMs
-  const bool pair_path = g.d == 128 && !g.packed && g.Nq == g.Nk;
+  const bool pair_path = g.d == 128;
   const long long kb = pair_path ? 256 : 128, units = pair_path ? sms / 2 : sms;
   const long long nkb = (g.Nk + kb - 1) / kb, nqb = (g.Nq + 127) / 128;
   const long long tiles1 = static_cast<long long>(g.B) * g.Hkv * nkb;
@@ -757,15 +758,20 @@ fa2_status_t backward_impl(const void* q, const void* k, const void* v, const vo
   // path; FA2_BWD_PAIR=0 in the environment selects the one-SM kernel instead (A/B runs and
   // the one-SM kernel's parity test)
   static const bool pair_env = [] { const char* e = std::getenv("FA2_BWD_PAIR"); return !(e && e[0] == '0'); }();
-  const bool pair = FA2_BWD_PAIR && pair_env && g.d == 128 && !g.packed && g.Nq == g.Nk;
+  const bool pair = FA2_BWD_PAIR && pair_env && g.d == 128;
   if (pair) {
     CUtensorMap mq64, mdo64;
     if ((s = make_rows_map(&mq64, q, dt, g, g.H, true, 2, 64)) != FA2_OK) return s;
     if ((s = make_rows_map(&mdo64, dout, dt, g, g.H, true, 2, 64)) != FA2_OK) return s;
-    s = bf16 ? (causal ? launch_bwd_pair<true, true>(maps, mq64, mdo64, p, sms, st)
-                       : launch_bwd_pair<true, false>(maps, mq64, mdo64, p, sms, st))
-             : (causal ? launch_bwd_pair<false, true>(maps, mq64, mdo64, p, sms, st)
-                       : launch_bwd_pair<false, false>(maps, mq64, mdo64, p, sms, st));
+    const bool gen = g.packed || g.Nq != g.Nk;
+#define FA2_PAIR_LAUNCH(B16, C, G) launch_bwd_pair<B16, C, G>(maps, mq64, mdo64, p, sms, st)
+    if (gen)
+      s = bf16 ? (causal ? FA2_PAIR_LAUNCH(true, true, true) : FA2_PAIR_LAUNCH(true, false, true))
+               : (causal ? FA2_PAIR_LAUNCH(false, true, true) : FA2_PAIR_LAUNCH(false, false, true));
+    else
+      s = bf16 ? (causal ? FA2_PAIR_LAUNCH(true, true, false) : FA2_PAIR_LAUNCH(true, false, false))
+               : (causal ? FA2_PAIR_LAUNCH(false, true, false) : FA2_PAIR_LAUNCH(false, false, false));
+#undef FA2_PAIR_LAUNCH
   } else if (g.d == 64)
     s = bf16 ? dispatch_bwd_causal<64, true>(causal, maps, p, sms, st) : dispatch_bwd_causal<64, false>(causal, maps, p, sms, st);
   else

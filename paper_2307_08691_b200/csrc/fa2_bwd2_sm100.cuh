@@ -101,9 +101,14 @@ struct BwdPairSmem {
 // A pair work tile: key block nb2 (256 rows) of key/value head kvh of batch b, visited
 // with query tiles i0 .. nqb-1 of query heads kvh*group + h0 .. + h0+nh-1 (the whole group
 // unless the GQA load balance splits it over hsplit tiles, BwdParams::hsplit).
+// nqt < 0: the key block lies past its sequence's keys (varlen: the tile grid is sized by the
+// longest sequence) -- no work and no rows; nqt == 0: no query row sees it (N_q == 0) -- dK =
+// dV = 0 are written, nothing else runs.
 struct PairTile {
   int b, kvh, nb2, i0, nqt, h0, nh;
+  Seq sq;
 };
+template <bool GEN>
 FA2_DEVICE PairTile pair_tile(const BwdParams& p, bool causal, int t) {
   PairTile w;
   int bh = t / p.num_n_blocks;   // (b * Hkv + kvh) * hsplit + split
@@ -118,10 +123,28 @@ FA2_DEVICE PairTile pair_tile(const BwdParams& p, bool causal, int t) {
     w.nb2 = p.num_n_blocks - 1 - w.nb2;
   w.b = bh / p.Hkv;
   w.kvh = bh % p.Hkv;
-  const int nqb = (p.geom.Nq + 127) / 128;
-  w.i0 = causal ? 2 * w.nb2 : 0;   // first query tile that sees key 256 nb2 (CTA 0's first key)
-  w.nqt = nqb - w.i0;
+  w.sq = seq_of<GEN>(p.geom, w.b);
+  const int nqb = (w.sq.nq + 127) / 128;
+  int i0 = 0;
+  if (causal) {   // first query tile that sees key 256 nb2 (CTA 0's first key): row >= 256 nb2 - off (R22)
+    const int first_row = w.nb2 * 256 - w.sq.off;
+    i0 = first_row > 0 ? first_row / 128 : 0;
+  }
+  w.i0 = i0;
+  w.nqt = w.nb2 * 256 >= w.sq.nk ? -1 : (nqb > i0 ? nqb - i0 : 0);
   return w;
+}
+// first padded dQ_acc / L / D row of query head hq of the tile's sequence (RowParams layout)
+template <bool GEN>
+FA2_DEVICE long long pair_acc_row0(const BwdParams& p, const PairTile& w, int hq) {
+  if (GEN && p.tile_off != nullptr) return hq * p.acc_hs + 128LL * __ldg(p.tile_off + w.b);
+  return w.sq.bc * p.acc_bs + hq * p.acc_hs;
+}
+// dK / dV element offset of sequence-relative key row kv_row of the tile's key/value head
+template <bool GEN>
+FA2_DEVICE long long pair_kv_off(const BwdParams& p, const PairTile& w, int kv_row) {
+  if constexpr (!GEN) return (static_cast<long long>(w.b * p.Hkv + w.kvh) * w.sq.nk + kv_row) * 128;
+  return w.sq.bc * p.k_bs + w.kvh * p.k_hs + (w.sq.k0 + kv_row) * p.k_rs;
 }
 // Deterministic mode (R21, §6.4): every dQ half-tile (query head,
 // query tile i, query half r, d half) receives the pair key blocks' contributions in a fixed
@@ -147,12 +170,14 @@ FA2_DEVICE int pair_rank(const BwdParams& p, bool causal, const PairTile& w, int
   return causal ? (i >> 1) - w.nb2 : (s >> 1);
 }
 
-template <bool BF16, bool CAUSAL>
+// GEN: N_q != N_k and/or the packed variable-length layout (fa2_seq.cuh), resolved per work
+// tile; the square fixed-length path keeps its constant lengths.
+template <bool BF16, bool CAUSAL, bool GEN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBwdThreads, 1)
 fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_constant__ CUtensorMap tm_q128,
                     const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                     const __grid_constant__ CUtensorMap tm_do64, const __grid_constant__ CUtensorMap tm_do128,
-                    const BwdParams p, const __grid_constant__ SchedT<CAUSAL> sched) {
+                    const BwdParams p, const __grid_constant__ SchedT<CAUSAL && !GEN> sched) {
   using L = BwdPairSmem;
   constexpr int D = 128, BM = 128;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -249,7 +274,6 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   constexpr uint32_t T_S = 0, T_DQ = 64, T_DP = 128, T_DV = 256, T_DK = 384;
-  const int N = p.geom.Nq;
 
   if (warp < 8) {
     // ====================== compute warpgroups: P^T, dS^T ======================
@@ -269,9 +293,18 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
     const float sl2 = p.scale_log2;
     uint32_t g = 0;
     int it = 0;
-    for (int n_ = 0, t; (t = pair::sched_tile_pair(sched, n_, p.num_tiles, pair_id, npairs)) >= 0; ++n_, ++it) {
-      const PairTile w = pair_tile(p, CAUSAL, t);
-      const int kv_row = w.nb2 * 256 + static_cast<int>(rank) * 128 + r;
+    for (int n_ = 0, t; (t = pair::sched_tile_pair(sched, n_, p.num_tiles, pair_id, npairs)) >= 0; ++n_) {
+      const PairTile w = pair_tile<GEN>(p, CAUSAL, t);
+      if (w.nqt < 0) continue;
+      const int kv_row = w.nb2 * 256 + static_cast<int>(rank) * 128 + r;   // sequence-relative
+      const int nk = w.sq.nk;
+      if (w.nqt == 0) {   // no query row sees this key block (N_q == 0): dV = dK = 0
+        if (p.hsplit == 1 && kv_row < nk) {   // (split: the zeroed fp32 accumulators already hold 0)
+          uint4* z = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(wg == 0 ? p.dv : p.dk) + pair_kv_off<GEN>(p, w, kv_row) * 2);
+          for (int e = 0; e < D / 8; ++e) z[e] = make_uint4(0u, 0u, 0u, 0u);
+        }
+        continue;
+      }
       const int nx = w.nqt * w.nh;
       for (int x = 0; x < nx; ++x, ++g) {
         const int i = pair_q_tile(p, CAUSAL, w, x % w.nqt);
@@ -280,7 +313,7 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
         // mask: causal tiles crossing the diagonal and the ragged key tail (query rows past N
         // need none: their L*log2e is +inf, so P = 0)
         const int kv_first = w.nb2 * 256 + static_cast<int>(rank) * 128;
-        const bool need_mask = (CAUSAL && kv_first + 127 > i * BM) || (kv_first + 128 > N);
+        const bool need_mask = (CAUSAL && kv_first + 127 > i * BM + w.sq.off) || (kv_first + 128 > nk);
         ptx::mbar_wait(&vec_full[slot], (g >> 1) & 1);
         ptx::mbar_wait(s_full, g & 1);
         if (threadIdx.x == 0) FA2_BTRACE(0, g);
@@ -320,8 +353,8 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
                 }
                 if (!EMU && need_mask) {
                   const int q_row = i * BM + c0 + e;
-                  if ((CAUSAL && kv_row > q_row) || kv_row >= N) pr.x = 0.f;
-                  if ((CAUSAL && kv_row > q_row + 1) || kv_row >= N) pr.y = 0.f;
+                  if ((CAUSAL && kv_row > q_row + w.sq.off) || kv_row >= nk) pr.x = 0.f;
+                  if ((CAUSAL && kv_row > q_row + 1 + w.sq.off) || kv_row >= nk) pr.y = 0.f;
                 }
                 pf[e] = pr.x;
                 pf[e + 1] = pr.y;
@@ -329,7 +362,9 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
             }
           }
         };
-        if (need_mask) p_block(std::integral_constant<int, 0>{});
+        // rows that see no key (R23) carry L*log2e = +inf: the polynomial would give 2^-125
+        // instead of 0, so the general geometry keeps MUFU everywhere
+        if (need_mask || GEN) p_block(std::integral_constant<int, 0>{});
         else p_block(std::integral_constant<int, FA2_BWD_PAIR_EMU>{});
         if (threadIdx.x == 0) FA2_BTRACE(15, g);
         {
@@ -407,13 +442,13 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
         // dV / dK (fa2_dkv_convert casts the sums)
         const uint32_t tsrc = tmem + lane_base + (wg == 0 ? T_DV : T_DK);
         const float mul = wg == 0 ? 1.f : p.scale;
-        float* acc = (wg == 0 ? p.dv_acc : p.dk_acc) + (static_cast<long long>(w.b * p.Hkv + w.kvh) * N + kv_row) * D;
+        float* acc = (wg == 0 ? p.dv_acc : p.dk_acc) + pair_kv_off<GEN>(p, w, kv_row);
 #pragma unroll
         for (int ch = 0; ch < D / 32; ++ch) {
           uint32_t v[32];
           ptx::tmem_ld_x32(tsrc + ch * 32, v);
           ptx::tmem_wait_ld();
-          if (kv_row < N) {
+          if (kv_row < nk) {
 #pragma unroll
             for (int e = 0; e < 8; ++e)
               ptx::red_add_v4_f32(acc + ch * 32 + 4 * e, __uint_as_float(v[4 * e]) * mul, __uint_as_float(v[4 * e + 1]) * mul,
@@ -423,8 +458,7 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
       } else {
         const uint32_t tsrc = tmem + lane_base + (wg == 0 ? T_DV : T_DK);
         const float mul = wg == 0 ? 1.f : p.scale;
-        uint8_t* dst = reinterpret_cast<uint8_t*>(wg == 0 ? p.dv : p.dk) +
-                       (static_cast<long long>(w.b * p.Hkv + w.kvh) * N + kv_row) * D * 2;
+        uint8_t* dst = reinterpret_cast<uint8_t*>(wg == 0 ? p.dv : p.dk) + pair_kv_off<GEN>(p, w, kv_row) * 2;
 #pragma unroll
         for (int ch = 0; ch < D / 32; ++ch) {
           uint32_t v[32];
@@ -433,7 +467,7 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
           uint32_t o16[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) o16[e] = ptx::pack2<BF16>(__uint_as_float(v[2 * e]) * mul, __uint_as_float(v[2 * e + 1]) * mul);
-          if (kv_row < N) {
+          if (kv_row < nk) {
             uint4* o = reinterpret_cast<uint4*>(dst + ch * 64);
 #pragma unroll
             for (int e = 0; e < 4; ++e) o[e] = make_uint4(o16[4 * e], o16[4 * e + 1], o16[4 * e + 2], o16[4 * e + 3]);
@@ -443,6 +477,7 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) pair::arrive_remote(dkv_empty, 0);
+      ++it;
     }
   } else if (warp < 12) {
     // ====================== dQ read-out + fp32 bulk reduce-add ======================
@@ -461,17 +496,17 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
     const bool leader = (threadIdx.x == 256);
     uint32_t g = 0;
     for (int n_ = 0, t; (t = pair::sched_tile_pair(sched, n_, p.num_tiles, pair_id, npairs)) >= 0; ++n_) {
-      const PairTile w = pair_tile(p, CAUSAL, t);
+      const PairTile w = pair_tile<GEN>(p, CAUSAL, t);
+      if (w.nqt <= 0) continue;
       const int nx = w.nqt * w.nh;
       for (int x = 0; x < nx; ++x, ++g) {
         const int i = pair_q_tile(p, CAUSAL, w, x % w.nqt);
         const int hq = w.kvh * p.group + w.h0 + x / w.nqt;
+        const long long acc0 = pair_acc_row0<GEN>(p, w, hq);
         // this CTA's 32 KB of the tile (query rows [64 rank, +64)), this d half's 16 KB
-        float* const acc = p.dq_acc + ((static_cast<long long>(w.b) * p.H + hq) * p.acc_hs + static_cast<long long>(i) * BM) * D +
-                           (rank * 32 + dh * 16) * 256;
+        float* const acc = p.dq_acc + (acc0 + static_cast<long long>(i) * BM) * D + (rank * 32 + dh * 16) * 256;
         // deterministic mode: this d half's counter of the dQ half-tile (see pair_rank)
-        int* const sem = p.dq_sem == nullptr ? nullptr
-            : p.dq_sem + (((static_cast<long long>(w.b) * p.H + hq) * p.acc_hs) / 128 + i) * 4 + rank * 2 + dh;
+        int* const sem = p.dq_sem == nullptr ? nullptr : p.dq_sem + (acc0 / 128 + i) * 4 + rank * 2 + dh;
         const int drank = pair_rank(p, CAUSAL, w, i, x % w.nqt);
         ptx::mbar_wait(dq_full, g & 1);
         if (leader) FA2_BTRACE(9, g);
@@ -600,8 +635,9 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
       // dS(x+1), and the exchange of dS(x) overlaps dK(x) / dP^T(x+1) and P(x+1).
       uint32_t g = 0;
       int it = 0;
-      for (int n_ = 0, t; (t = pair::sched_tile_pair(sched, n_, p.num_tiles, pair_id, npairs)) >= 0; ++n_, ++it) {
-        const PairTile w = pair_tile(p, CAUSAL, t);
+      for (int n_ = 0, t; (t = pair::sched_tile_pair(sched, n_, p.num_tiles, pair_id, npairs)) >= 0; ++n_) {
+        const PairTile w = pair_tile<GEN>(p, CAUSAL, t);
+        if (w.nqt <= 0) continue;
         const uint32_t n = static_cast<uint32_t>(w.nqt * w.nh);
         const uint32_t g0 = g, end = g0 + n;
         // prologue: S^T(g0), dP^T(g0), dV(g0), S^T(g0+1)
@@ -654,6 +690,7 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
           pair::commit_both(kv_empty);
         }
         __syncwarp();
+        ++it;
       }
     }
   } else if (warp == 13) {
@@ -665,49 +702,55 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
       const uint64_t pol_q = ptx::l2_policy_evict_last();
       const uint64_t pol_kv = ptx::l2_policy_evict_first();
       const int ro = static_cast<int>(rank);
+      // rows [row, row + box) of head `head` (of `heads`) at column c, in this tile's sequence:
+      // fixed layout {d, N, B*heads}, packed {d, heads, T} (fa2_seq.cuh tma_load_rows)
+      auto load = [&](void* dst, const CUtensorMap* m, uint64_t* bar, int c, int row, int head, int heads,
+                      const Seq& sq, uint64_t pol) {
+        if (GEN && p.geom.cu_q != nullptr) pair::tma_load_pair(dst, m, bar, c, head, row, pol);
+        else pair::tma_load_pair(dst, m, bar, c, row, sq.bc * heads + head, pol);
+      };
       uint32_t g = 0;
       int it = 0;
-      for (int n_ = 0, t; (t = pair::sched_tile_pair(sched, n_, p.num_tiles, pair_id, npairs)) >= 0; ++n_, ++it) {
-        const PairTile w = pair_tile(p, CAUSAL, t);
-        const int kvb = w.b * p.Hkv + w.kvh;
+      for (int n_ = 0, t; (t = pair::sched_tile_pair(sched, n_, p.num_tiles, pair_id, npairs)) >= 0; ++n_) {
+        const PairTile w = pair_tile<GEN>(p, CAUSAL, t);
+        if (w.nqt <= 0) continue;
         if (it > 0) ptx::mbar_wait(kv_empty, (it - 1) & 1);
+        ++it;
         if (rank == 0) ptx::mbar_arrive_expect_tx(kv_full, 2 * 6 * L::BOX128);
-        const int k0 = w.nb2 * 256;
+        const int k0 = w.sq.k0 + w.nb2 * 256;
         for (int s = 0; s < 2; ++s) {
-          pair::tma_load_pair(sK + s * L::BOX128, &tm_k, kv_full, s * 64, k0 + ro * 128, kvb, pol_kv);
-          pair::tma_load_pair(sV + s * L::BOX128, &tm_v, kv_full, s * 64, k0 + ro * 128, kvb, pol_kv);
-          pair::tma_load_pair(sKd + s * L::BOX128, &tm_k, kv_full, ro * 64, k0 + s * 128, kvb, pol_kv);
+          load(sK + s * L::BOX128, &tm_k, kv_full, s * 64, k0 + ro * 128, w.kvh, p.Hkv, w.sq, pol_kv);
+          load(sV + s * L::BOX128, &tm_v, kv_full, s * 64, k0 + ro * 128, w.kvh, p.Hkv, w.sq, pol_kv);
+          load(sKd + s * L::BOX128, &tm_k, kv_full, ro * 64, k0 + s * 128, w.kvh, p.Hkv, w.sq, pol_kv);
         }
         const int nx = w.nqt * w.nh;
         for (int x = 0; x < nx; ++x, ++g) {
           const int i = pair_q_tile(p, CAUSAL, w, x % w.nqt);
           const int hq = w.kvh * p.group + w.h0 + x / w.nqt;
-          const int bhq = w.b * p.H + hq;
+          const int q0 = w.sq.q0 + i * BM;
           const uint32_t slot = g & 1;
           // L_i * log2(e), D_i: this CTA's own copy (local barrier)
           if (g >= 2) ptx::mbar_wait(&vec_empty[slot], ((g >> 1) - 1) & 1);
           ptx::mbar_arrive_expect_tx(&vec_full[slot], 2 * BM * 4);
-          const long long voff = static_cast<long long>(bhq) * p.acc_hs + static_cast<long long>(i) * BM;
+          const long long voff = pair_acc_row0<GEN>(p, w, hq) + static_cast<long long>(i) * BM;
           ptx::bulk_load_1d(sVec + slot * 2 * BM, gL2 + voff, BM * 4, &vec_full[slot]);
           ptx::bulk_load_1d(sVec + slot * 2 * BM + BM, gD + voff, BM * 4, &vec_full[slot]);
           // Q_i rows of this CTA's query half, all d (released after S^T(i))
           if (g >= 1) ptx::mbar_wait(q_empty, (g - 1) & 1);
           if (rank == 0) ptx::mbar_arrive_expect_tx(q_full, 2 * 2 * L::BOX64);
-          for (int s = 0; s < 2; ++s)
-            pair::tma_load_pair(sQS + s * L::BOX64, &tm_q64, q_full, s * 64, i * BM + ro * 64, bhq, pol_q);
+          for (int s = 0; s < 2; ++s) load(sQS + s * L::BOX64, &tm_q64, q_full, s * 64, q0 + ro * 64, hq, p.H, w.sq, pol_q);
           // dO_i rows of this CTA's query half, all d (released after dP^T(i))
           if (g >= 1) ptx::mbar_wait(dop_empty, (g - 1) & 1);
           if (rank == 0) ptx::mbar_arrive_expect_tx(dop_full, 2 * 2 * L::BOX64);
-          for (int s = 0; s < 2; ++s)
-            pair::tma_load_pair(sDOP + s * L::BOX64, &tm_do64, dop_full, s * 64, i * BM + ro * 64, bhq, pol_q);
+          for (int s = 0; s < 2; ++s) load(sDOP + s * L::BOX64, &tm_do64, dop_full, s * 64, q0 + ro * 64, hq, p.H, w.sq, pol_q);
           // dO_i all rows, this CTA's d half (released after dV(i))
           if (g >= 1) ptx::mbar_wait(dov_empty, (g - 1) & 1);
           if (rank == 0) ptx::mbar_arrive_expect_tx(dov_full, 2 * L::BOX128);
-          pair::tma_load_pair(sDOV, &tm_do128, dov_full, ro * 64, i * BM, bhq, pol_q);
+          load(sDOV, &tm_do128, dov_full, ro * 64, q0, hq, p.H, w.sq, pol_q);
           // Q_i all rows, this CTA's d half (released after dK(i))
           if (g >= 1) ptx::mbar_wait(qk_empty, (g - 1) & 1);
           if (rank == 0) ptx::mbar_arrive_expect_tx(qk_full, 2 * L::BOX128);
-          pair::tma_load_pair(sQK, &tm_q128, qk_full, ro * 64, i * BM, bhq, pol_q);
+          load(sQK, &tm_q128, qk_full, ro * 64, q0, hq, p.H, w.sq, pol_q);
         }
       }
     }
@@ -719,8 +762,8 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
     if (lane == 0) {
       uint32_t g = 0;
       for (int n_ = 0, t; (t = pair::sched_tile_pair(sched, n_, p.num_tiles, pair_id, npairs)) >= 0; ++n_) {
-        const PairTile w = pair_tile(p, CAUSAL, t);
-        const int nx = w.nqt * w.nh;
+        const PairTile w = pair_tile<GEN>(p, CAUSAL, t);
+        const int nx = w.nqt > 0 ? w.nqt * w.nh : 0;
         for (int x = 0; x < nx; ++x, ++g) {
           ptx::mbar_arrive_expect_tx(dsx_full, L::BOX128);
           ptx::mbar_wait(dsx_full, g & 1);
@@ -740,8 +783,8 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
       const uint32_t peer_bar = pair::map_cta(ptx::smem_u32(dsx_full), peer);
       uint32_t g = 0;
       for (int n_ = 0, t; (t = pair::sched_tile_pair(sched, n_, p.num_tiles, pair_id, npairs)) >= 0; ++n_) {
-        const PairTile w = pair_tile(p, CAUSAL, t);
-        const int nx = w.nqt * w.nh;
+        const PairTile w = pair_tile<GEN>(p, CAUSAL, t);
+        const int nx = w.nqt > 0 ? w.nqt * w.nh : 0;
         for (int x = 0; x < nx; ++x, ++g) {
           ptx::mbar_wait(xs_full, g & 1);
           FA2_BTRACE(17, g);
