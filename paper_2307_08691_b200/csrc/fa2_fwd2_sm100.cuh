@@ -39,6 +39,18 @@ namespace fa2 {
 #define FA2_FWD_PAIR_EMU 2
 #endif
 constexpr int kFwdPairEmuPairs = FA2_FWD_PAIR_EMU;
+// Ping-pong of the two sub-tiles' exponential phases (named barriers 1 / 2, 256 threads):
+// softmax warpgroup 1 starts the exponentials of block g once warpgroup 0 has produced
+// FA2_FWD_PP_C of its 16 P~ chunks of block g, and warpgroup 0 starts block g + 1 once
+// warpgroup 1 is as far into block g.  Left free, the two warpgroups drift into phase (row
+// max, S loads and P~V waits of both at once, MUFU idle) on most pairs: 2775-3250 cycles
+// per key block depending on the pair, 2890-2930 on every pair with the ping-pong.
+#ifndef FA2_FWD_PINGPONG
+#define FA2_FWD_PINGPONG 1
+#endif
+#ifndef FA2_FWD_PP_C
+#define FA2_FWD_PP_C 8
+#endif
 
 
 struct FwdPairSmem {
@@ -146,6 +158,23 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       const int grow = mb * 512 + static_cast<int>(rank) * 256 + wg * 128 + row;
       float m_used = -INFINITY, l_sum = 0.f;
       const bool tr = threadIdx.x % 128 == 0 && t == pair_id;
+      const int tn = (t - pair_id) / npairs;
+      const bool last_tile = t + npairs >= p.num_tiles;
+      // ping-pong: wait for the partner warpgroup before this block's exponentials, signal it
+      // FA2_FWD_PP_C chunks in (warpgroup 1 skips its very last signal: nobody waits for it)
+      auto pp_wait = [&]() {
+        if (FA2_FWD_PINGPONG && (wg == 1 || pv_count > 0)) ptx::named_bar_sync(wg == 0 ? 2 : 1, 256);
+      };
+      auto pp_signal = [&](int j) {
+        if (FA2_FWD_PINGPONG && !(wg == 1 && last_tile && j + 1 == nkb)) ptx::named_bar_arrive(wg == 0 ? 1 : 2, 256);
+      };
+      if (threadIdx.x % 128 == 0) {
+        fa2_tile_trace(p.trace, tn, wg, 0, fa2_gtime());
+        fa2_tile_trace(p.trace, tn, wg, 1, clock64());
+        fa2_tile_trace(p.trace, tn, wg, 4, t);
+        fa2_tile_trace(p.trace, tn, wg, 5, nkb);
+        fa2_tile_trace(p.trace, tn, wg, 6, fa2_smid());
+      }
       for (int j = 0; j < nkb; ++j) {
         ptx::mbar_wait(&s_full[wg], s_count & 1);
         ++s_count;
@@ -203,10 +232,12 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
           }
           ptx::tmem_wait_st();
         }
+        pp_wait();
         auto exp_block = [&](auto emu_tag) {
           constexpr int EMU = decltype(emu_tag)::value;
 #pragma unroll
           for (int c = 0; c < 16; ++c) {   // chunk c: keys [8c, 8c + 8), 16 B of P~
+            if (c == FA2_FWD_PP_C) pp_signal(j);
             uint32_t pk[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -262,6 +293,10 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) pair::arrive_remote(&o_empty[wg], 0);
+      if (threadIdx.x % 128 == 0) {
+        fa2_tile_trace(p.trace, tn, wg, 2, fa2_gtime());
+        fa2_tile_trace(p.trace, tn, wg, 3, clock64());
+      }
     }
   } else {
     ptx::setmaxnreg_dec<56>();

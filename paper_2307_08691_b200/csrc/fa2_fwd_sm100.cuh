@@ -75,11 +75,31 @@ struct FwdParams {
 
 // Debug timeline: trace[(ev * 2 + who) * 64 + j] = clock64() for CTA 0's first
 // work tile (j < 64).  who = sub-tile / MMA-side index.
+// Every CTA's first work tile also lands at trace[65536 + ((cta * 8 + ev) * 2 + who) * 64 + j].
 #define FA2_TRACE(ev, who, j)                                                          \
   do {                                                                                 \
-    if (p.trace != nullptr && blockIdx.x == 0 && (j) < 64)                             \
-      p.trace[((ev) * 2 + (who)) * 64 + (j)] = clock64();                              \
+    if (p.trace != nullptr && (j) < 64) {                                              \
+      const unsigned long long c_ = clock64();                                         \
+      if (blockIdx.x == 0) p.trace[((ev) * 2 + (who)) * 64 + (j)] = c_;                \
+      p.trace[65536 + ((blockIdx.x * 8 + (ev)) * 2 + (who)) * 64 + (j)] = c_;          \
+    }                                                                                  \
   } while (0)
+// Debug tile timeline (same buffer, from element 4096): for each CTA's first 16 work tiles and
+// each softmax warpgroup, {globaltimer, clock64} at the tile's start and after its epilogue,
+// the tile index and its key-block count.
+FA2_DEVICE void fa2_tile_trace(unsigned long long* tr, int n, int wg, int k, unsigned long long v) {
+  if (tr != nullptr && n < 16) tr[4096 + ((blockIdx.x * 16 + n) * 2 + wg) * 8 + k] = v;
+}
+FA2_DEVICE unsigned fa2_smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+FA2_DEVICE unsigned long long fa2_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Causal, square fixed-length path: host-computed balanced tile schedule (fa2_seq.cuh).
 template <bool CAUSAL, bool GEN>
@@ -232,6 +252,14 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       const int nb = n_blocks(sq, mb, wg);
       const int row0 = mb * 256 + wg * 128;
       const int grow = row0 + row;
+      const bool ttr = threadIdx.x % 128 == 0;
+      if (ttr) {
+        fa2_tile_trace(p.trace, n, wg, 0, fa2_gtime());
+        fa2_tile_trace(p.trace, n, wg, 1, clock64());
+        fa2_tile_trace(p.trace, n, wg, 4, t);
+        fa2_tile_trace(p.trace, n, wg, 5, nb);
+        fa2_tile_trace(p.trace, n, wg, 6, fa2_smid());
+      }
       if (nb == 0) {
         // rows that see no key (R23): O = 0, L = -inf; no MMA work was scheduled
         if (grow < sq.nq) {
@@ -397,6 +425,10 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&o_empty[wg]);
+      if (ttr) {
+        fa2_tile_trace(p.trace, n, wg, 2, fa2_gtime());
+        fa2_tile_trace(p.trace, n, wg, 3, clock64());
+      }
     }
   } else {
     ptx::setmaxnreg_dec<CFG::REG_OTHER>();
