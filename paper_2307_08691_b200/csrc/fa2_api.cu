@@ -358,11 +358,29 @@ fa2_status_t dispatch_fwd_causal(bool causal, const CUtensorMap& mq, const CUten
 #ifndef FA2_FWD_PAIR
 #define FA2_FWD_PAIR 1   // 0: the one-SM forward kernel for every shape (A/B builds)
 #endif
-// CTA-pair forward (fa2_fwd2_sm100.cuh): non-causal, square fixed-length, d = 128, bf16/fp16
-template <bool BF16>
+#ifndef FA2_FWD_PAIR_CAUSAL
+#define FA2_FWD_PAIR_CAUSAL 1   // 0: causal square d = 128 on the one-SM kernel (A/B builds)
+#endif
+// Pair forward (causal, square): tile t = (head, 512-row block mb = nmb - 1 - t % nmb), work =
+// key blocks of its two sub-tiles (sub-tile i: 4 mb + 2 i + 2, at most T_c) + 2 (prologue /
+// epilogue); one list per CTA pair.
+SchedPtr fwd_pair_sched(const fa2::FwdParams& p, int npairs) {
+  const int nmb = p.num_m_blocks, N = p.geom.Nq;
+  return cached_sched(3, p.num_tiles, nmb, N, 1, npairs, [&](std::vector<int>& work) {
+    const int nkb = (N + 127) / 128;
+    for (int t = 0; t < p.num_tiles; ++t) {
+      const int mb = nmb - 1 - t % nmb;
+      work[t] = 2;
+      for (int i = 0; i < 2; ++i) work[t] += std::min(nkb, (mb * 512 + i * 256 + 255) / 128 + 1);
+    }
+  });
+}
+
+// CTA-pair forward (fa2_fwd2_sm100.cuh): square fixed-length, d = 128, bf16/fp16
+template <bool BF16, bool CAUSAL>
 fa2_status_t launch_fwd_pair(const CUtensorMap& mq, const CUtensorMap& mk64, const CUtensorMap& mv,
                              fa2::FwdParams p, int sms, cudaStream_t st) {
-  auto kern = fa2::fa2_fwd_pair_kernel<BF16>;
+  auto kern = fa2::fa2_fwd_pair_kernel<BF16, CAUSAL>;
   constexpr int smem = fa2::FwdPairSmem::ALLOC;
   fa2_status_t s = set_smem(kern, smem);
   if (s != FA2_OK) return s;
@@ -374,8 +392,20 @@ fa2_status_t launch_fwd_pair(const CUtensorMap& mq, const CUtensorMap& mk64, con
   int grid = 2 * p.num_tiles < sms ? 2 * p.num_tiles : sms;
   grid &= ~1;
   if (grid > 2 * max_clusters) grid = 2 * max_clusters;
+  if constexpr (CAUSAL) {
+    if (FA2_SCHED && p.num_tiles <= fa2::kSchedMaxTiles && grid / 2 <= fa2::kSchedMaxCtas) {
+      const SchedPtr sc = fwd_pair_sched(p, grid / 2);
+      mark(0, st);
+      kern<<<grid, 384, smem, st>>>(mq, mk64, mv, p, *sc);
+      mark(1, st);
+      FA2_CUDA(cudaGetLastError());
+      return FA2_OK;
+    }
+  }
+  fa2::SchedT<CAUSAL> sched;
+  sched.n = 0;
   mark(0, st);
-  kern<<<grid, 384, smem, st>>>(mq, mk64, mv, p);
+  kern<<<grid, 384, smem, st>>>(mq, mk64, mv, p, sched);
   mark(1, st);
   FA2_CUDA(cudaGetLastError());
   return FA2_OK;
@@ -387,7 +417,7 @@ fa2_status_t forward_impl(const void* q, const void* k, const void* v, void* o, 
   const CUtensorMapDataType dt = tma_dtype(dtype);
   fa2_status_t s;
   if ((s = make_rows_map(&mq, q, dt, g, g.H, true)) != FA2_OK) return s;
-  const bool pair = FA2_FWD_PAIR && !causal && g.d == 128 && !g.packed && g.Nq == g.Nk;
+  const bool pair = FA2_FWD_PAIR && (!causal || FA2_FWD_PAIR_CAUSAL) && g.d == 128 && !g.packed && g.Nq == g.Nk;
   if ((s = make_rows_map(&mk, k, dt, g, g.Hkv, false, 2, pair ? 64 : 128)) != FA2_OK) return s;
   if ((s = make_rows_map(&mv, v, dt, g, g.Hkv, false)) != FA2_OK) return s;
   fa2::FwdParams p;
@@ -411,7 +441,10 @@ fa2_status_t forward_impl(const void* q, const void* k, const void* v, void* o, 
   p.scale_log2 = scale * 1.4426950408889634f;
   p.trace = g_trace;
   const bool bf16 = dtype == FA2_BF16;
-  if (pair) return bf16 ? launch_fwd_pair<true>(mq, mk, mv, p, sms, st) : launch_fwd_pair<false>(mq, mk, mv, p, sms, st);
+  if (pair) {
+    if (causal) return bf16 ? launch_fwd_pair<true, true>(mq, mk, mv, p, sms, st) : launch_fwd_pair<false, true>(mq, mk, mv, p, sms, st);
+    return bf16 ? launch_fwd_pair<true, false>(mq, mk, mv, p, sms, st) : launch_fwd_pair<false, false>(mq, mk, mv, p, sms, st);
+  }
   if (g.d == 64)
     s = bf16 ? dispatch_fwd_causal<64, true>(causal, mq, mk, mv, p, sms, st)
              : dispatch_fwd_causal<64, false>(causal, mq, mk, mv, p, sms, st);

@@ -306,6 +306,15 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
         continue;
       }
       const int nx = w.nqt * w.nh;
+      // debug tile timeline (trace[4096 + (cta * 32 + n) * 8 + k]): start / end globaltimer and
+      // clock64, tile index, query-tile steps, SM id
+      const bool ttr = p.trace != nullptr && threadIdx.x == 0 && n_ < 32;
+      unsigned long long* const trow = ttr ? p.trace + 4096 + (blockIdx.x * 32 + n_) * 8 : nullptr;
+      if (ttr) {
+        unsigned long long gt; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        unsigned sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        trow[0] = gt; trow[1] = clock64(); trow[4] = t; trow[5] = nx; trow[6] = sm;
+      }
       for (int x = 0; x < nx; ++x, ++g) {
         const int i = pair_q_tile(p, CAUSAL, w, x % w.nqt);
         const uint32_t slot = g & 1;
@@ -477,6 +486,10 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) pair::arrive_remote(dkv_empty, 0);
+      if (ttr) {
+        unsigned long long gt; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        trow[2] = gt; trow[3] = clock64();
+      }
       ++it;
     }
   } else if (warp < 12) {

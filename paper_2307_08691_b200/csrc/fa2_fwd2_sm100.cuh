@@ -76,11 +76,18 @@ struct FwdPairSmem {
   static_assert(ALLOC <= 232448, "shared memory budget");
 };
 
-// p: as for fa2_fwd_kernel with num_m_blocks = ceil(N / 512), num_tiles = BH * num_m_blocks
-template <bool BF16>
+// p: as for fa2_fwd_kernel with num_m_blocks = ceil(N / 512), num_tiles = BH * num_m_blocks.
+// CAUSAL: CTA r's sub-tile i holds rows [512 m + 256 i + 128 r, +128), so every M = 256 MMA
+// covers 256 consecutive rows and sub-tile i visits key blocks 0 .. 4 m + 2 i + 1 (the last
+// two straddle or pass the diagonal of CTA 0's rows: masked).  Sub-tile 0 has two blocks
+// fewer; its warpgroup runs them as empty ping-pong steps (no S, no exponentials, no P~V,
+// its issuer only releases their K/V stages) so the two warpgroups keep alternating.  Tiles
+// come heaviest first from the host's balanced pair schedule (fa2_seq.cuh TileSched).
+template <bool BF16, bool CAUSAL>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k64,
-                    const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
+                    const __grid_constant__ CUtensorMap tm_v, const FwdParams p,
+                    const __grid_constant__ SchedT<CAUSAL> sched) {
   using L = FwdPairSmem;
   constexpr int D = 128, STAGES = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -140,6 +147,18 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
   const uint32_t tmem = *tmem_slot;
   const int N = p.geom.Nq;
   const int nkb = (N + 127) / 128;
+  // work tiles (shared by all roles): n-th tile of this pair, its head and 512-row block
+  auto tile_at = [&](int n) { return pair::sched_tile_pair(sched, n, p.num_tiles, pair_id, npairs); };
+  auto decode = [&](int t, int& bh, int& mb) {
+    bh = t / p.num_m_blocks;
+    const int r = t % p.num_m_blocks;
+    mb = CAUSAL ? p.num_m_blocks - 1 - r : r;   // causal: heavy row blocks first in the tile order
+  };
+  // first row of this CTA's sub-tile i, and the key blocks sub-tile i visits (both CTAs)
+  auto row0_of = [&](int mb, int i) {
+    return CAUSAL ? mb * 512 + i * 256 + static_cast<int>(rank) * 128 : mb * 512 + static_cast<int>(rank) * 256 + i * 128;
+  };
+  auto nblk = [&](int mb, int i) { return CAUSAL ? min(nkb, (mb * 512 + i * 256 + 255) / 128 + 1) : nkb; };
 
   if (warp < 8) {
     // ======================= softmax warpgroups =======================
@@ -151,31 +170,65 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     const uint32_t tO = tmem + lane_base + 256 + wg * D;
     // P~ row `row` of sub-tile wg: SW128 K-major, box b = keys [64 b, 64 b + 64)
     const uint32_t sP_row = ptx::smem_u32(sP + wg * L::P_TILE) + row * 128;
-    uint32_t s_count = 0, pv_count = 0;
+    uint32_t s_count = 0, pv_count = 0, gblk = 0;   // gblk: key blocks stepped (incl. empty steps)
     const float sl2 = p.scale_log2;
-    for (int t = pair_id; t < p.num_tiles; t += npairs) {
-      const int bh = t / p.num_m_blocks, mb = t % p.num_m_blocks;
-      const int grow = mb * 512 + static_cast<int>(rank) * 256 + wg * 128 + row;
+    for (int tn = 0, t; (t = tile_at(tn)) >= 0; ++tn) {
+      int bh, mb;
+      decode(t, bh, mb);
+      const int r0 = row0_of(mb, wg), grow = r0 + row;
+      const int nb = nblk(mb, wg), nkv = nblk(mb, 1);
       float m_used = -INFINITY, l_sum = 0.f;
-      const bool tr = threadIdx.x % 128 == 0 && t == pair_id;
-      const int tn = (t - pair_id) / npairs;
-      const bool last_tile = t + npairs >= p.num_tiles;
+      const bool tr = threadIdx.x % 128 == 0 && tn == 0;
+      const bool last_tile = tile_at(tn + 1) < 0;
       // ping-pong: wait for the partner warpgroup before this block's exponentials, signal it
       // FA2_FWD_PP_C chunks in (warpgroup 1 skips its very last signal: nobody waits for it)
       auto pp_wait = [&]() {
-        if (FA2_FWD_PINGPONG && (wg == 1 || pv_count > 0)) ptx::named_bar_sync(wg == 0 ? 2 : 1, 256);
+        if (FA2_FWD_PINGPONG && (wg == 1 || gblk > 0)) ptx::named_bar_sync(wg == 0 ? 2 : 1, 256);
       };
       auto pp_signal = [&](int j) {
-        if (FA2_FWD_PINGPONG && !(wg == 1 && last_tile && j + 1 == nkb)) ptx::named_bar_arrive(wg == 0 ? 1 : 2, 256);
+        if (FA2_FWD_PINGPONG && !(wg == 1 && last_tile && j + 1 == nkv)) ptx::named_bar_arrive(wg == 0 ? 1 : 2, 256);
       };
       if (threadIdx.x % 128 == 0) {
         fa2_tile_trace(p.trace, tn, wg, 0, fa2_gtime());
         fa2_tile_trace(p.trace, tn, wg, 1, clock64());
         fa2_tile_trace(p.trace, tn, wg, 4, t);
-        fa2_tile_trace(p.trace, tn, wg, 5, nkb);
+        fa2_tile_trace(p.trace, tn, wg, 5, nb);
         fa2_tile_trace(p.trace, tn, wg, 6, fa2_smid());
       }
-      for (int j = 0; j < nkb; ++j) {
+      // ---- epilogue: O = O / l, L = m + log l ----
+      auto epilogue = [&]() {
+        ptx::mbar_wait(&o_done[wg], (pv_count - 1) & 1);
+        ptx::tc_fence_after();
+        const float inv_l = l_sum > 0.f ? 1.f / l_sum : 0.f;
+        uint8_t* orow = reinterpret_cast<uint8_t*>(p.o) + (static_cast<size_t>(bh) * N + grow) * D * 2;
+#pragma unroll
+        for (int ch = 0; ch < D / 32; ++ch) {
+          uint32_t o[32];
+          ptx::tmem_ld_x32(tO + ch * 32, o);
+          ptx::tmem_wait_ld();
+          uint32_t q[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            q[e] = ptx::pack2<BF16>(__uint_as_float(o[2 * e]) * inv_l, __uint_as_float(o[2 * e + 1]) * inv_l);
+          if (grow < N) {
+            uint4* dst = reinterpret_cast<uint4*>(orow + ch * 64);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) dst[e] = make_uint4(q[4 * e], q[4 * e + 1], q[4 * e + 2], q[4 * e + 3]);
+          }
+        }
+        if (grow < N)
+          p.lse[static_cast<size_t>(bh) * N + grow] = l_sum > 0.f ? (m_used + ptx::lg2(l_sum)) * 0.69314718055994531f : -INFINITY;
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) pair::arrive_remote(&o_empty[wg], 0);
+      };
+      for (int j = 0; j < nkv; ++j) {
+        if (CAUSAL && j >= nb) {   // empty step of sub-tile 0 (its rows see none of these keys)
+          pp_wait();
+          pp_signal(j);
+          ++gblk;
+          continue;
+        }
         ptx::mbar_wait(&s_full[wg], s_count & 1);
         ++s_count;
         if (tr) FA2_TRACE(0, wg, j);
@@ -194,11 +247,14 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 #pragma unroll
         for (int c = 0; c < 128; ++c) s[c] = __uint_as_float(su[c]);
         const int c0 = j * 128;
-        const bool need_mask = c0 + 128 > N;
+        // ragged key tail; causal: blocks past the first row's diagonal (fully masked rows of
+        // CTA 0 keep m: block 0 always holds a visible key, so m is finite by then)
+        const bool need_mask = c0 + 128 > N || (CAUSAL && c0 + 127 > r0);
         if (need_mask) {
+          const int lim = CAUSAL ? min(N - 1, grow) : N - 1;
 #pragma unroll
           for (int c = 0; c < 128; ++c)
-            if (c0 + c >= N) s[c] = -INFINITY;
+            if (c0 + c > lim) s[c] = -INFINITY;
         }
         float mx = s[0];   // (a tree of 3-input maxima measured 1.7% slower here)
 #pragma unroll
@@ -267,32 +323,9 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         if (lane == 0) pair::arrive_remote(&p_full[wg], 0);
         if (tr) FA2_TRACE(3, wg, j);
         ++pv_count;
+        ++gblk;
       }
-      // ---- epilogue: O = O / l, L = m + log l ----
-      ptx::mbar_wait(&o_done[wg], (pv_count - 1) & 1);
-      ptx::tc_fence_after();
-      const float inv_l = l_sum > 0.f ? 1.f / l_sum : 0.f;
-      uint8_t* orow = reinterpret_cast<uint8_t*>(p.o) + (static_cast<size_t>(bh) * N + grow) * D * 2;
-#pragma unroll
-      for (int ch = 0; ch < D / 32; ++ch) {
-        uint32_t o[32];
-        ptx::tmem_ld_x32(tO + ch * 32, o);
-        ptx::tmem_wait_ld();
-        uint32_t q[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          q[e] = ptx::pack2<BF16>(__uint_as_float(o[2 * e]) * inv_l, __uint_as_float(o[2 * e + 1]) * inv_l);
-        if (grow < N) {
-          uint4* dst = reinterpret_cast<uint4*>(orow + ch * 64);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) dst[e] = make_uint4(q[4 * e], q[4 * e + 1], q[4 * e + 2], q[4 * e + 3]);
-        }
-      }
-      if (grow < N)
-        p.lse[static_cast<size_t>(bh) * N + grow] = l_sum > 0.f ? (m_used + ptx::lg2(l_sum)) * 0.69314718055994531f : -INFINITY;
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) pair::arrive_remote(&o_empty[wg], 0);
+      epilogue();   // (between sub-tile 0's empty steps instead: 1182 vs 1200 TFLOP/s causal N = 8k)
       if (threadIdx.x % 128 == 0) {
         fa2_tile_trace(p.trace, tn, wg, 2, fa2_gtime());
         fa2_tile_trace(p.trace, tn, wg, 3, clock64());
@@ -312,10 +345,18 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       int kslot = 0, vslot = 0;
       uint32_t kphase = 0, vphase = 0, s_iss = 0, p_cnt = 0, o_use = 0;
       int it = 0;
-      for (int t = pair_id; t < p.num_tiles; t += npairs, ++it) {
+      for (int n_ = 0, t; (t = tile_at(n_)) >= 0; ++n_, ++it) {
+        int bh, mb;
+        decode(t, bh, mb);
+        const int nb = nblk(mb, i), nkv = nblk(mb, 1);
         ptx::mbar_wait(&q_full[i], it & 1);
-        for (int j = -1; j < nkb; ++j) {
-          if (j + 1 < nkb) {   // S_i(j+1) = Q_i K_{j+1}^T once the softmax has read S_i(j)
+        for (int j = -1; j < nkv; ++j) {
+          if (CAUSAL && j + 1 >= nb && j + 1 < nkv) {   // sub-tile 0 skips this key block: release its K stage
+            ptx::mbar_wait(&k_full[kslot], kphase);
+            if (ptx::elect_one()) pair::commit_both(&k_empty[kslot]);
+            __syncwarp();
+            if (++kslot == STAGES) { kslot = 0; kphase ^= 1; }
+          } else if (j + 1 < nkv) {   // S_i(j+1) = Q_i K_{j+1}^T once the softmax has read S_i(j)
             ptx::mbar_wait(&k_full[kslot], kphase);
             if (s_iss > 0) pair::wait_cluster(&s_consumed[i], (s_iss - 1) & 1);
             ptx::tc_fence_after();
@@ -327,7 +368,7 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 pair::mma_ss2(tmem + i * 128, dQ + (offa >> 4), dK + (offb >> 4), IDESC_S, k > 0 ? 1u : 0u);
               }
               pair::commit_both(&s_full[i]);
-              if (j + 2 == nkb) pair::commit_both(&q_empty[i]);   // Q_i's last S
+              if (j + 2 == nb) pair::commit_both(&q_empty[i]);   // Q_i's last S
               pair::commit_both(&k_empty[kslot]);
             }
             __syncwarp();
@@ -338,6 +379,12 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
           if (j < 0) continue;
           // O_i += P~_i(j) V_j once both CTAs' softmax wrote P~_i(j)
           ptx::mbar_wait(&v_full[vslot], vphase);
+          if (CAUSAL && j >= nb) {   // skipped key block: release its V stage
+            if (ptx::elect_one()) pair::commit_both(&v_empty[vslot]);
+            __syncwarp();
+            if (++vslot == STAGES) { vslot = 0; vphase ^= 1; }
+            continue;
+          }
           if (j == 0) {
             if (o_use > 0) pair::wait_cluster(&o_empty[i], (o_use - 1) & 1);
             ++o_use;
@@ -368,8 +415,10 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       int slot = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = pair_id; t < p.num_tiles; t += npairs, ++it) {
-        const int bh = t / p.num_m_blocks, mb = t % p.num_m_blocks;
+      for (int n_ = 0, t; (t = tile_at(n_)) >= 0; ++n_, ++it) {
+        int bh, mb;
+        decode(t, bh, mb);
+        const int nkv = nblk(mb, 1);
         const int kvh = (bh % p.H) / p.group, b = bh / p.H;
         if (is_k) {
           for (int i = 0; i < 2; ++i) {
@@ -377,10 +426,10 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             if (rank == 0) ptx::mbar_arrive_expect_tx(&q_full[i], 2 * L::Q_TILE);
             for (int s = 0; s < 2; ++s)
               pair::tma_load_pair(sQ + i * L::Q_TILE + s * L::Q_BOX, &tm_q, &q_full[i], s * 64,
-                                  mb * 512 + static_cast<int>(rank) * 256 + i * 128, bh, pol_q);
+                                  row0_of(mb, i), bh, pol_q);
           }
         }
-        for (int j = 0; j < nkb; ++j) {
+        for (int j = 0; j < nkv; ++j) {
           ptx::mbar_wait(is_k ? &k_empty[slot] : &v_empty[slot], phase ^ 1);
           if (is_k) {   // key rows [128 j + 64 rank, +64), all d
             if (rank == 0) ptx::mbar_arrive_expect_tx(&k_full[slot], 2 * L::K_HALF);

@@ -19,6 +19,7 @@ SHAPES = [  # (B, H, N, d)
     (1, 2, 256, 128),
     (2, 2, 257, 64),
     (1, 2, 600, 128),
+    (1, 2, 1100, 128),    # three 512-row pair tiles, ragged (causal pair forward: empty steps, masks)
     (1, 1, 1000, 64),
     (1, 1, 2048, 128),
 ]
