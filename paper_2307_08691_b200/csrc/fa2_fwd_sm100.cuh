@@ -57,6 +57,18 @@ template <int D, bool FP8> struct FwdCfg {
   static constexpr int REG_OTHER = 56;
 };
 constexpr int kFwdEmuPairsD64 = FA2_FWD_EMU_PAIRS_D64;
+// d = 64, causal square: ping-pong of the two softmax warpgroups' exponential phases through
+// named barriers 1 / 2, as in the pair kernel (fa2_fwd2_sm100.cuh): S_{j+1} is issued as soon
+// as S_j was read, so nothing else keeps the two sub-tiles out of phase, and the causal tiles
+// (sub-tile 0 one block shorter) reset their phase every tile.  Causal N = 8k: 601-604 ->
+// 667-691 TFLOP/s; non-causal measured 3-5% slower with it (725-739 -> 697-724), so it stays
+// causal-only.
+#ifndef FA2_FWD_PINGPONG64
+#define FA2_FWD_PINGPONG64 1
+#endif
+#ifndef FA2_FWD_PP64_CH
+#define FA2_FWD_PP64_CH 2   // signal after this many of the four 32-column chunks
+#endif
 
 struct FwdParams {
   void* o;             // fixed: [B, H, N_q, D]; packed: [T_q, H, D] (dtype)
@@ -244,12 +256,24 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     const uint32_t tO = tmem + lane_base + TO0 + wg * D;
     uint32_t s_count = 0;   // completed waits on s_full[wg]
     uint32_t pv_count = 0;  // PV MMAs issued so far for this sub-tile (all tiles)
+    constexpr bool PP = SEP_P && CAUSAL && !GEN && !FP8 && FA2_FWD_PINGPONG64;
+    uint32_t gblk = 0;      // PP: key-block steps so far (incl. sub-tile 0's empty causal steps)
     const float sl2 = p.scale_log2;
     for (int n = 0, t; (t = tile_at(n)) >= 0; ++n) {
       int bh, mb;
       Seq sq;
       decode(t, bh, mb, sq);
       const int nb = n_blocks(sq, mb, wg);
+      const int nkv = max(n_blocks(sq, mb, 0), n_blocks(sq, mb, 1));
+      const bool last_tile = tile_at(n + 1) < 0;
+      // PP: wait for the partner warpgroup before a block's exponentials, signal it half-way
+      // (warpgroup 1 skips its very last signal: nobody waits for it)
+      auto pp_wait = [&]() {
+        if (PP && (wg == 1 || gblk > 0)) ptx::named_bar_sync(wg == 0 ? 2 : 1, 256);
+      };
+      auto pp_signal = [&](int j) {
+        if (PP && !(wg == 1 && last_tile && j + 1 == nkv)) ptx::named_bar_arrive(wg == 0 ? 1 : 2, 256);
+      };
       const int row0 = mb * 256 + wg * 128;
       const int grow = row0 + row;
       const bool ttr = threadIdx.x % 128 == 0;
@@ -261,6 +285,14 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         fa2_tile_trace(p.trace, n, wg, 6, fa2_smid());
       }
       if (nb == 0) {
+        // PP: sub-tile 1 past the sequence end still steps through the ping-pong
+        if constexpr (PP) {
+          for (int j = 0; j < nkv; ++j) {
+            pp_wait();
+            pp_signal(j);
+            ++gblk;
+          }
+        }
         // rows that see no key (R23): O = 0, L = -inf; no MMA work was scheduled
         if (grow < sq.nq) {
           uint4* dst = reinterpret_cast<uint4*>(
@@ -273,7 +305,13 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       }
       float m_used = -INFINITY;   // running max in log2 units (may lag the true max by <= 8)
       float l_sum = 0.f;
-      for (int j = 0; j < nb; ++j) {
+      for (int j = 0; j < (PP ? nkv : nb); ++j) {
+        if (PP && j >= nb) {   // causal: empty step of sub-tile 0 (one block fewer than sub-tile 1)
+          pp_wait();
+          pp_signal(j);
+          ++gblk;
+          continue;
+        }
         ptx::mbar_wait(&s_full[wg], s_count & 1);
         ++s_count;
         if (threadIdx.x % 128 == 0 && n == 0) FA2_TRACE(0, wg, j);
@@ -338,6 +376,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           uint32_t pk_all[COLS / 32][16];
 #pragma unroll
           for (int ch = 0; ch < COLS / 32; ++ch) {
+            if (ch == FA2_FWD_PP64_CH) pp_signal(j);
             uint32_t* pk = pk_all[ch];
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
@@ -371,6 +410,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
             for (int ch = 0; ch < COLS / 32; ++ch) ptx::tmem_st_x16(tP + ch * 16, pk_all[ch]);
           }
         };
+        pp_wait();
         if (need_mask) exp_block(std::integral_constant<int, 0>{});
         else exp_block(std::integral_constant<int, D == 64 ? kFwdEmuPairsD64 : kFwdEmuPairs>{});
         l_sum = l_sum * alpha + (rs2.x + rs2.y);
@@ -396,6 +436,7 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
         if (lane == 0) ptx::mbar_arrive(od_bar(p_full, wg, pv_count));
         if (threadIdx.x % 128 == 0 && n == 0) FA2_TRACE(3, wg, j);
         ++pv_count;
+        ++gblk;
       }
       // ---- epilogue: O = O / l, L = m + log l (natural log) ----
       ptx::mbar_wait(od_bar(o_done, wg, pv_count - 1), od_par(pv_count - 1));

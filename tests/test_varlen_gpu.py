@@ -102,12 +102,13 @@ def test_varlen_parity(case, d, causal, dtype):
 @pytest.mark.parametrize("d", [64, 128])
 @pytest.mark.parametrize("causal", [False, True])
 def test_varlen_equal_lengths_match_fixed_layout(causal, d):
-    """Equal lengths: the packed path computes what the [B,H,N,d] path does.  Causal:
-    the same one-SM forward kernel, forward bitwise.  Non-causal d = 128: the fixed
-    layout runs the CTA-pair forward, whose exponential split (2 of 16 pairs on the FMA
-    pipe instead of 4) and key-block split over the pair round P~ differently, so forward
-    to within a bf16 rounding step (d = 64: same kernel, compared the same way).  Backward
-    up to the dQ summation order (and the forward difference)."""
+    """Equal lengths: the packed path computes what the [B,H,N,d] path does.  Causal
+    d = 64: the same one-SM forward kernel, forward bitwise.  d = 128 (causal and not): the
+    fixed layout runs the CTA-pair forward, whose exponential split (2 of 16 pairs on the FMA
+    pipe instead of 4; masked blocks all on MUFU in both) and key-block split over the pair
+    round P~ differently, so forward to within a bf16 rounding step (non-causal d = 64: same
+    kernel, compared the same way).  Backward up to the dQ summation order (and the forward
+    difference)."""
     B, H, N = 3, 2, 300
     q, k, v, do = W.qkv(B, H, N, d, "bf16", seed=320)
     qc, kc, vc, doc = q.cuda(), k.cuda(), v.cuda(), do.cuda()
@@ -118,7 +119,7 @@ def test_varlen_equal_lengths_match_fixed_layout(causal, d):
     o2, lse2 = fa2.forward_varlen(pk(qc), pk(kc), pk(vc), cu, cu, N, N, causal=causal)
     dq2, dk2, dv2 = fa2.backward_varlen(pk(qc), pk(kc), pk(vc), o2, lse2, pk(doc), cu, cu, N, N, causal=causal)
     torch.cuda.synchronize()
-    if causal:
+    if causal and d == 64:
         assert torch.equal(pk(o), o2)
         assert torch.equal(lse.transpose(0, 1).reshape(H, B * N), lse2)
     else:
