@@ -288,7 +288,9 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
           }
           ptx::tmem_wait_st();
         }
+        if (tr) FA2_TRACE(6, wg, j);
         pp_wait();
+        if (tr) FA2_TRACE(7, wg, j);
         auto exp_block = [&](auto emu_tag) {
           constexpr int EMU = decltype(emu_tag)::value;
 #pragma unroll

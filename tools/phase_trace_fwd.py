@@ -1,5 +1,7 @@
 """Per-CTA block timeline of the forward's first work tile (every CTA; debug trace hook):
-period per key block, phase offset between the two softmax warpgroups, exp-phase length.
+period per key block, phase offset between the two softmax warpgroups, and the softmax
+sub-phases (pair kernel events: 0 S ready, 1 row max done, 6 P~ buffer free / O rescaled,
+7 ping-pong wait done, 2 exponentials done, 3 P~ handed over).
 usage: python tools/phase_trace_fwd.py D CAUSAL [N]"""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -21,20 +23,28 @@ fa2.forward(q, k, v, causal=causal)
 fa2.lib().fa2_debug_set_trace(None)
 torch.cuda.synchronize()
 t = tr.cpu().numpy()[65536:].reshape(148, 8, 2, 64).astype(np.float64)
-J = slice(8, 56)
+J = slice(8, 40)
 rows = []
+sub = {w: [] for w in (0, 1)}
 for c in range(148):
     e3 = t[c, 3]
-    if not (e3[0, 8:57] > 0).all() or not (e3[1, 8:57] > 0).all():
+    if not (e3[0, 8:41] > 0).all() or not (e3[1, 8:41] > 0).all():
         continue
-    per = np.mean(np.diff(e3[0, 8:57]))
+    per = np.mean(np.diff(e3[0, 8:41]))
     ph = np.mean(((e3[1, J] - e3[0, J]) % per) / per)
-    expl = [np.mean(t[c, 2, w, J] - t[c, 1, w, J]) for w in (0, 1)]
-    wait_s = [np.mean(t[c, 1, w, 9:57] - t[c, 3, w, 8:56]) for w in (0, 1)]   # arrive(j) -> top of j+1
-    rows.append((per, ph, expl[0], expl[1], wait_s[0], wait_s[1], c))
+    rows.append((per, ph, c))
+    for w in (0, 1):
+        ev = lambda e, lag=0: t[c, e, w, 8 + lag:40 + lag]
+        sub[w].append([np.mean(ev(0, 1) - ev(3)),   # arrive(j) -> S(j+1) seen
+                       np.mean(ev(1) - ev(0)),       # S seen -> max done
+                       np.mean(ev(6) - ev(1)),       # -> P~ buffer free (o_done) / rescale
+                       np.mean(ev(7) - ev(6)),       # ping-pong wait
+                       np.mean(ev(2) - ev(7)),       # exponentials
+                       np.mean(ev(3) - ev(2))])      # fence + arrive
 rows.sort()
-print(f"{len(rows)} CTAs traced; columns: period, phase(wg1-wg0)/period, exp0, exp1, arrive->next top 0/1, cta")
-for r in rows[:8] + [None] + rows[-8:]:
-    print("  ..." if r is None else "  %6.0f  %.2f  %6.0f %6.0f  %6.0f %6.0f  cta %d" % r)
-per = np.array([r[0] for r in rows]); ph = np.array([r[1] for r in rows])
-print("corr(period, |phase-0.5|) = %.2f" % np.corrcoef(per, np.abs(ph - 0.5))[0, 1])
+print(f"{len(rows)} CTAs; period min {rows[0][0]:.0f} median {rows[len(rows) // 2][0]:.0f} max {rows[-1][0]:.0f}; "
+      f"phase (wg1 - wg0) / period median {np.median([r[1] for r in rows]):.2f}")
+for w in (0, 1):
+    m = np.mean(np.array(sub[w]), axis=0) if sub[w] else np.zeros(6)
+    print(f"wg{w} sub-phases (cycles): arrive->S seen {m[0]:.0f} | ld+max {m[1]:.0f} | o_done/rescale {m[2]:.0f} | "
+          f"pp wait {m[3]:.0f} | exps {m[4]:.0f} | fence+arrive {m[5]:.0f}")
