@@ -17,9 +17,9 @@ if [[ $WHAT == all || $WHAT == bench ]]; then
 fi
 if [[ $WHAT == all || $WHAT == ncu ]]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/${TAG}_launches.csv \
-     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/${TAG}_ncu_bench.log 2>&1; echo "ncu launches exit $?"
+     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-tables --no-check > $OUT/${TAG}_ncu_bench.log 2>&1; echo "ncu launches exit $?"
   timeout 900 ncu --set full --clock-control none --import-source on -k "regex:fa2_bwd.*kernel" -s 3 -c 1 -o $OUT/${TAG}_prof_bwd \
-     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/${TAG}_ncu_bwd.log 2>&1; echo "ncu bwd exit $?"
+     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-tables --no-check > $OUT/${TAG}_ncu_bwd.log 2>&1; echo "ncu bwd exit $?"
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:fa2_fwd -s 3 -c 1 -o $OUT/${TAG}_prof_fwd \
-     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/${TAG}_ncu_fwd.log 2>&1; echo "ncu fwd exit $?"
+     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-tables --no-check > $OUT/${TAG}_ncu_fwd.log 2>&1; echo "ncu fwd exit $?"
 fi

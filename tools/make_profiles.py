@@ -34,7 +34,8 @@ def to_bytes(unit, val):
 
 # algorithmic FLOPs per launch at the bench workload (B=2, H=16, N=8192, d=128, non-causal;
 # paper count P:617-625): forward 4 N^2 d B H, backward 2.5x that
-FLOPS = {"fwd": 4.0 * 8192 ** 2 * 128 * 32, "bwd": 2.5 * 4.0 * 8192 ** 2 * 128 * 32}
+FLOPS = {"fwd": 4.0 * 8192 ** 2 * 128 * 32, "bwd": 2.5 * 4.0 * 8192 ** 2 * 128 * 32,
+         "fwdc": 2.0 * 8192 ** 2 * 128 * 32}   # causal forward: half the score matrix
 
 
 def summarise(rep, name, key=None):
@@ -96,14 +97,15 @@ if __name__ == "__main__":
         parts += ["## Launch list (our kernels)", "", launches(lf)]
     traffic = {}
     for key, label in (("fwd", "forward (fa2_fwd_pair_kernel, CTA pair)"), ("bwd", "backward main (fa2_bwd_pair_kernel, CTA pair)"),
+                       ("fwdc", "causal forward (fa2_fwd_pair_kernel<., true>, CTA pair; `bench.py --causal 1`)"),
                        ("pre", "fa2_bwd_preprocess"), ("dq", "dQ convert")):
-        rep = os.path.join(g, f"{tag}_prof_{key}.ncu-rep")
+        rep = os.path.join(g, f"{tag}_prof_{'fwd_causal' if key == 'fwdc' else key}.ncu-rep")
         if os.path.exists(rep):
             md, t = summarise(rep, label, key)
             parts += [md]
-            traffic[{"fwd": "fwd", "bwd": "bwd_main", "pre": "bwd_pre", "dq": "bwd_dq"}[key]] = t
+            traffic[{"fwd": "fwd", "bwd": "bwd_main", "fwdc": "fwd_causal", "pre": "bwd_pre", "dq": "bwd_dq"}[key]] = t
             h, u, v = raw(rep)
-            if "Kernel Name" in h:   # also keyed by the kernel's short name (bench.py looks that up first)
+            if "Kernel Name" in h and key != "fwdc":   # also keyed by the kernel's short name (bench.py looks that up first)
                 traffic[v[h.index("Kernel Name")].split("(")[0].split("<")[0].replace("void ", "").replace("fa2::", "")] = t
     open(out_md, "w").write("\n".join(parts))
     json.dump({"tag": tag, **traffic}, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)

@@ -23,7 +23,7 @@ fa2.forward(q, k, v, causal=causal)
 fa2.lib().fa2_debug_set_trace(None)
 torch.cuda.synchronize()
 t = tr.cpu().numpy()[65536:].reshape(148, 8, 2, 64).astype(np.float64)
-J = slice(8, 40)
+J = slice(8, 40)  # steady-state blocks of the first tile
 rows = []
 sub = {w: [] for w in (0, 1)}
 for c in range(148):
@@ -48,3 +48,17 @@ for w in (0, 1):
     m = np.mean(np.array(sub[w]), axis=0) if sub[w] else np.zeros(6)
     print(f"wg{w} sub-phases (cycles): arrive->S seen {m[0]:.0f} | ld+max {m[1]:.0f} | o_done/rescale {m[2]:.0f} | "
           f"pp wait {m[3]:.0f} | exps {m[4]:.0f} | fence+arrive {m[5]:.0f}")
+# MMA side (leader CTAs; issuer i = sub-tile i): P~ handed over -> issuer sees it (ev3 -> ev4),
+# P~V issued -> softmax sees it complete (ev4[j] -> ev6[j + 1]), S(j+1) issued -> S seen (ev5 -> ev0)
+lat = {w: [] for w in (0, 1)}
+for c in range(0, 148, 2):
+    for w in (0, 1):
+        e = lambda ev, lag=0: t[c, ev, w, 8 + lag:40 + lag]
+        if not (e(4) > 0).all() or not (e(6, 1) > 0).all():
+            continue
+        lat[w].append([np.mean(e(4) - e(3)), np.mean(e(6, 1) - e(4)), np.mean(e(0, 1) - e(5, 1))])
+for w in (0, 1):
+    if lat[w]:
+        m = np.mean(np.array(lat[w]), axis=0)
+        print(f"sub-tile {w} (leader CTAs): p_full -> issuer sees {m[0]:.0f} | P~V issued -> o_done seen by softmax "
+              f"{m[1]:.0f} | S issued -> s_full seen {m[2]:.0f}")

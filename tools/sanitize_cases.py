@@ -28,7 +28,7 @@ for d in (64, 128):
     q3, k3, v3, do3 = (mk(1, 3, 1500, d) for _ in range(4))
     o3, l3 = fa2.forward(q3, k3, v3, causal=True)
     fa2.backward(q3, k3, v3, o3, l3, do3, causal=True)
-    # square MHA shapes: the CTA-pair forward (non-causal d = 128) and the CTA-pair backward
+    # square MHA shapes: the CTA-pair forward (d = 128, causal and not) and the CTA-pair backward
     # (d = 128, causal and not), ragged (700 = 2 pair key blocks + a 188-row tail)
     for causal in (False, True):
         q4, k4, v4, do4 = (mk(1, 2, 700, d) for _ in range(4))
