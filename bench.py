@@ -429,8 +429,11 @@ def run_ours(args, world, rank, local):
     roofline = {"bound": "tensor", "kernel": names[dominant],
                 "achieved": round(achieved, 1), "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
                 "frac": round(achieved / peaks["bf16_tflops"], 4), "traffic": traffic,
-                "peak_source": peaks["source"] + ", burst bf16 GEMM (the timed region runs at max SM clock, "
-                               "see clocks; fp16 has the same nominal tensor rate)",
+                "peak_source": peaks["source"] + ", burst bf16 GEMM (the conservative choice: the timed region "
+                               "is ~0.2 s and the SM clock under it is in `clocks`; against the sustained figure "
+                               f"{peaks.get('bf16_tflops_sustained')} the fraction is "
+                               f"{(achieved / peaks['bf16_tflops_sustained']) if peaks.get('bf16_tflops_sustained') else float('nan'):.3f}; "
+                               "fp16 has the same nominal tensor rate)",
                 "algorithmic_flops_per_launch": dom_fl,
                 "kernels": names,
                 "kernel_ms": {kk: round(vv, 4) for kk, vv in k_avg.items()},
