@@ -361,17 +361,18 @@ fa2_status_t dispatch_fwd_causal(bool causal, const CUtensorMap& mq, const CUten
 #ifndef FA2_FWD_PAIR_CAUSAL
 #define FA2_FWD_PAIR_CAUSAL 1   // 0: causal square d = 128 on the one-SM kernel (A/B builds)
 #endif
-// Pair forward (causal, square): tile t = (head, 512-row block mb = nmb - 1 - t % nmb), work =
-// key blocks of its two sub-tiles (sub-tile i: 4 mb + 2 i + 2, at most T_c) + 2 (prologue /
-// epilogue); one list per CTA pair.
+// Pair forward (causal, fixed layout, N_q <= N_k): tile t = (head, 512-row block mb = nmb - 1 -
+// t % nmb), work = key blocks of its two sub-tiles (sub-tile i: the blocks up to its last row +
+// N_k - N_q, at most T_c) + 2 (prologue / epilogue); one list per CTA pair.
 SchedPtr fwd_pair_sched(const fa2::FwdParams& p, int npairs) {
-  const int nmb = p.num_m_blocks, N = p.geom.Nq;
-  return cached_sched(3, p.num_tiles, nmb, N, 1, npairs, [&](std::vector<int>& work) {
-    const int nkb = (N + 127) / 128;
+  const int nmb = p.num_m_blocks, N = p.geom.Nq, Nk = p.geom.Nk;
+  // (N_k rides in the cache key's heads-per-tile slot, which the forward schedules leave at 1)
+  return cached_sched(3, p.num_tiles, nmb, N, Nk, npairs, [&](std::vector<int>& work) {
+    const int nkb = (Nk + 127) / 128, off = Nk - N;
     for (int t = 0; t < p.num_tiles; ++t) {
       const int mb = nmb - 1 - t % nmb;
       work[t] = 2;
-      for (int i = 0; i < 2; ++i) work[t] += std::min(nkb, (mb * 512 + i * 256 + 255) / 128 + 1);
+      for (int i = 0; i < 2; ++i) work[t] += std::min(nkb, (mb * 512 + i * 256 + 255 + off) / 128 + 1);
     }
   });
 }
@@ -417,7 +418,9 @@ fa2_status_t forward_impl(const void* q, const void* k, const void* v, void* o, 
   const CUtensorMapDataType dt = tma_dtype(dtype);
   fa2_status_t s;
   if ((s = make_rows_map(&mq, q, dt, g, g.H, true)) != FA2_OK) return s;
-  const bool pair = FA2_FWD_PAIR && (!causal || FA2_FWD_PAIR_CAUSAL) && g.d == 128 && !g.packed && g.Nq == g.Nk;
+  // CTA pair: fixed layout, d = 128; N_q != N_k too, except causal N_q > N_k (rows without a
+  // visible key, R23: the one-SM GEN kernel writes their O = 0, L = -inf)
+  const bool pair = FA2_FWD_PAIR && (!causal || (FA2_FWD_PAIR_CAUSAL && g.Nq <= g.Nk)) && g.d == 128 && !g.packed;
   if ((s = make_rows_map(&mk, k, dt, g, g.Hkv, false, 2, pair ? 64 : 128)) != FA2_OK) return s;
   if ((s = make_rows_map(&mv, v, dt, g, g.Hkv, false)) != FA2_OK) return s;
   fa2::FwdParams p;

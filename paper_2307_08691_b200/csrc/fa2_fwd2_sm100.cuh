@@ -1,5 +1,6 @@
-// FlashAttention-2 forward (Alg. 1) on a CTA pair (cta_group::2):
-// the non-causal, square, d = 128, bf16/fp16 path (the paper's benchmark shape).
+// FlashAttention-2 forward (Alg. 1) on a CTA pair (cta_group::2): the
+// d = 128, bf16/fp16, fixed-layout path (the paper's benchmark shapes; also N_q != N_k, causal
+// with N_q <= N_k).
 //
 // Why a pair: on one SM the chain softmax_i -> P~V_i -> S_i ->
 // softmax_i bounds the forward, and breaking it needs P~ outside the S columns -- TMEM
@@ -145,8 +146,11 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
   pair::cluster_sync();   // barriers initialised and TMEM allocated in both CTAs
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int N = p.geom.Nq;
-  const int nkb = (N + 127) / 128;
+  // N_q query rows, N_k key rows (fixed layout; N_q != N_k is served for non-causal calls and
+  // for causal ones with N_q <= N_k, where the bottom-right offset N_k - N_q >= 0 leaves every
+  // row a visible key: R22)
+  const int N = p.geom.Nq, Nk = p.geom.Nk, off = Nk - N;
+  const int nkb = (Nk + 127) / 128;
   // work tiles (shared by all roles): n-th tile of this pair, its head and 512-row block
   auto tile_at = [&](int n) { return pair::sched_tile_pair(sched, n, p.num_tiles, pair_id, npairs); };
   auto decode = [&](int t, int& bh, int& mb) {
@@ -158,7 +162,7 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
   auto row0_of = [&](int mb, int i) {
     return CAUSAL ? mb * 512 + i * 256 + static_cast<int>(rank) * 128 : mb * 512 + static_cast<int>(rank) * 256 + i * 128;
   };
-  auto nblk = [&](int mb, int i) { return CAUSAL ? min(nkb, (mb * 512 + i * 256 + 255) / 128 + 1) : nkb; };
+  auto nblk = [&](int mb, int i) { return CAUSAL ? min(nkb, (mb * 512 + i * 256 + 255 + off) / 128 + 1) : nkb; };
 
   if (warp < 8) {
     // ======================= softmax warpgroups =======================
@@ -249,9 +253,9 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         const int c0 = j * 128;
         // ragged key tail; causal: blocks past the first row's diagonal (fully masked rows of
         // CTA 0 keep m: block 0 always holds a visible key, so m is finite by then)
-        const bool need_mask = c0 + 128 > N || (CAUSAL && c0 + 127 > r0);
+        const bool need_mask = c0 + 128 > Nk || (CAUSAL && c0 + 127 > r0 + off);
         if (need_mask) {
-          const int lim = CAUSAL ? min(N - 1, grow) : N - 1;
+          const int lim = CAUSAL ? min(Nk - 1, grow + off) : Nk - 1;
 #pragma unroll
           for (int c = 0; c < 128; ++c)
             if (c0 + c > lim) s[c] = -INFINITY;
