@@ -372,16 +372,19 @@ SchedPtr fwd_pair_sched(const fa2::FwdParams& p, int npairs) {
     for (int t = 0; t < p.num_tiles; ++t) {
       const int mb = nmb - 1 - t % nmb;
       work[t] = 2;
-      for (int i = 0; i < 2; ++i) work[t] += std::min(nkb, (mb * 512 + i * 256 + 255 + off) / 128 + 1);
+      for (int i = 0; i < 2; ++i) {
+        const int last = std::min(N - 1, mb * 512 + i * 256 + 255) + off;
+        work[t] += last < 0 ? 0 : std::min(nkb, last / 128 + 1);
+      }
     }
   });
 }
 
 // CTA-pair forward (fa2_fwd2_sm100.cuh): square fixed-length, d = 128, bf16/fp16
-template <bool BF16, bool CAUSAL>
+template <bool BF16, bool CAUSAL, bool GEN>
 fa2_status_t launch_fwd_pair(const CUtensorMap& mq, const CUtensorMap& mk64, const CUtensorMap& mv,
                              fa2::FwdParams p, int sms, cudaStream_t st) {
-  auto kern = fa2::fa2_fwd_pair_kernel<BF16, CAUSAL>;
+  auto kern = fa2::fa2_fwd_pair_kernel<BF16, CAUSAL, GEN>;
   constexpr int smem = fa2::FwdPairSmem::ALLOC;
   fa2_status_t s = set_smem(kern, smem);
   if (s != FA2_OK) return s;
@@ -393,7 +396,7 @@ fa2_status_t launch_fwd_pair(const CUtensorMap& mq, const CUtensorMap& mk64, con
   int grid = 2 * p.num_tiles < sms ? 2 * p.num_tiles : sms;
   grid &= ~1;
   if (grid > 2 * max_clusters) grid = 2 * max_clusters;
-  if constexpr (CAUSAL) {
+  if constexpr (CAUSAL && !GEN) {
     if (FA2_SCHED && p.num_tiles <= fa2::kSchedMaxTiles && grid / 2 <= fa2::kSchedMaxCtas) {
       const SchedPtr sc = fwd_pair_sched(p, grid / 2);
       mark(0, st);
@@ -403,7 +406,7 @@ fa2_status_t launch_fwd_pair(const CUtensorMap& mq, const CUtensorMap& mk64, con
       return FA2_OK;
     }
   }
-  fa2::SchedT<CAUSAL> sched;
+  fa2::SchedT<CAUSAL && !GEN> sched;
   sched.n = 0;
   mark(0, st);
   kern<<<grid, 384, smem, st>>>(mq, mk64, mv, p, sched);
@@ -418,9 +421,8 @@ fa2_status_t forward_impl(const void* q, const void* k, const void* v, void* o, 
   const CUtensorMapDataType dt = tma_dtype(dtype);
   fa2_status_t s;
   if ((s = make_rows_map(&mq, q, dt, g, g.H, true)) != FA2_OK) return s;
-  // CTA pair: fixed layout, d = 128; N_q != N_k too, except causal N_q > N_k (rows without a
-  // visible key, R23: the one-SM GEN kernel writes their O = 0, L = -inf)
-  const bool pair = FA2_FWD_PAIR && (!causal || (FA2_FWD_PAIR_CAUSAL && g.Nq <= g.Nk)) && g.d == 128 && !g.packed;
+  // CTA pair: every d = 128 bf16/fp16 forward (fixed layout incl. N_q != N_k, and packed varlen)
+  const bool pair = FA2_FWD_PAIR && (!causal || FA2_FWD_PAIR_CAUSAL) && g.d == 128;
   if ((s = make_rows_map(&mk, k, dt, g, g.Hkv, false, 2, pair ? 64 : 128)) != FA2_OK) return s;
   if ((s = make_rows_map(&mv, v, dt, g, g.Hkv, false)) != FA2_OK) return s;
   fa2::FwdParams p;
@@ -445,8 +447,12 @@ fa2_status_t forward_impl(const void* q, const void* k, const void* v, void* o, 
   p.trace = g_trace;
   const bool bf16 = dtype == FA2_BF16;
   if (pair) {
-    if (causal) return bf16 ? launch_fwd_pair<true, true>(mq, mk, mv, p, sms, st) : launch_fwd_pair<false, true>(mq, mk, mv, p, sms, st);
-    return bf16 ? launch_fwd_pair<true, false>(mq, mk, mv, p, sms, st) : launch_fwd_pair<false, false>(mq, mk, mv, p, sms, st);
+    if (g.packed) {
+      if (causal) return bf16 ? launch_fwd_pair<true, true, true>(mq, mk, mv, p, sms, st) : launch_fwd_pair<false, true, true>(mq, mk, mv, p, sms, st);
+      return bf16 ? launch_fwd_pair<true, false, true>(mq, mk, mv, p, sms, st) : launch_fwd_pair<false, false, true>(mq, mk, mv, p, sms, st);
+    }
+    if (causal) return bf16 ? launch_fwd_pair<true, true, false>(mq, mk, mv, p, sms, st) : launch_fwd_pair<false, true, false>(mq, mk, mv, p, sms, st);
+    return bf16 ? launch_fwd_pair<true, false, false>(mq, mk, mv, p, sms, st) : launch_fwd_pair<false, false, false>(mq, mk, mv, p, sms, st);
   }
   if (g.d == 64)
     s = bf16 ? dispatch_fwd_causal<64, true>(causal, mq, mk, mv, p, sms, st)

@@ -84,11 +84,15 @@ struct FwdPairSmem {
 // fewer; its warpgroup runs them as empty ping-pong steps (no S, no exponentials, no P~V,
 // its issuer only releases their K/V stages) so the two warpgroups keep alternating.  Tiles
 // come heaviest first from the host's balanced pair schedule (fa2_seq.cuh TileSched).
-template <bool BF16, bool CAUSAL>
+// GEN: the packed variable-length layout (fa2_seq.cuh): every tile resolves its sequence (first
+// rows, N_q, N_k, causal offset N_k - N_q); tiles past a sequence's rows are skipped by every
+// role, sub-tiles whose rows see no key (N_k = 0, or causal N_q > N_k) write O = 0, L = -inf (R23)
+// and step through the ping-pong empty.
+template <bool BF16, bool CAUSAL, bool GEN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k64,
                     const __grid_constant__ CUtensorMap tm_v, const FwdParams p,
-                    const __grid_constant__ SchedT<CAUSAL> sched) {
+                    const __grid_constant__ SchedT<CAUSAL && !GEN> sched) {
   using L = FwdPairSmem;
   constexpr int D = 128, STAGES = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -146,23 +150,48 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
   pair::cluster_sync();   // barriers initialised and TMEM allocated in both CTAs
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // N_q query rows, N_k key rows (fixed layout; N_q != N_k is served for non-causal calls and
-  // for causal ones with N_q <= N_k, where the bottom-right offset N_k - N_q >= 0 leaves every
-  // row a visible key: R22)
-  const int N = p.geom.Nq, Nk = p.geom.Nk, off = Nk - N;
-  const int nkb = (Nk + 127) / 128;
+  // fixed layout: N_q query rows, N_k key rows, bottom-right causal offset N_k - N_q (R22)
   // work tiles (shared by all roles): n-th tile of this pair, its head and 512-row block
   auto tile_at = [&](int n) { return pair::sched_tile_pair(sched, n, p.num_tiles, pair_id, npairs); };
-  auto decode = [&](int t, int& bh, int& mb) {
-    bh = t / p.num_m_blocks;
-    const int r = t % p.num_m_blocks;
-    mb = CAUSAL ? p.num_m_blocks - 1 - r : r;   // causal: heavy row blocks first in the tile order
+  // A work tile as every role sees it: head, 512-row block, its sequence's geometry
+  struct PairFwdTile {
+    int bh, mb, h, b;
+    int q0, k0, nq, nk, off;   // first query / key row of the sequence in its tensor, lengths, offset
   };
+  auto decode = [&](int t) {
+    PairFwdTile w;
+    w.bh = t / p.num_m_blocks;
+    const int r = t % p.num_m_blocks;
+    w.mb = CAUSAL ? p.num_m_blocks - 1 - r : r;   // causal: heavy row blocks first in the tile order
+    w.h = w.bh % p.H;
+    w.b = w.bh / p.H;
+    if constexpr (GEN) {
+      const Seq sq = seq_of<true>(p.geom, w.b);
+      w.q0 = sq.q0; w.k0 = sq.k0; w.nq = sq.nq; w.nk = sq.nk;
+    } else {
+      w.q0 = 0; w.k0 = 0; w.nq = p.geom.Nq; w.nk = p.geom.Nk;
+    }
+    w.off = w.nk - w.nq;
+    return w;
+  };
+  auto tile_empty = [&](const PairFwdTile& w) { return GEN && w.mb * 512 >= w.nq; };
   // first row of this CTA's sub-tile i, and the key blocks sub-tile i visits (both CTAs)
   auto row0_of = [&](int mb, int i) {
     return CAUSAL ? mb * 512 + i * 256 + static_cast<int>(rank) * 128 : mb * 512 + static_cast<int>(rank) * 256 + i * 128;
   };
-  auto nblk = [&](int mb, int i) { return CAUSAL ? min(nkb, (mb * 512 + i * 256 + 255 + off) / 128 + 1) : nkb; };
+  // key blocks sub-tile i visits (both CTAs): all of N_k, causal up to its last row's diagonal
+  auto nblk = [&](const PairFwdTile& w, int i) -> int {
+    const int nkb = (w.nk + 127) / 128;
+    if (!CAUSAL) return nkb;
+    const int last = min(w.nq - 1, w.mb * 512 + i * 256 + 255) + w.off;
+    return last < 0 ? 0 : min(nkb, last / 128 + 1);
+  };
+  // the next tile of this pair that is not skipped (-1: none)
+  auto next_tile = [&](int n) {
+    int t;
+    while ((t = tile_at(n)) >= 0 && tile_empty(decode(t))) ++n;
+    return t;
+  };
 
   if (warp < 8) {
     // ======================= softmax warpgroups =======================
@@ -177,13 +206,17 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     uint32_t s_count = 0, pv_count = 0, gblk = 0;   // gblk: key blocks stepped (incl. empty steps)
     const float sl2 = p.scale_log2;
     for (int tn = 0, t; (t = tile_at(tn)) >= 0; ++tn) {
-      int bh, mb;
-      decode(t, bh, mb);
+      const PairFwdTile w = decode(t);
+      if (tile_empty(w)) continue;
+      const int mb = w.mb, nq = w.nq, nk = w.nk, off = w.off;
       const int r0 = row0_of(mb, wg), grow = r0 + row;
-      const int nb = nblk(mb, wg), nkv = nblk(mb, 1);
+      const int nb = nblk(w, wg), nkv = nblk(w, 1);
       float m_used = -INFINITY, l_sum = 0.f;
       const bool tr = threadIdx.x % 128 == 0 && tn == 0;
-      const bool last_tile = tile_at(tn + 1) < 0;
+      const bool last_tile = next_tile(tn + 1) < 0;
+      // this row of O and L in the output tensors
+      const long long o_off = static_cast<long long>(w.b) * p.o_bs + w.h * p.o_hs + static_cast<long long>(w.q0 + grow) * p.o_rs;
+      const long long l_off = static_cast<long long>(w.b) * p.l_bs + w.h * p.l_hs + w.q0 + grow;
       // ping-pong: wait for the partner warpgroup before this block's exponentials, signal it
       // FA2_FWD_PP_C chunks in (warpgroup 1 skips its very last signal: nobody waits for it)
       auto pp_wait = [&]() {
@@ -204,7 +237,7 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         ptx::mbar_wait(&o_done[wg], (pv_count - 1) & 1);
         ptx::tc_fence_after();
         const float inv_l = l_sum > 0.f ? 1.f / l_sum : 0.f;
-        uint8_t* orow = reinterpret_cast<uint8_t*>(p.o) + (static_cast<size_t>(bh) * N + grow) * D * 2;
+        uint8_t* orow = reinterpret_cast<uint8_t*>(p.o) + o_off * 2;
 #pragma unroll
         for (int ch = 0; ch < D / 32; ++ch) {
           uint32_t o[32];
@@ -214,20 +247,33 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 #pragma unroll
           for (int e = 0; e < 16; ++e)
             q[e] = ptx::pack2<BF16>(__uint_as_float(o[2 * e]) * inv_l, __uint_as_float(o[2 * e + 1]) * inv_l);
-          if (grow < N) {
+          if (grow < nq) {
             uint4* dst = reinterpret_cast<uint4*>(orow + ch * 64);
 #pragma unroll
             for (int e = 0; e < 4; ++e) dst[e] = make_uint4(q[4 * e], q[4 * e + 1], q[4 * e + 2], q[4 * e + 3]);
           }
         }
-        if (grow < N)
-          p.lse[static_cast<size_t>(bh) * N + grow] = l_sum > 0.f ? (m_used + ptx::lg2(l_sum)) * 0.69314718055994531f : -INFINITY;
+        if (grow < nq) p.lse[l_off] = l_sum > 0.f ? (m_used + ptx::lg2(l_sum)) * 0.69314718055994531f : -INFINITY;
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) pair::arrive_remote(&o_empty[wg], 0);
       };
+      if (nb == 0) {   // no row of this sub-tile sees a key (R23): O = 0, L = -inf; no MMA work
+        for (int j = 0; j < nkv; ++j) {
+          pp_wait();
+          pp_signal(j);
+          ++gblk;
+        }
+        if (grow < nq) {
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(p.o) + o_off * 2);
+#pragma unroll
+          for (int e = 0; e < D / 8; ++e) dst[e] = make_uint4(0u, 0u, 0u, 0u);
+          p.lse[l_off] = -INFINITY;
+        }
+        continue;
+      }
       for (int j = 0; j < nkv; ++j) {
-        if (CAUSAL && j >= nb) {   // empty step of sub-tile 0 (its rows see none of these keys)
+        if (j >= nb) {   // empty step of sub-tile 0 (its rows see none of these keys)
           pp_wait();
           pp_signal(j);
           ++gblk;
@@ -253,9 +299,9 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         const int c0 = j * 128;
         // ragged key tail; causal: blocks past the first row's diagonal (fully masked rows of
         // CTA 0 keep m: block 0 always holds a visible key, so m is finite by then)
-        const bool need_mask = c0 + 128 > Nk || (CAUSAL && c0 + 127 > r0 + off);
+        const bool need_mask = c0 + 128 > nk || (CAUSAL && c0 + 127 > r0 + off);
         if (need_mask) {
-          const int lim = CAUSAL ? min(Nk - 1, grow + off) : Nk - 1;
+          const int lim = CAUSAL ? min(nk - 1, grow + off) : nk - 1;
 #pragma unroll
           for (int c = 0; c < 128; ++c)
             if (c0 + c > lim) s[c] = -INFINITY;
@@ -351,13 +397,18 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       int kslot = 0, vslot = 0;
       uint32_t kphase = 0, vphase = 0, s_iss = 0, p_cnt = 0, o_use = 0;
       int it = 0;
-      for (int n_ = 0, t; (t = tile_at(n_)) >= 0; ++n_, ++it) {
-        int bh, mb;
-        decode(t, bh, mb);
-        const int nb = nblk(mb, i), nkv = nblk(mb, 1);
+      for (int n_ = 0, t; (t = tile_at(n_)) >= 0; ++n_) {
+        const PairFwdTile w = decode(t);
+        if (tile_empty(w)) continue;
+        const int nb = nblk(w, i), nkv = nblk(w, 1);
         ptx::mbar_wait(&q_full[i], it & 1);
+        ++it;
+        if (nb == 0) {   // no row of sub-tile i sees a key: release Q_i now
+          if (ptx::elect_one()) pair::commit_both(&q_empty[i]);
+          __syncwarp();
+        }
         for (int j = -1; j < nkv; ++j) {
-          if (CAUSAL && j + 1 >= nb && j + 1 < nkv) {   // sub-tile 0 skips this key block: release its K stage
+          if (j + 1 >= nb && j + 1 < nkv) {   // sub-tile i skips this key block: release its K stage
             ptx::mbar_wait(&k_full[kslot], kphase);
             if (ptx::elect_one()) pair::commit_both(&k_empty[kslot]);
             __syncwarp();
@@ -378,14 +429,14 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
               pair::commit_both(&k_empty[kslot]);
             }
             __syncwarp();
-            if (it == 0) FA2_TRACE(5, i, j + 1);
+            if (it == 1) FA2_TRACE(5, i, j + 1);
             ++s_iss;
             if (++kslot == STAGES) { kslot = 0; kphase ^= 1; }
           }
           if (j < 0) continue;
           // O_i += P~_i(j) V_j once both CTAs' softmax wrote P~_i(j)
           ptx::mbar_wait(&v_full[vslot], vphase);
-          if (CAUSAL && j >= nb) {   // skipped key block: release its V stage
+          if (j >= nb) {   // skipped key block: release its V stage
             if (ptx::elect_one()) pair::commit_both(&v_empty[vslot]);
             __syncwarp();
             if (++vslot == STAGES) { vslot = 0; vphase ^= 1; }
@@ -397,7 +448,7 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
           }
           pair::wait_cluster(&p_full[i], p_cnt & 1);
           ++p_cnt;
-          if (it == 0) FA2_TRACE(4, i, j);
+          if (it == 1) FA2_TRACE(4, i, j);
           ptx::tc_fence_after();
           if (ptx::elect_one()) {
 #pragma unroll
@@ -421,31 +472,36 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       int slot = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int n_ = 0, t; (t = tile_at(n_)) >= 0; ++n_, ++it) {
-        int bh, mb;
-        decode(t, bh, mb);
-        const int nkv = nblk(mb, 1);
-        const int kvh = (bh % p.H) / p.group, b = bh / p.H;
+      // rows [row, row + box) of head `head` (of `heads`) at column c: fixed {d, N, B*heads},
+      // packed {d, heads, T} (fa2_seq.cuh)
+      auto load = [&](void* dst, const CUtensorMap* m, uint64_t* bar, int c, int row, int head, int heads, int b) {
+        if constexpr (GEN) pair::tma_load_pair(dst, m, bar, c, head, row, m == &tm_q ? pol_q : pol_kv);
+        else pair::tma_load_pair(dst, m, bar, c, row, b * heads + head, m == &tm_q ? pol_q : pol_kv);
+      };
+      for (int n_ = 0, t; (t = tile_at(n_)) >= 0; ++n_) {
+        const PairFwdTile w = decode(t);
+        if (tile_empty(w)) continue;
+        const int mb = w.mb, nkv = nblk(w, 1);
+        const int kvh = w.h / p.group, b = w.b;
         if (is_k) {
           for (int i = 0; i < 2; ++i) {
             if (it > 0) ptx::mbar_wait(&q_empty[i], (it - 1) & 1);
             if (rank == 0) ptx::mbar_arrive_expect_tx(&q_full[i], 2 * L::Q_TILE);
             for (int s = 0; s < 2; ++s)
-              pair::tma_load_pair(sQ + i * L::Q_TILE + s * L::Q_BOX, &tm_q, &q_full[i], s * 64,
-                                  row0_of(mb, i), bh, pol_q);
+              load(sQ + i * L::Q_TILE + s * L::Q_BOX, &tm_q, &q_full[i], s * 64, w.q0 + row0_of(mb, i), w.h, p.H, b);
           }
         }
+        ++it;
         for (int j = 0; j < nkv; ++j) {
           ptx::mbar_wait(is_k ? &k_empty[slot] : &v_empty[slot], phase ^ 1);
           if (is_k) {   // key rows [128 j + 64 rank, +64), all d
             if (rank == 0) ptx::mbar_arrive_expect_tx(&k_full[slot], 2 * L::K_HALF);
             for (int s = 0; s < 2; ++s)
-              pair::tma_load_pair(sK + slot * L::K_HALF + s * L::K_BOX, &tm_k64, &k_full[slot], s * 64,
-                                  j * 128 + static_cast<int>(rank) * 64, b * p.Hkv + kvh, pol_kv);
+              load(sK + slot * L::K_HALF + s * L::K_BOX, &tm_k64, &k_full[slot], s * 64,
+                   w.k0 + j * 128 + static_cast<int>(rank) * 64, kvh, p.Hkv, b);
           } else {      // key rows [128 j, +128), head-dim columns [64 rank, +64)
             if (rank == 0) ptx::mbar_arrive_expect_tx(&v_full[slot], 2 * L::V_HALF);
-            pair::tma_load_pair(sV + slot * L::V_HALF, &tm_v, &v_full[slot], static_cast<int>(rank) * 64, j * 128,
-                                b * p.Hkv + kvh, pol_kv);
+            load(sV + slot * L::V_HALF, &tm_v, &v_full[slot], static_cast<int>(rank) * 64, w.k0 + j * 128, kvh, p.Hkv, b);
           }
           if (++slot == STAGES) { slot = 0; phase ^= 1; }
         }
