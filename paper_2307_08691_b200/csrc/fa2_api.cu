@@ -458,8 +458,14 @@ fa2_status_t forward_impl(const void* q, const void* k, const void* v, void* o, 
     s = bf16 ? dispatch_fwd_causal<64, true>(causal, mq, mk, mv, p, sms, st)
              : dispatch_fwd_causal<64, false>(causal, mq, mk, mv, p, sms, st);
   else
+#if !FA2_FWD_PAIR || !FA2_FWD_PAIR_CAUSAL
+    // (d = 128 on the one-SM kernel: A/B builds without the pair forward only; the product
+    // build instantiates it for FP8 alone)
     s = bf16 ? dispatch_fwd_causal<128, true>(causal, mq, mk, mv, p, sms, st)
              : dispatch_fwd_causal<128, false>(causal, mq, mk, mv, p, sms, st);
+#else
+    s = fail(FA2_ERR_UNSUPPORTED, "internal: d = 128 forward not routed to the pair kernel");
+#endif
   return s;
 }
 
