@@ -230,8 +230,9 @@ FA2_API fa2_status_t fa2_attention_step_host(const void* q_h, const void* k_h, c
 FA2_API fa2_status_t fa2_kv_block_range(int N, int Br, int Bc, int i, int causal, int* n_blocks, int* first_masked);
 
 /* Host-side balanced tile schedule (no GPU needed) that the causal square-length
- * forward (`pass` = 0) and arrival-order backward (`pass` = 1) launches pass to
- * their kernels (the row-block loops of Alg. 1/2, P:345-351,
+ * one-SM forward (`pass` = 0) and arrival-order backward (`pass` = 1) launches (d = 64)
+ * pass to their kernels; the d = 128 CTA-pair kernels use per-pair lists built by the same
+ * greedy assignment over 512-row / 256-key-row pair tiles (the row-block loops of Alg. 1/2, P:345-351,
  * P:421-436, with the causal skip of P:378-386 making tiles unequal).
  *   heads: B * H query heads (forward) or B * H_kv * hsplit work heads (backward)
  *   N: sequence length; heads_per_tile: query heads one backward tile visits
