@@ -383,7 +383,7 @@ SchedPtr fwd_pair_sched(const fa2::FwdParams& p, int npairs) {
 // CTA-pair forward (fa2_fwd2_sm100.cuh): square fixed-length, d = 128, bf16/fp16
 template <bool BF16, bool CAUSAL, bool GEN>
 fa2_status_t launch_fwd_pair(const CUtensorMap& mq, const CUtensorMap& mk64, const CUtensorMap& mv,
-                             fa2::FwdParams p, int sms, cudaStream_t st) {
+                             const CUtensorMap& mo, fa2::FwdParams p, int sms, cudaStream_t st) {
   auto kern = fa2::fa2_fwd_pair_kernel<BF16, CAUSAL, GEN>;
   constexpr int smem = fa2::FwdPairSmem::ALLOC;
   fa2_status_t s = set_smem(kern, smem);
@@ -400,7 +400,7 @@ fa2_status_t launch_fwd_pair(const CUtensorMap& mq, const CUtensorMap& mk64, con
     if (FA2_SCHED && p.num_tiles <= fa2::kSchedMaxTiles && grid / 2 <= fa2::kSchedMaxCtas) {
       const SchedPtr sc = fwd_pair_sched(p, grid / 2);
       mark(0, st);
-      kern<<<grid, 384, smem, st>>>(mq, mk64, mv, p, *sc);
+      kern<<<grid, 384, smem, st>>>(mq, mk64, mv, mo, p, *sc);
       mark(1, st);
       FA2_CUDA(cudaGetLastError());
       return FA2_OK;
@@ -409,7 +409,7 @@ fa2_status_t launch_fwd_pair(const CUtensorMap& mq, const CUtensorMap& mk64, con
   fa2::SchedT<CAUSAL && !GEN> sched;
   sched.n = 0;
   mark(0, st);
-  kern<<<grid, 384, smem, st>>>(mq, mk64, mv, p, sched);
+  kern<<<grid, 384, smem, st>>>(mq, mk64, mv, mo, p, sched);
   mark(1, st);
   FA2_CUDA(cudaGetLastError());
   return FA2_OK;
@@ -447,12 +447,15 @@ fa2_status_t forward_impl(const void* q, const void* k, const void* v, void* o, 
   p.trace = g_trace;
   const bool bf16 = dtype == FA2_BF16;
   if (pair) {
+    // O as a TMA store target (fixed layout; the packed layout stores rows one by one)
+    CUtensorMap mo = mq;
+    if (!g.packed && (s = make_rows_map(&mo, o, dt, g, g.H, true)) != FA2_OK) return s;
     if (g.packed) {
-      if (causal) return bf16 ? launch_fwd_pair<true, true, true>(mq, mk, mv, p, sms, st) : launch_fwd_pair<false, true, true>(mq, mk, mv, p, sms, st);
-      return bf16 ? launch_fwd_pair<true, false, true>(mq, mk, mv, p, sms, st) : launch_fwd_pair<false, false, true>(mq, mk, mv, p, sms, st);
+      if (causal) return bf16 ? launch_fwd_pair<true, true, true>(mq, mk, mv, mo, p, sms, st) : launch_fwd_pair<false, true, true>(mq, mk, mv, mo, p, sms, st);
+      return bf16 ? launch_fwd_pair<true, false, true>(mq, mk, mv, mo, p, sms, st) : launch_fwd_pair<false, false, true>(mq, mk, mv, mo, p, sms, st);
     }
-    if (causal) return bf16 ? launch_fwd_pair<true, true, false>(mq, mk, mv, p, sms, st) : launch_fwd_pair<false, true, false>(mq, mk, mv, p, sms, st);
-    return bf16 ? launch_fwd_pair<true, false, false>(mq, mk, mv, p, sms, st) : launch_fwd_pair<false, false, false>(mq, mk, mv, p, sms, st);
+    if (causal) return bf16 ? launch_fwd_pair<true, true, false>(mq, mk, mv, mo, p, sms, st) : launch_fwd_pair<false, true, false>(mq, mk, mv, mo, p, sms, st);
+    return bf16 ? launch_fwd_pair<true, false, false>(mq, mk, mv, mo, p, sms, st) : launch_fwd_pair<false, false, false>(mq, mk, mv, mo, p, sms, st);
   }
   if (g.d == 64)
     s = bf16 ? dispatch_fwd_causal<64, true>(causal, mq, mk, mv, p, sms, st)

@@ -91,7 +91,8 @@ struct FwdPairSmem {
 template <bool BF16, bool CAUSAL, bool GEN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k64,
-                    const __grid_constant__ CUtensorMap tm_v, const FwdParams p,
+                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+                    const FwdParams p,
                     const __grid_constant__ SchedT<CAUSAL && !GEN> sched) {
   using L = FwdPairSmem;
   constexpr int D = 128, STAGES = L::STAGES;
@@ -234,29 +235,54 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
       }
       // ---- epilogue: O = O / l, L = m + log l ----
       auto epilogue = [&]() {
+        if (threadIdx.x % 128 == 0) fa2_tile_trace(p.trace, tn, wg, 7, clock64());   // epilogue start
         ptx::mbar_wait(&o_done[wg], (pv_count - 1) & 1);
         ptx::tc_fence_after();
         const float inv_l = l_sum > 0.f ? 1.f / l_sum : 0.f;
-        uint8_t* orow = reinterpret_cast<uint8_t*>(p.o) + o_off * 2;
+        uint32_t q[4][16];
 #pragma unroll
         for (int ch = 0; ch < D / 32; ++ch) {
           uint32_t o[32];
           ptx::tmem_ld_x32(tO + ch * 32, o);
           ptx::tmem_wait_ld();
-          uint32_t q[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e)
-            q[e] = ptx::pack2<BF16>(__uint_as_float(o[2 * e]) * inv_l, __uint_as_float(o[2 * e + 1]) * inv_l);
-          if (grow < nq) {
-            uint4* dst = reinterpret_cast<uint4*>(orow + ch * 64);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) dst[e] = make_uint4(q[4 * e], q[4 * e + 1], q[4 * e + 2], q[4 * e + 3]);
-          }
+            q[ch][e] = ptx::pack2<BF16>(__uint_as_float(o[2 * e]) * inv_l, __uint_as_float(o[2 * e + 1]) * inv_l);
         }
-        if (grow < nq) p.lse[l_off] = l_sum > 0.f ? (m_used + ptx::lg2(l_sum)) * 0.69314718055994531f : -INFINITY;
+        // O_i has been read out of TMEM: the next tile's first P~V may overwrite it
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) pair::arrive_remote(&o_empty[wg], 0);
+        if (grow < nq) p.lse[l_off] = l_sum > 0.f ? (m_used + ptx::lg2(l_sum)) * 0.69314718055994531f : -INFINITY;
+        if constexpr (!GEN) {
+          // the sub-tile's P~ buffer (free: the last P~V has completed) stages O in the SW128
+          // layout of two 64-column boxes, and one TMA store per box writes the 128 rows (rows
+          // past N_q are clipped by the tensor map)
+#pragma unroll
+          for (int c = 0; c < 16; ++c)
+            ptx::sts_v4(sP_row + (c / 8) * L::Q_BOX + (((c % 8) ^ (row % 8)) * 16), q[c / 4][4 * (c % 4)],
+                        q[c / 4][4 * (c % 4) + 1], q[c / 4][4 * (c % 4) + 2], q[c / 4][4 * (c % 4) + 3]);
+          ptx::fence_proxy_async_smem();
+          ptx::named_bar_sync(3 + wg, 128);
+          if (threadIdx.x % 128 == 0) {
+            ptx::tma_store_3d(&tm_o, sP + wg * L::P_TILE, 0, r0, w.bh);
+            ptx::tma_store_3d(&tm_o, sP + wg * L::P_TILE + L::Q_BOX, 64, r0, w.bh);
+            ptx::bulk_commit();
+            ptx::bulk_wait_read<0>();   // the buffer is read: the next tile's P~ may go there
+          }
+          ptx::named_bar_sync(3 + wg, 128);
+        } else {
+          // packed layout: rows past this sequence belong to the next one, so per-row stores
+          if (grow < nq) {
+            uint8_t* orow = reinterpret_cast<uint8_t*>(p.o) + o_off * 2;
+#pragma unroll
+            for (int ch = 0; ch < D / 32; ++ch) {
+              uint4* dst = reinterpret_cast<uint4*>(orow + ch * 64);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) dst[e] = make_uint4(q[ch][4 * e], q[ch][4 * e + 1], q[ch][4 * e + 2], q[ch][4 * e + 3]);
+            }
+          }
+        }
       };
       if (nb == 0) {   // no row of this sub-tile sees a key (R23): O = 0, L = -inf; no MMA work
         for (int j = 0; j < nkv; ++j) {
@@ -383,6 +409,7 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         fa2_tile_trace(p.trace, tn, wg, 3, clock64());
       }
     }
+    if (!GEN && threadIdx.x % 128 == 0) ptx::bulk_wait<0>();   // the O stores have completed
   } else {
     ptx::setmaxnreg_dec<56>();
     if ((warp == 8 || warp == 11) && rank == 0) {

@@ -128,6 +128,11 @@ FA2_DEVICE void tma_load_3d_hint(void* smem_dst, const CUtensorMap* d, uint64_t*
       :: "r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(d)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+// TMA tensor store shared -> global (rows outside the tensor map's bounds are not written)
+FA2_DEVICE void tma_store_3d(const CUtensorMap* d, const void* smem_src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];"
+               :: "l"(reinterpret_cast<uint64_t>(d)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(smem_src)) : "memory");
+}
 FA2_DEVICE void tma_reduce_add_2d(const CUtensorMap* d, const void* smem_src, int c0, int c1) {
   asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];"
                :: "l"(reinterpret_cast<uint64_t>(d)), "r"(c0), "r"(c1), "r"(smem_u32(smem_src)) : "memory");

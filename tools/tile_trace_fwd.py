@@ -77,3 +77,7 @@ for c in range(148):
     by_tpc.setdefault(int(smid[c]) // 2, []).append(cpb[c])
 print("cyc/blk by smid//16 (GPC-ish):", [round(float(np.mean([cpb[c] for c in range(148) if smid[c] // 16 == gg])))
                                         for gg in range(10) if any(smid[c] // 16 == gg for c in range(148))])
+# pair kernel: clock64 at the epilogue's start (slot 7) -> tile end: epilogue cycles per tile
+ep = np.where(valid & (t[:, :, :, 7] > 0), t[:, :, :, 3].astype(np.float64) - t[:, :, :, 7], np.nan)
+if np.isfinite(ep).any():
+    print("epilogue (last P~V wait + O/L stores) cycles per tile: wg0 %.0f wg1 %.0f" % (np.nanmean(ep[:, :, 0]), np.nanmean(ep[:, :, 1])))
