@@ -675,7 +675,7 @@ fa2_status_t dispatch_bwd_causal(bool causal, const fa2::BwdMaps& maps, const fa
 // tiling; the pair kernel tiles keys by 256.
 template <bool BF16, bool CAUSAL, bool GEN>
 fa2_status_t launch_bwd_pair(const fa2::BwdMaps& maps, const CUtensorMap& mq64, const CUtensorMap& mdo64,
-                             fa2::BwdParams p, int sms, cudaStream_t st) {
+                             const CUtensorMap& mdk, const CUtensorMap& mdv, fa2::BwdParams p, int sms, cudaStream_t st) {
   auto kern = fa2::fa2_bwd_pair_kernel<BF16, CAUSAL, GEN>;
   constexpr int smem = fa2::BwdPairSmem::ALLOC;
   fa2_status_t s = set_smem(kern, smem);
@@ -704,14 +704,14 @@ fa2_status_t launch_bwd_pair(const fa2::BwdMaps& maps, const CUtensorMap& mq64, 
         for (int t = 0; t < nt; ++t) work[t] = (nqb - 2 * (t % nnb2)) * nh + 1;
       });
       mark(3, st);
-      kern<<<2 * npairs, fa2::kBwdThreads, smem, st>>>(mq64, maps.q, maps.k, maps.v, mdo64, maps.dout, p, *sc);
+      kern<<<2 * npairs, fa2::kBwdThreads, smem, st>>>(mq64, maps.q, maps.k, maps.v, mdo64, maps.dout, mdk, mdv, p, *sc);
       mark(4, st);
       FA2_CUDA(cudaGetLastError());
       return FA2_OK;
     }
   }
   mark(3, st);
-  kern<<<2 * npairs, fa2::kBwdThreads, smem, st>>>(mq64, maps.q, maps.k, maps.v, mdo64, maps.dout, p, sched);
+  kern<<<2 * npairs, fa2::kBwdThreads, smem, st>>>(mq64, maps.q, maps.k, maps.v, mdo64, maps.dout, mdk, mdv, p, sched);
   mark(4, st);
   FA2_CUDA(cudaGetLastError());
   return FA2_OK;
@@ -814,8 +814,14 @@ fa2_status_t backward_impl(const void* q, const void* k, const void* v, const vo
     CUtensorMap mq64, mdo64;
     if ((s = make_rows_map(&mq64, q, dt, g, g.H, true, 2, 64)) != FA2_OK) return s;
     if ((s = make_rows_map(&mdo64, dout, dt, g, g.H, true, 2, 64)) != FA2_OK) return s;
+    // dK / dV as TMA store targets (fixed layout; the packed one stores rows one by one)
+    CUtensorMap mdk = maps.k, mdv = maps.v;
+    if (!g.packed && hsplit == 1) {
+      if ((s = make_rows_map(&mdk, dk, dt, g, g.Hkv, false)) != FA2_OK) return s;
+      if ((s = make_rows_map(&mdv, dv, dt, g, g.Hkv, false)) != FA2_OK) return s;
+    }
     const bool gen = g.packed || g.Nq != g.Nk;
-#define FA2_PAIR_LAUNCH(B16, C, G) launch_bwd_pair<B16, C, G>(maps, mq64, mdo64, p, sms, st)
+#define FA2_PAIR_LAUNCH(B16, C, G) launch_bwd_pair<B16, C, G>(maps, mq64, mdo64, mdk, mdv, p, sms, st)
     if (gen)
       s = bf16 ? (causal ? FA2_PAIR_LAUNCH(true, true, true) : FA2_PAIR_LAUNCH(true, false, true))
                : (causal ? FA2_PAIR_LAUNCH(false, true, true) : FA2_PAIR_LAUNCH(false, false, true));

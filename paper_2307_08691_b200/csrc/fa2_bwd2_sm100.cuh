@@ -177,6 +177,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBwdThreads, 1)
 fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_constant__ CUtensorMap tm_q128,
                     const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                     const __grid_constant__ CUtensorMap tm_do64, const __grid_constant__ CUtensorMap tm_do128,
+                    const __grid_constant__ CUtensorMap tm_dk, const __grid_constant__ CUtensorMap tm_dv,
                     const BwdParams p, const __grid_constant__ SchedT<CAUSAL && !GEN> sched) {
   using L = BwdPairSmem;
   constexpr int D = 128, BM = 128;
@@ -444,6 +445,7 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
         if (threadIdx.x == 0) FA2_BTRACE(3, g);
       }
       // ---- epilogue: dV_j (warpgroup 0), dK_j * scale (warpgroup 1) ----
+      if (ttr) trow[7] = clock64();   // debug: epilogue start (before the last MMAs' completion wait)
       ptx::mbar_wait(dkv_full, it & 1);
       ptx::tc_fence_after();
       if (p.hsplit > 1) {
@@ -464,6 +466,55 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
                                   __uint_as_float(v[4 * e + 2]) * mul, __uint_as_float(v[4 * e + 3]) * mul);
           }
         }
+      } else if (p.geom.cu_q == nullptr) {
+        // fixed layout: dV (warpgroup 0), then dK (warpgroup 1), packed into the SW128 boxes of
+        // the free own dS slot A_rank (d 0-63) and XS (d 64-127) -- both free once the tile's
+        // last dQ completed, which dkv_full implies -- and written by TMA tensor stores (rows
+        // past N_k are clipped by the tensor map); 16-byte per-row stores took ~7000 cycles
+        const uint32_t tsrc = tmem + lane_base + (wg == 0 ? T_DV : T_DK);
+        const float mul = wg == 0 ? 1.f : p.scale;
+        uint32_t pk[D / 32][16];
+#pragma unroll
+        for (int ch = 0; ch < D / 32; ++ch) {
+          uint32_t v[32];
+          ptx::tmem_ld_x32(tsrc + ch * 32, v);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) pk[ch][e] = ptx::pack2<BF16>(__uint_as_float(v[2 * e]) * mul, __uint_as_float(v[2 * e + 1]) * mul);
+        }
+        // dV / dK are out of TMEM: the next tile's MMAs may overwrite them
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) pair::arrive_remote(dkv_empty, 0);
+        if (wg == 1) ptx::named_bar_sync(7, 256);   // warpgroup 0's stores have read the staging
+        const uint32_t st0 = ptx::smem_u32(sDS) + rank * L::BOX128 + r * 128, st1 = ptx::smem_u32(sXS) + r * 128;
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          ptx::sts_v4((c < 8 ? st0 : st1) + (((c % 8) ^ (r % 8)) * 16), pk[c / 4][4 * (c % 4)], pk[c / 4][4 * (c % 4) + 1],
+                      pk[c / 4][4 * (c % 4) + 2], pk[c / 4][4 * (c % 4) + 3]);
+        ptx::fence_proxy_async_smem();
+        ptx::named_bar_sync(wg == 0 ? 6 : 8, 128);
+        if (r == 0) {
+          const CUtensorMap* m = wg == 0 ? &tm_dv : &tm_dk;
+          const int krow = w.sq.k0 + w.nb2 * 256 + static_cast<int>(rank) * 128, z = w.sq.bc * p.Hkv + w.kvh;
+          ptx::tma_store_3d(m, sDS + rank * L::BOX128, 0, krow, z);
+          ptx::tma_store_3d(m, sXS, 64, krow, z);
+          ptx::bulk_commit();
+          ptx::bulk_wait_read<0>();
+        }
+        ptx::named_bar_sync(wg == 0 ? 6 : 8, 128);
+        if (wg == 0) {
+          ptx::named_bar_arrive(7, 256);
+          ptx::named_bar_sync(9, 256);   // warpgroup 1's stores have read the staging too
+        } else {
+          ptx::named_bar_arrive(9, 256);
+        }
+        if (ttr) {
+          unsigned long long gt; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+          trow[2] = gt; trow[3] = clock64();
+        }
+        ++it;
+        continue;
       } else {
         const uint32_t tsrc = tmem + lane_base + (wg == 0 ? T_DV : T_DK);
         const float mul = wg == 0 ? 1.f : p.scale;
@@ -492,6 +543,7 @@ fa2_bwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q64, const __grid_con
       }
       ++it;
     }
+    if (r == 0) ptx::bulk_wait<0>();   // the dK / dV tensor stores have completed
   } else if (warp < 12) {
     // ====================== dQ read-out + fp32 bulk reduce-add ======================
     // lane L holds query row L % 64 of this CTA's half and d half L / 64 (64 columns); the two

@@ -54,3 +54,6 @@ print(f"cycles = {a:.0f} + {b:.0f} * steps per tile (steps {x.min():.0f}-{x.max(
 gap = t[:, 1:, 0] - t[:, :-1, 2]
 gm = valid[:, 1:] & valid[:, :-1]
 print(f"inter-tile gap: mean {np.mean(gap[gm]) / 1e3:.2f} us")
+ep = np.where(valid & (t[:, :, 7] > 0), t[:, :, 3] - t[:, :, 7], np.nan)
+if np.isfinite(ep).any():
+    print(f"epilogue (last MMAs' wait + dK/dV stores) cycles per tile: {np.nanmean(ep):.0f}")
