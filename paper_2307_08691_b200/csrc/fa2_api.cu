@@ -318,8 +318,8 @@ SchedPtr bwd_sched(const fa2::BwdParams& p, int grid) {
 }
 
 template <int D, bool BF16, bool CAUSAL, bool GEN, bool FP8 = false>
-fa2_status_t launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const fa2::FwdParams& p,
-                        int sms, cudaStream_t st) {
+fa2_status_t launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mo,
+                        const fa2::FwdParams& p, int sms, cudaStream_t st) {
   auto kern = fa2::fa2_fwd_kernel<D, BF16, CAUSAL, GEN, FP8>;
   constexpr int smem = fa2::FwdSmem<D, FP8 ? 1 : 2>::ALLOC;
   fa2_status_t s = set_smem(kern, smem);
@@ -331,14 +331,14 @@ fa2_status_t launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUte
     if (FA2_SCHED && p.num_tiles <= fa2::kSchedMaxTiles && grid <= fa2::kSchedMaxCtas) {
       const SchedPtr sc = fwd_sched(p, grid);
       mark(0, st);
-      kern<<<grid, fa2::FwdCfg<D, FP8>::THREADS, smem, st>>>(mq, mk, mv, p, *sc);
+      kern<<<grid, fa2::FwdCfg<D, FP8>::THREADS, smem, st>>>(mq, mk, mv, mo, p, *sc);
       mark(1, st);
       FA2_CUDA(cudaGetLastError());
       return FA2_OK;
     }
   }
   mark(0, st);
-  kern<<<grid, fa2::FwdCfg<D, FP8>::THREADS, smem, st>>>(mq, mk, mv, p, sched);
+  kern<<<grid, fa2::FwdCfg<D, FP8>::THREADS, smem, st>>>(mq, mk, mv, mo, p, sched);
   mark(1, st);
   FA2_CUDA(cudaGetLastError());
   return FA2_OK;
@@ -346,13 +346,14 @@ fa2_status_t launch_fwd(const CUtensorMap& mq, const CUtensorMap& mk, const CUte
 
 template <int D, bool BF16>
 fa2_status_t dispatch_fwd_causal(bool causal, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                                 const CUtensorMap& mo,
                                  const fa2::FwdParams& p, int sms, cudaStream_t st) {
   // general geometry (packed varlen or N_q != N_k) vs the square fixed-length path
   if (p.geom.cu_q != nullptr || p.geom.Nq != p.geom.Nk)
-    return causal ? launch_fwd<D, BF16, true, true>(mq, mk, mv, p, sms, st)
-                  : launch_fwd<D, BF16, false, true>(mq, mk, mv, p, sms, st);
-  return causal ? launch_fwd<D, BF16, true, false>(mq, mk, mv, p, sms, st)
-                : launch_fwd<D, BF16, false, false>(mq, mk, mv, p, sms, st);
+    return causal ? launch_fwd<D, BF16, true, true>(mq, mk, mv, mo, p, sms, st)
+                  : launch_fwd<D, BF16, false, true>(mq, mk, mv, mo, p, sms, st);
+  return causal ? launch_fwd<D, BF16, true, false>(mq, mk, mv, mo, p, sms, st)
+                : launch_fwd<D, BF16, false, false>(mq, mk, mv, mo, p, sms, st);
 }
 
 #ifndef FA2_FWD_PAIR
@@ -446,10 +447,10 @@ fa2_status_t forward_impl(const void* q, const void* k, const void* v, void* o, 
   p.scale_log2 = scale * 1.4426950408889634f;
   p.trace = g_trace;
   const bool bf16 = dtype == FA2_BF16;
+  // O as a TMA store target (fixed layout; the packed layout stores rows one by one)
+  CUtensorMap mo = mq;
+  if (!g.packed && (s = make_rows_map(&mo, o, dt, g, g.H, true)) != FA2_OK) return s;
   if (pair) {
-    // O as a TMA store target (fixed layout; the packed layout stores rows one by one)
-    CUtensorMap mo = mq;
-    if (!g.packed && (s = make_rows_map(&mo, o, dt, g, g.H, true)) != FA2_OK) return s;
     if (g.packed) {
       if (causal) return bf16 ? launch_fwd_pair<true, true, true>(mq, mk, mv, mo, p, sms, st) : launch_fwd_pair<false, true, true>(mq, mk, mv, mo, p, sms, st);
       return bf16 ? launch_fwd_pair<true, false, true>(mq, mk, mv, mo, p, sms, st) : launch_fwd_pair<false, false, true>(mq, mk, mv, mo, p, sms, st);
@@ -458,14 +459,14 @@ fa2_status_t forward_impl(const void* q, const void* k, const void* v, void* o, 
     return bf16 ? launch_fwd_pair<true, false, false>(mq, mk, mv, mo, p, sms, st) : launch_fwd_pair<false, false, false>(mq, mk, mv, mo, p, sms, st);
   }
   if (g.d == 64)
-    s = bf16 ? dispatch_fwd_causal<64, true>(causal, mq, mk, mv, p, sms, st)
-             : dispatch_fwd_causal<64, false>(causal, mq, mk, mv, p, sms, st);
+    s = bf16 ? dispatch_fwd_causal<64, true>(causal, mq, mk, mv, mo, p, sms, st)
+             : dispatch_fwd_causal<64, false>(causal, mq, mk, mv, mo, p, sms, st);
   else
 #if !FA2_FWD_PAIR || !FA2_FWD_PAIR_CAUSAL
     // (d = 128 on the one-SM kernel: A/B builds without the pair forward only; the product
     // build instantiates it for FP8 alone)
-    s = bf16 ? dispatch_fwd_causal<128, true>(causal, mq, mk, mv, p, sms, st)
-             : dispatch_fwd_causal<128, false>(causal, mq, mk, mv, p, sms, st);
+    s = bf16 ? dispatch_fwd_causal<128, true>(causal, mq, mk, mv, mo, p, sms, st)
+             : dispatch_fwd_causal<128, false>(causal, mq, mk, mv, mo, p, sms, st);
 #else
     s = fail(FA2_ERR_UNSUPPORTED, "internal: d = 128 forward not routed to the pair kernel");
 #endif
@@ -497,8 +498,10 @@ fa2_status_t forward_fp8_impl(const void* q, const void* k, const void* v, void*
   p.scale_log2 = static_cast<float>(static_cast<double>(scale) * dq * dk * 1.4426950408889634);
   p.o_descale = dv;
   p.trace = g_trace;
-  return causal ? launch_fwd<128, true, true, false, true>(mq, mk, mv, p, sms, st)
-                : launch_fwd<128, true, false, false, true>(mq, mk, mv, p, sms, st);
+  CUtensorMap mo;   // O (bf16) as the TMA store target
+  if ((s = make_rows_map(&mo, o, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, g, g.H, true)) != FA2_OK) return s;
+  return causal ? launch_fwd<128, true, true, false, true>(mq, mk, mv, mo, p, sms, st)
+                : launch_fwd<128, true, false, false, true>(mq, mk, mv, mo, p, sms, st);
 }
 
 // Copy streams and events of fa2_attention_step_host, created once per host thread and

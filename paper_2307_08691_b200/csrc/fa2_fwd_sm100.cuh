@@ -126,7 +126,13 @@ struct FwdSmem {
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + 2 * TILE;
   static constexpr int OFF_V = OFF_K + STAGES * TILE;
-  static constexpr int OFF_BAR = OFF_V + STAGES * TILE;
+  // O staging for the TMA-store epilogue (FP8: bf16 O, 128 x 128 per softmax warpgroup).  At
+  // d = 64 the extra 32 KB of shared memory alone cost the non-causal kernel 6% (same-box A/B,
+  // with the per-row store epilogue unchanged), so d = 64 keeps per-row stores.
+  static constexpr bool HAS_OST = (EB == 1);
+  static constexpr int O_TILE = 128 * D * 2;
+  static constexpr int OFF_OST = OFF_V + STAGES * TILE;
+  static constexpr int OFF_BAR = OFF_OST + (HAS_OST ? 2 * O_TILE : 0);
   // barriers: q_full[2] q_empty[2] k_full[S] k_empty[S] v_full[S] v_empty[S] s_full[2] p_full[2][2] o_done[2][2] o_empty[2]
   static constexpr int NBAR = 2 + 2 + 4 * STAGES + 2 + 4 + 4 + 2 + 2;   // + s_consumed[2]
   static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
@@ -140,7 +146,7 @@ struct FwdSmem {
 template <int D, bool BF16, bool CAUSAL, bool GEN, bool FP8 = false>
 __global__ void __launch_bounds__(FwdCfg<D, FP8>::THREADS, 1)
 fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-               const __grid_constant__ CUtensorMap tm_v, const FwdParams p,
+               const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o, const FwdParams p,
                const __grid_constant__ FwdSchedT<CAUSAL, GEN> sched) {
   static_assert(!FP8 || (D == 128 && BF16), "FP8 forward: d = 128, bf16 output");
   using L = FwdSmem<D, FP8 ? 1 : 2>;
@@ -446,31 +452,56 @@ fa2_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       uint8_t* orow = reinterpret_cast<uint8_t*>(p.o) +
                       (GEN ? (sq.bc * p.o_bs + (bh % p.H) * p.o_hs + (sq.q0 + grow) * p.o_rs)
                            : (static_cast<size_t>(bh) * sq.nq + grow) * D) * 2;
+      uint32_t pk[D / 32][16];
 #pragma unroll
       for (int ch = 0; ch < D / 32; ++ch) {
         uint32_t o[32];
         ptx::tmem_ld_x32(tO + ch * 32, o);
         ptx::tmem_wait_ld();
-        uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e)
-          pk[e] = ptx::pack2<BF16>(__uint_as_float(o[2 * e]) * inv_l, __uint_as_float(o[2 * e + 1]) * inv_l);
-        if (grow < sq.nq) {
-          uint4* dst = reinterpret_cast<uint4*>(orow + ch * 64);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) dst[e] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
-        }
+          pk[ch][e] = ptx::pack2<BF16>(__uint_as_float(o[2 * e]) * inv_l, __uint_as_float(o[2 * e + 1]) * inv_l);
       }
-      if (grow < sq.nq)
-        p.lse[GEN ? sq.bc * p.l_bs + (bh % p.H) * p.l_hs + sq.q0 + grow : static_cast<size_t>(bh) * sq.nq + grow] = l_sum > 0.f ? (m_used + ptx::lg2(l_sum)) * 0.69314718055994531f : -INFINITY;
+      // O_i is out of TMEM: the next tile's first P~V may overwrite it
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&o_empty[wg]);
+      if (grow < sq.nq)
+        p.lse[GEN ? sq.bc * p.l_bs + (bh % p.H) * p.l_hs + sq.q0 + grow : static_cast<size_t>(bh) * sq.nq + grow] = l_sum > 0.f ? (m_used + ptx::lg2(l_sum)) * 0.69314718055994531f : -INFINITY;
+      // TMA-store epilogue (FP8; same-box A/B 1442-1471 -> 1504-1529 TFLOP/s non-causal)
+      constexpr bool OST = !GEN && L::HAS_OST;
+      if constexpr (OST) {
+        // staged in SW128 boxes of 64 columns and written by TMA tensor stores (rows past N
+        // clipped by the tensor map)
+        uint8_t* ost = smem + L::OFF_OST + wg * L::O_TILE;
+        const uint32_t ost_row = ptx::smem_u32(ost) + row * 128;
+#pragma unroll
+        for (int c = 0; c < D / 8; ++c)
+          ptx::sts_v4(ost_row + (c / 8) * (128 * 128) + (((c % 8) ^ (row % 8)) * 16), pk[c / 4][4 * (c % 4)],
+                      pk[c / 4][4 * (c % 4) + 1], pk[c / 4][4 * (c % 4) + 2], pk[c / 4][4 * (c % 4) + 3]);
+        ptx::fence_proxy_async_smem();
+        ptx::named_bar_sync(3 + wg, 128);
+        if (row == 0) {
+#pragma unroll
+          for (int bx = 0; bx < D / 64; ++bx) ptx::tma_store_3d(&tm_o, ost + bx * 128 * 128, bx * 64, row0, bh);
+          ptx::bulk_commit();
+          ptx::bulk_wait_read<0>();   // the staging is read: the next tile's epilogue may reuse it
+        }
+        ptx::named_bar_sync(3 + wg, 128);
+      } else if (grow < sq.nq) {
+#pragma unroll
+        for (int ch = 0; ch < D / 32; ++ch) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + ch * 64);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) dst[e] = make_uint4(pk[ch][4 * e], pk[ch][4 * e + 1], pk[ch][4 * e + 2], pk[ch][4 * e + 3]);
+        }
+      }
       if (ttr) {
         fa2_tile_trace(p.trace, n, wg, 2, fa2_gtime());
         fa2_tile_trace(p.trace, n, wg, 3, clock64());
       }
     }
+    if (!GEN && L::HAS_OST && row == 0) ptx::bulk_wait<0>();   // the O tensor stores have completed
   } else {
     ptx::setmaxnreg_dec<CFG::REG_OTHER>();
     if (warp == W_MMA) {
