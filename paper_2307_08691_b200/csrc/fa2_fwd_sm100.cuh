@@ -127,8 +127,8 @@ struct FwdSmem {
   static constexpr int OFF_K = OFF_Q + 2 * TILE;
   static constexpr int OFF_V = OFF_K + STAGES * TILE;
   // O staging for the TMA-store epilogue (FP8: bf16 O, 128 x 128 per softmax warpgroup).  At
-  // d = 64 the extra 32 KB of shared memory alone cost the non-causal kernel 6% (same-box A/B,
-  // with the per-row store epilogue unchanged), so d = 64 keeps per-row stores.
+  // d = 64 the same epilogue measured slower non-causal (792 -> 743 TFLOP/s, same box), so d = 64
+  // keeps per-row stores.
   static constexpr bool HAS_OST = (EB == 1);
   static constexpr int O_TILE = 128 * D * 2;
   static constexpr int OFF_OST = OFF_V + STAGES * TILE;
