@@ -463,7 +463,7 @@ fa2_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
               pair::commit_both(&k_empty[kslot]);
             }
             __syncwarp();
-            if (it == 1) FA2_TRACE(5, i, j + 1);
+            if (it == 1) FA2_TRACE(5, i, j + 1);   // (it counts this pair's tiles, already incremented)
             ++s_iss;
             if (++kslot == STAGES) { kslot = 0; kphase ^= 1; }
           }
